@@ -1,0 +1,137 @@
+/*
+ * bs.h: C ABI of the B200 balanced-sparsity library (libbs.so).
+ *
+ * The library implements the inference hot path of "Balanced Sparsity for Efficient DNN Inference
+ * on GPU" (arXiv 1811.00206; /root/reference/PAPER.md, cited as P:<line>). That path is the product
+ * of a balanced-sparse weight matrix and dense activations:
+ *   - the FC layer Y = W·X + B of Eq. 1, with bias B = 0 as in the analysis;
+ *   - W pruned to Balanced Sparsity: "each matrix row is split into multiple equal-sized blocks and
+ *     each block has the same number of non-zero weights";
+ *   - one block partition's multiply-accumulates go to one thread;
+ *   - x is rearranged in shared memory so that the gathers hit distinct banks.
+ *
+ * Conventions (every entry point):
+ *   - Device pointers are caller-owned (allocated by PyTorch or cudaMalloc). The library never
+ *     allocates device memory and keeps no state beyond a per-device property cache.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream). Every device call
+ *     is asynchronous and stream-ordered; none synchronises.
+ *   - Arguments are validated synchronously, before anything is enqueued. A failed check returns a
+ *     status != BS_OK and enqueues nothing. Launch failures return BS_ERR_CUDA. Asynchronous device
+ *     faults surface at the caller's next synchronisation, as usual in CUDA.
+ *   - Inputs must not alias outputs.
+ *   - Results are deterministic: the same inputs give bit-identical outputs. No reduction uses atomics.
+ *   - Storage layouts (canonical, SPMV, SPMM, SP24) are specified in docs/layout.md.
+ *   - Value, x and y dtypes are equal. Accumulation is fp32.
+ */
+#ifndef BS_H_
+#define BS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BS_OK = 0,
+  BS_ERR_ARG = 1,         /* null pointer, k outside [0,B], sparsity outside [0,1), N < 1, bad ld */
+  BS_ERR_SHAPE = 2,       /* K mod B != 0 ("equal-sized blocks"; rejected, not padded), M/K < 1 */
+  BS_ERR_DTYPE = 3,       /* unknown dtype code */
+  BS_ERR_UNSUPPORTED = 4, /* valid but not implemented: B > 65536, SP24 with B != 4 or k != 2, ... */
+  BS_ERR_CUDA = 5         /* a CUDA runtime call or kernel launch failed */
+} bs_status;
+
+typedef enum { BS_F32 = 0, BS_F16 = 1, BS_BF16 = 2 } bs_dtype;
+
+typedef enum { BS_LAYOUT_SPMV = 1, BS_LAYOUT_SPMM = 2, BS_LAYOUT_SP24 = 3 } bs_layout;
+
+/* A packed balanced-sparse matrix: M×K, blocks of width `block`, `k` kept per block, values of
+ * dtype `dt`, stored in `layout` at device pointer `packed` (bs_packed_bytes bytes). */
+typedef struct {
+  int64_t M, K;
+  int32_t block, k;
+  int32_t dt;      /* bs_dtype */
+  int32_t layout;  /* bs_layout */
+  const void* packed;
+} bs_matrix;
+
+/* ---------------------------------------------------------------- host helpers (pure, sync) */
+
+/* Kept entries per block for a nominal sparsity s: k = lround((1 - s) * block), computed in IEEE
+ * double with round-half-away-from-zero. Alg. 1 zeros "a fraction of weights with smallest absolute
+ * magnitudes", and every block keeps the same count. The rounding rule is
+ * SURVEY reading A1, pinned by P:95 (4, 0.5 -> 2), P:409 (32, 0.9 -> 3) and P:380 (32, 0.875 -> 4).
+ * Returns -1 if block < 1 or s is outside [0, 1). */
+int bs_k_from_sparsity(int block, double sparsity);
+
+/* Bytes of a packed buffer in `layout` (docs/layout.md). Returns 0 on invalid arguments. */
+size_t bs_packed_bytes(int64_t M, int64_t K, int block, int k, int dt, int layout);
+
+/* Human-readable status name. */
+const char* bs_status_str(int status);
+
+/* Library build string: compile target and version. */
+const char* bs_version(void);
+
+/* ---------------------------------------------------------------- device work (async) */
+
+/* bs_prune_k: one balance-aware pruning step (Alg. 1 inner loop, with the count-based
+ * reading A2 that guarantees P:94's "same number of non-zero weights"). For every row r and block b
+ * it keeps the k entries of W[r][b·B .. b·B+B) with the largest magnitude (ties -> lower offset,
+ * NaN above Inf; docs/layout.md "Canonical form").
+ *   W     device, M×K of dtype dt, row-major, leading dimension ldw >= K elements
+ *   vals  device out, [M][K/B][k] of dt: bit copies of the kept weights
+ *   idx   device out, [M][K/B][k] of uint16: kept block-local offsets, ascending
+ * Errors: BS_ERR_SHAPE if K mod B != 0; BS_ERR_ARG if k not in [0,B] or ldw < K or a pointer is NULL
+ * (vals/idx may be NULL only when k == 0); BS_ERR_UNSUPPORTED if B > 65536. */
+int bs_prune_k(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block, int k,
+               void* vals, uint16_t* idx, void* stream);
+
+/* bs_prune: bs_prune_k with k = bs_k_from_sparsity(block, sparsity). The k used is written to
+ * *k_out (a host int; may be NULL). BS_ERR_ARG if sparsity is outside [0,1). */
+int bs_prune(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block, double sparsity,
+             int* k_out, void* vals, uint16_t* idx, void* stream);
+
+/* bs_pack: permute canonical (vals, idx) into the device layout `layout` and narrow the indices
+ * (docs/layout.md). This is a pure permutation, so the output is byte-exact. The paper stores "the
+ * same number of non-zero values in each block partition", so the format needs no row
+ * pointers. `packed` receives bs_packed_bytes(...) bytes; alignment padding bytes are zeroed.
+ * Errors: as bs_prune_k; BS_ERR_UNSUPPORTED for SP24 unless block == 4, k == 2 and K mod 8 == 0. */
+int bs_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int block, int k, int dt,
+            int layout, void* packed, void* stream);
+
+/* bs_unpack: the inverse of bs_pack (used by tests: unpack(pack(c)) == c). */
+int bs_unpack(const void* packed, int64_t M, int64_t K, int block, int k, int dt, int layout,
+              void* vals, uint16_t* idx, void* stream);
+
+/* bs_spmv: y = W_bs · x (Eq. 1, with B = 0; batch 1). A must be in layout SPMV or SPMM.
+ *   x  device, K elements of A->dt;  y  device out, M elements of A->dt.
+ * Products are exact in fp32 for f16/bf16, and accumulation is fp32 in a fixed order that does not
+ * depend on the row range (so row-sharded results are bit-identical). y is rounded to nearest even.
+ * Errors: BS_ERR_ARG for NULL pointers or a bad descriptor; BS_ERR_UNSUPPORTED for an unsupported
+ * layout. */
+int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream);
+
+/* bs_spmv_host: the same product with HOST x and y. The call enqueues H2D(x) -> bs_spmv -> D2H(y) on
+ * `stream`, using caller-owned device scratch x_dev (K elements) and y_dev (M elements). x_host and
+ * y_host should be pinned for the copies to be asynchronous. The call does not synchronise: y_host
+ * is valid after the stream is synchronised. */
+int bs_spmv_host(const bs_matrix* A, const void* x_host, void* y_host, void* x_dev, void* y_dev,
+                 void* stream);
+
+/* bs_spmm: Y = W_bs · X for a batch of N columns (Fig. `benchmark`(b), "batchsize = 8").
+ *   X  device, column n at X + n·ldx (K elements each), i.e. torch [N, K] with row stride ldx
+ *   Y  device out, column n at Y + n·ldy (M elements each), i.e. torch [N, M]
+ * A must be in layout SPMM or SPMV. Column n of Y depends only on column n of X, with an order of
+ * fp32 accumulation that does not depend on N or on the position of the column in the batch. So
+ * batch-sharded SpMM reproduces the unsharded columns bit for bit.
+ * Errors: BS_ERR_ARG if N < 1, ldx < K or ldy < M. */
+int bs_spmm(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, void* Y, int64_t ldy,
+            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BS_H_ */

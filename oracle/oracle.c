@@ -1,0 +1,345 @@
+/*
+ * oracle.c: fp64 CPU ORACLE for balanced sparsity (arXiv 1811.00206).
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library. The product path (paper_1811_00206_b200) never
+ * imports, links or executes it, and this file shares no code, header, table or constant generator
+ * with the CUDA library. The only thing the two share is the seeded input generator (synth/), which
+ * holds none of the method's arithmetic.
+ *
+ * Everything here is plain, slow and single-threaded. It follows the paper's definitions:
+ *   - Balanced Sparsity pattern: "each matrix row is split into multiple equal-sized blocks
+ *     and each block has the same number of non-zero weights".
+ *   - One pruning step, Alg. 1 inner loop: "sorts the weights in each block by
+ *     their absolute magnitude and then zeros out a fraction of weights with smallest absolute
+ *     magnitudes". Implemented literally: a stable sort of each block by magnitude, then keep the
+ *     first k. This is the count-based reading: ties go to the lower offset, and a
+ *     NaN ranks above +Inf with all NaNs equal (A17).
+ *   - k = lround((1 - s) * B).
+ *   - The FC layer Y = W·X + B with B = 0 (Eq. 1), summed in fp64:
+ *     y_r = sum_c W_bs[r][c] * x_c.
+ *   - The SPMV/SPMM/SP24 byte layouts, written from docs/layout.md (not from kernel code).
+ *
+ * Half-precision decoding is written out from the IEEE 754 binary16 and bfloat16 definitions.
+ *
+ * Parity pinning: every function here is pinned by tests/test_oracle_pins.py against values the
+ * paper prints, SPEC worked examples, closed forms, brute force on tiny inputs,
+ * and special cases that reduce to textbook routines. See DESIGN.md §3.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_F32 0
+#define ORC_F16 1
+#define ORC_BF16 2
+
+#define ORC_SPMV 1
+#define ORC_SPMM 2
+#define ORC_SP24 3
+
+/* ------------------------------------------------------------------ element decoding */
+
+/* IEEE 754 binary16: 1 sign, 5 exponent (bias 15), 10 fraction bits. */
+static double half_to_double(uint16_t h) {
+  int sign = (h >> 15) & 1;
+  int e = (h >> 10) & 0x1f;
+  int f = h & 0x3ff;
+  double v;
+  if (e == 0)
+    v = ldexp((double)f, -24); /* subnormal: f * 2^-14 * 2^-10 */
+  else if (e == 31)
+    v = f ? NAN : INFINITY;
+  else
+    v = ldexp((double)(f + 1024), e - 25); /* (1 + f/1024) * 2^(e-15) */
+  return sign ? -v : v;
+}
+
+/* bfloat16 is the high half of an IEEE 754 binary32. */
+static double bf16_to_double(uint16_t h) {
+  uint32_t u = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return (double)f;
+}
+
+static double f32_to_double(const void* p) {
+  float f;
+  memcpy(&f, p, 4);
+  return (double)f;
+}
+
+static int dtype_size(int dt) { return dt == ORC_F32 ? 4 : 2; }
+
+/* Element i of an array of dtype dt, converted exactly to double. */
+double orc_elem(const void* base, int dt, int64_t i) {
+  const unsigned char* p = (const unsigned char*)base + i * dtype_size(dt);
+  if (dt == ORC_F32) return f32_to_double(p);
+  uint16_t h;
+  memcpy(&h, p, 2);
+  return dt == ORC_F16 ? half_to_double(h) : bf16_to_double(h);
+}
+
+/* ------------------------------------------------------------------ k */
+
+int orc_k_from_sparsity(int B, double s) {
+  if (B < 1 || !(s >= 0.0) || !(s < 1.0)) return -1;
+  return (int)lround((1.0 - s) * (double)B);
+}
+
+/* ------------------------------------------------------------------ pruning (Alg. 1 step) */
+
+/* "a ranks above b" in magnitude: NaN above everything else, all NaNs equal; otherwise |a| > |b|. */
+static int mag_above(double a, double b) {
+  if (isnan(a)) return !isnan(b);
+  if (isnan(b)) return 0;
+  return fabs(a) > fabs(b);
+}
+
+/* One balance-aware pruning step over W (M×K, leading dim ldw, dtype dt).
+ * Output: canonical vals[M][NB][k] (dtype dt, bit copies) and idx[M][NB][k] (ascending offsets).
+ * Returns 0, or -1 on a shape or argument error. */
+int orc_prune(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int B, int k, void* vals,
+              uint16_t* idx) {
+  if (M < 1 || K < 1 || B < 1 || K % B != 0 || k < 0 || k > B || ldw < K) return -1;
+  int64_t NB = K / B;
+  int es = dtype_size(dt);
+  int* order = (int*)malloc(sizeof(int) * (size_t)B);
+  double* mag = (double*)malloc(sizeof(double) * (size_t)B);
+  for (int64_t r = 0; r < M; ++r) {
+    for (int64_t b = 0; b < NB; ++b) {
+      int64_t c0 = r * ldw + b * B;
+      for (int j = 0; j < B; ++j) {
+        mag[j] = orc_elem(W, dt, c0 + j);
+        order[j] = j;
+      }
+      /* stable insertion sort of offsets by magnitude, largest first: an element moves before
+       * its predecessor only if it ranks strictly above it, so equal keys keep ascending offsets */
+      for (int i = 1; i < B; ++i) {
+        int cur = order[i];
+        int j = i - 1;
+        while (j >= 0 && mag_above(mag[cur], mag[order[j]])) {
+          order[j + 1] = order[j];
+          --j;
+        }
+        order[j + 1] = cur;
+      }
+      /* keep the first k; emit them in ascending offset order (insertion sort again) */
+      for (int i = 1; i < k; ++i) {
+        int cur = order[i];
+        int j = i - 1;
+        while (j >= 0 && order[j] > cur) {
+          order[j + 1] = order[j];
+          --j;
+        }
+        order[j + 1] = cur;
+      }
+      for (int t = 0; t < k; ++t) {
+        int64_t pos = (r * NB + b) * k + t;
+        idx[pos] = (uint16_t)order[t];
+        memcpy((unsigned char*)vals + pos * es, (const unsigned char*)W + (c0 + order[t]) * es, es);
+      }
+    }
+  }
+  free(order);
+  free(mag);
+  return 0;
+}
+
+/* W_bs as a dense fp64 M×K matrix: kept values at (r, b·B + idx), zeros elsewhere. */
+int orc_decode(const void* vals, const uint16_t* idx, int dt, int64_t M, int64_t K, int B, int k,
+               double* Wd) {
+  if (K % B != 0) return -1;
+  int64_t NB = K / B;
+  memset(Wd, 0, sizeof(double) * (size_t)(M * K));
+  for (int64_t r = 0; r < M; ++r)
+    for (int64_t b = 0; b < NB; ++b)
+      for (int t = 0; t < k; ++t) {
+        int64_t pos = (r * NB + b) * k + t;
+        Wd[r * K + b * B + idx[pos]] = orc_elem(vals, dt, pos);
+      }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ layouts (docs/layout.md) */
+
+static int64_t align256(int64_t n) { return (n + 255) / 256 * 256; }
+
+typedef struct {
+  int64_t V, P, NBf, T;
+  int es, is;                      /* value bytes, index bytes */
+  int64_t offVA, offVB, offIA, offIB, total;
+} orc_geom;
+
+static int geom(int64_t M, int64_t K, int B, int k, int dt, int layout, orc_geom* g) {
+  if (M < 1 || K < 1 || B < 1 || K % B != 0 || k < 0 || k > B) return -1;
+  if (dt != ORC_F32 && dt != ORC_F16 && dt != ORC_BF16) return -1;
+  int64_t NB = K / B;
+  g->es = dtype_size(dt);
+  g->is = B <= 256 ? 1 : 2;
+  if (layout == ORC_SPMV || layout == ORC_SPMM) {
+    int64_t vmax = layout == ORC_SPMM ? 1 : 16 / g->es;
+    int64_t V = 1;
+    while (V * 2 <= vmax && 32 * V * 2 <= NB) V *= 2;
+    g->V = V;
+    g->P = 32 * V;
+    g->NBf = NB / g->P;
+    g->T = NB - g->NBf * g->P;
+    int64_t nA = M * g->NBf * g->P * k, nB = M * g->T * k;
+    g->offVA = 0;
+    g->offVB = g->offVA + align256(nA * g->es);
+    g->offIA = g->offVB + align256(nB * g->es);
+    g->offIB = g->offIA + align256(nA * g->is);
+    g->total = g->offIB + align256(nB * g->is);
+    return 0;
+  }
+  if (layout == ORC_SP24) {
+    if (B != 4 || k != 2 || K % 8 != 0) return -1;
+    g->V = g->P = g->NBf = g->T = 0;
+    g->offVA = 0;
+    g->offIA = align256(M * (K / 2) * g->es);
+    g->offVB = g->offIB = 0;
+    g->total = g->offIA + align256(M * (NB / 2));
+    return 0;
+  }
+  return -1;
+}
+
+size_t orc_packed_bytes(int64_t M, int64_t K, int B, int k, int dt, int layout) {
+  orc_geom g;
+  if (geom(M, K, B, k, dt, layout, &g)) return 0;
+  return (size_t)g.total;
+}
+
+static void put_index(unsigned char* dst, int is, uint16_t v) {
+  dst[0] = (unsigned char)(v & 0xff);
+  if (is == 2) dst[1] = (unsigned char)(v >> 8);
+}
+
+/* Reference permutation pi_L(canonical) -> packed bytes. Padding bytes are zero. */
+int orc_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int B, int k, int dt,
+             int layout, void* packed) {
+  orc_geom g;
+  if (geom(M, K, B, k, dt, layout, &g)) return -1;
+  int64_t NB = K / B;
+  unsigned char* out = (unsigned char*)packed;
+  const unsigned char* in = (const unsigned char*)vals;
+  memset(out, 0, (size_t)g.total);
+  if (layout == ORC_SP24) {
+    for (int64_t r = 0; r < M; ++r)
+      for (int64_t b = 0; b < NB; ++b) {
+        int64_t pos = (r * NB + b) * 2;
+        memcpy(out + g.offVA + pos * g.es, in + pos * g.es, 2 * g.es);
+        int nib = idx[pos] | (idx[pos + 1] << 2);
+        out[g.offIA + r * (NB / 2) + b / 2] |= (unsigned char)(nib << (4 * (b % 2)));
+      }
+    return 0;
+  }
+  for (int64_t r = 0; r < M; ++r) {
+    /* full panels: element (r, p, t, l, v) <- canonical (r, b = p*P + v*32 + l, t) */
+    for (int64_t p = 0; p < g.NBf; ++p)
+      for (int t = 0; t < k; ++t)
+        for (int l = 0; l < 32; ++l)
+          for (int64_t v = 0; v < g.V; ++v) {
+            int64_t b = p * g.P + v * 32 + l;
+            int64_t src = (r * NB + b) * k + t;
+            int64_t dst = ((r * g.NBf + p) * k + t) * g.P + l * g.V + v;
+            memcpy(out + g.offVA + dst * g.es, in + src * g.es, g.es);
+            put_index(out + g.offIA + dst * g.is, g.is, idx[src]);
+          }
+    /* tail: element (r, t, v, l) <- canonical (r, b = NBf*P + v*32 + l, t), for v*32 + l < T */
+    for (int t = 0; t < k; ++t)
+      for (int64_t v = 0; v * 32 < g.T; ++v)
+        for (int l = 0; l < 32; ++l) {
+          if (v * 32 + l >= g.T) continue;
+          int64_t b = g.NBf * g.P + v * 32 + l;
+          int64_t src = (r * NB + b) * k + t;
+          int64_t dst = (r * k + t) * g.T + v * 32 + l;
+          memcpy(out + g.offVB + dst * g.es, in + src * g.es, g.es);
+          put_index(out + g.offIB + dst * g.is, g.is, idx[src]);
+        }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ products (Eq. 1, B = 0) */
+
+/* Sparse-form SpMV over canonical arrays, fp64, restricted to `nrows` listed rows:
+ * for each listed row r (rows[i]; or row i when rows == NULL),
+ *   y[i]     = sum over b, t of vals[r][b][t] * x[b*B + idx[r][b][t]]
+ *   bound[i] = sum over b, t of |vals[r][b][t]| * |x[...]|   (the tolerance scale of O-7)
+ * The sum over canonical entries equals the dense-masked sum over columns because every other
+ * column of W_bs is zero. */
+int orc_spmv_rows(const void* vals, const uint16_t* idx, int dt, int64_t M, int64_t K, int B, int k,
+                  const void* x, const int64_t* rows, int64_t nrows, double* y, double* bound) {
+  if (K % B != 0) return -1;
+  int64_t NB = K / B;
+  for (int64_t i = 0; i < nrows; ++i) {
+    int64_t r = rows ? rows[i] : i;
+    if (r < 0 || r >= M) return -1;
+    double acc = 0.0, mag = 0.0;
+    for (int64_t b = 0; b < NB; ++b)
+      for (int t = 0; t < k; ++t) {
+        int64_t pos = (r * NB + b) * k + t;
+        double w = orc_elem(vals, dt, pos);
+        double xv = orc_elem(x, dt, b * B + idx[pos]);
+        acc += w * xv;
+        mag += fabs(w) * fabs(xv);
+      }
+    y[i] = acc;
+    if (bound) bound[i] = mag;
+  }
+  return 0;
+}
+
+/* As orc_spmv_rows, but `vals`/`idx` hold ONLY the listed rows (nrows × NB × k, in list order).
+ * This lets the big config's sampled rows be checked without copying the whole matrix to the host. */
+int orc_spmv_rowslice(const void* vals, const uint16_t* idx, int dt, int64_t nrows, int64_t K,
+                      int B, int k, const void* x, double* y, double* bound) {
+  return orc_spmv_rows(vals, idx, dt, nrows, K, B, k, x, NULL, nrows, y, bound);
+}
+
+/* Dense fp64 GEMV y = Wd · x (Wd M×K row-major doubles). This is the "dense-masked W·x" of O-7
+ * when Wd = orc_decode(...). */
+int orc_gemv_dense(const double* Wd, int64_t M, int64_t K, const double* x, double* y) {
+  for (int64_t r = 0; r < M; ++r) {
+    double acc = 0.0;
+    for (int64_t c = 0; c < K; ++c) acc += Wd[r * K + c] * x[c];
+    y[r] = acc;
+  }
+  return 0;
+}
+
+/* SpMM: column n of Y (M doubles at Y + n*M) = SpMV of column n of X (X + n*ldx, dtype dt). */
+int orc_spmm(const void* vals, const uint16_t* idx, int dt, int64_t M, int64_t K, int B, int k,
+             const void* X, int64_t N, int64_t ldx, double* Y, double* bound) {
+  int es = dtype_size(dt);
+  for (int64_t n = 0; n < N; ++n) {
+    const unsigned char* xn = (const unsigned char*)X + n * ldx * es;
+    if (orc_spmv_rows(vals, idx, dt, M, K, B, k, xn, NULL, M, Y + n * M, bound ? bound + n * M : NULL))
+      return -1;
+  }
+  return 0;
+}
+
+/* SpMM restricted to listed rows (for big configs): Y[n*nrows + i] for row rows[i]. */
+int orc_spmm_rows(const void* vals, const uint16_t* idx, int dt, int64_t M, int64_t K, int B, int k,
+                  const void* X, int64_t N, int64_t ldx, const int64_t* rows, int64_t nrows,
+                  double* Y, double* bound) {
+  int es = dtype_size(dt);
+  for (int64_t n = 0; n < N; ++n) {
+    const unsigned char* xn = (const unsigned char*)X + n * ldx * es;
+    if (orc_spmv_rows(vals, idx, dt, M, K, B, k, xn, rows, nrows, Y + n * nrows,
+                      bound ? bound + n * nrows : NULL))
+      return -1;
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ reporting */
+
+/* The paper's ideal inference time: i_time = (d_time - o_time) * (1 - sparsity) + o_time. */
+double orc_ideal_time(double d_time, double o_time, double sparsity) {
+  return (d_time - o_time) * (1.0 - sparsity) + o_time;
+}

@@ -1,0 +1,433 @@
+"""Pins for the fp64 oracle (oracle/oracle.c) against what the paper and the mathematics fix.
+
+These are CPU-only tests. Each pin is chosen so that a plausible mistake in the oracle fails at
+least one of them: a dropped term, a wrong sign or index, a transposed operand, the wrong tie-break
+or the wrong rounding. Citations: P:n = PAPER.md line, S:n = SPEC.md line.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _key(v: float):
+    """Magnitude key of docs/layout.md: NaN above everything (all NaNs equal), else |v|."""
+    return (1, 0.0) if math.isnan(v) else (0, abs(v))
+
+
+# ------------------------------------------------------------------ k (A1)
+
+def test_k_paper_instances():
+    for B, s, k, cite in _gold("paper_k.json")["cases"]:
+        assert oracle.k_from_sparsity(B, s) == k, cite
+
+
+def test_k_invalid():
+    assert oracle.k_from_sparsity(32, 1.0) == -1
+    assert oracle.k_from_sparsity(32, -0.1) == -1
+    assert oracle.k_from_sparsity(0, 0.5) == -1
+    assert oracle.k_from_sparsity(32, float("nan")) == -1
+    assert oracle.k_from_sparsity(32, 0.0) == 32
+
+
+# ------------------------------------------------------------------ prune (Alg. 1 step)
+
+def test_prune_spec_example_S143():
+    g = _gold("spec_examples.json")["prune_S143"]
+    W = np.array([g["row"]], dtype=np.float32)
+    k = oracle.k_from_sparsity(g["block"], g["sparsity"])
+    vals, idx = oracle.prune(W, oracle.F32, g["block"], k)
+    assert idx[0].tolist() == g["kept_idx"]
+    np.testing.assert_array_equal(vals[0], np.array(g["kept_vals"], dtype=np.float32))
+
+
+def test_encode_example_S59():
+    g = _gold("spec_examples.json")["encode_S59"]
+    W = np.array([g["row"]], dtype=np.float32)
+    vals, idx = oracle.prune(W, oracle.F32, g["block"], g["k"])
+    assert idx[0].tolist() == g["idx"]
+    assert vals[0].tolist() == g["vals"]
+
+
+def test_prune_fig2_shape():
+    """a 16-wide row in 4 blocks of 4 at 50% leaves 2 per block, and the same split applies to every row."""
+    W = synth.to_numpy(synth.matrix(3, 16, "f32", seed=5))
+    vals, idx = oracle.prune(W, oracle.F32, 4, 2)
+    assert vals.shape == (3, 4, 2) and idx.shape == (3, 4, 2)
+    assert np.all(idx[..., 0] < idx[..., 1])
+
+
+def _brute_force_keep(block_vals, k):
+    """The unique k-subset S with: for kept i and dropped j, key_i > key_j, or key_i == key_j and i < j.
+    Enumerates all C(B, k) subsets (SURVEY §8(c) selection pin (i))."""
+    B = len(block_vals)
+    keys = [_key(float(v)) for v in block_vals]
+    winners = []
+    for S in itertools.combinations(range(B), k):
+        Sset = set(S)
+        ok = True
+        for i in S:
+            for j in range(B):
+                if j in Sset:
+                    continue
+                if keys[i] > keys[j] or (keys[i] == keys[j] and i < j):
+                    continue
+                ok = False
+                break
+            if not ok:
+                break
+        if ok:
+            winners.append(S)
+    assert len(winners) == 1, "exactly one subset must satisfy the ordering"
+    return list(winners[0])
+
+
+@pytest.mark.parametrize("B", [4, 6, 8, 12, 16])
+@pytest.mark.parametrize("family", ["gaussian", "ties"])
+def test_prune_brute_force(B, family):
+    K = 2 * B
+    Wt = synth.matrix(3, K, "f16", family=family, seed=100 + B, B=B)
+    W = synth.to_numpy(Wt)
+    Wd = W.astype(np.float64)
+    for k in range(0, B + 1):
+        vals, idx = oracle.prune(W, oracle.F16, B, k)
+        for r in range(3):
+            for b in range(K // B):
+                want = _brute_force_keep(Wd[r, b * B:(b + 1) * B], k)
+                assert idx[r, b].tolist() == want
+                np.testing.assert_array_equal(vals[r, b].view(np.uint16), W[r, b * B + np.array(want, dtype=int)].view(np.uint16))
+
+
+def _rank_count_keep(W: np.ndarray, B: int, k: int) -> np.ndarray:
+    """Independent vectorised rank count: keep j iff #{i: key_i > key_j} + #{i < j: key_i == key_j} < k.
+    Returns a boolean mask. This is the second oracle of SURVEY §8(c) O-3."""
+    M, K = W.shape
+    x = W.astype(np.float64).reshape(M, K // B, B)
+    nan = np.isnan(x)
+    mag = np.where(nan, np.inf, np.abs(x))
+    tier = nan.astype(np.int8)
+    gt = (tier[..., :, None] > tier[..., None, :]) | ((tier[..., :, None] == tier[..., None, :]) & (mag[..., :, None] > mag[..., None, :]))
+    eq = (tier[..., :, None] == tier[..., None, :]) & ((mag[..., :, None] == mag[..., None, :]) | (nan[..., :, None] & nan[..., None, :]))
+    lower = np.arange(B)[:, None] < np.arange(B)[None, :]  # [i, j]: i < j
+    rank = gt.sum(axis=-2) + (eq & lower).sum(axis=-2)  # count over i for each j
+    return (rank < k).reshape(M, K)
+
+
+def _mask_from_canonical(idx, M, K, B):
+    mask = np.zeros((M, K), dtype=bool)
+    NB = K // B
+    for b in range(NB):
+        cols = b * B + idx[:, b, :].astype(np.int64)
+        np.put_along_axis(mask, cols, True, axis=1) if cols.size else None
+    return mask
+
+
+@pytest.mark.parametrize("dt,dname", [(oracle.F32, "f32"), (oracle.F16, "f16"), (oracle.BF16, "bf16")])
+@pytest.mark.parametrize("B,k", [(16, 8), (32, 3), (32, 1), (32, 16), (4, 2), (25, 8), (64, 7)])
+@pytest.mark.parametrize("family", ["gaussian", "ties"])
+def test_prune_rank_count_agreement(dt, dname, B, k, family):
+    M, K = 24, B * 6
+    W = synth.to_numpy(synth.matrix(M, K, dname, family=family, seed=7 + B + k, B=B))
+    vals, idx = oracle.prune(W, dt, B, k)
+    want = _rank_count_keep(oracle.to_double(W, dt) if dt == oracle.BF16 else W, B, k)
+    got = _mask_from_canonical(idx, M, K, B)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_prune_special_values():
+    """NaN ranks above +Inf, all NaNs tie (lower offset wins), ±0 tie, ±Inf tie."""
+    W = synth.to_numpy(synth.special_block_matrix("f32"))
+    vals, idx = oracle.prune(W, oracle.F32, 16, 4)
+    want = _rank_count_keep(W, 16, 4)
+    np.testing.assert_array_equal(_mask_from_canonical(idx, 4, 32, 16), want)
+    # hand-derived: block (0,0) = [0,-0,1,-1,1,2,-2,.5,-.5,3,nan,.25,-inf,inf,0,1]
+    assert idx[0, 0].tolist() == [9, 10, 12, 13]  # nan, -inf, inf, then 3.0
+    # block (0,1) = [nan,nan,1,nan,-nan,0,0,5,-5,5,inf,-inf,inf,.1,.2,.3] -> the four NaNs
+    assert idx[0, 1].tolist() == [0, 1, 3, 4]
+    # all-equal block keeps offsets 0..k-1 (pin (vii))
+    assert idx[1, 0].tolist() == [0, 1, 2, 3]
+    # ±0 block: all tie -> 0..3
+    assert idx[1, 1].tolist() == [0, 1, 2, 3]
+
+
+def test_prune_rowwise_reduction():
+    """B = K reduces balanced pruning to row-wise magnitude pruning with the same k (BJ.north_star; A8)."""
+    M, K = 16, 96
+    W = synth.to_numpy(synth.matrix(M, K, "f32", seed=11))
+    for s in (0.5, 0.75, 0.9):
+        k = oracle.k_from_sparsity(K, s)
+        vals, idx = oracle.prune(W, oracle.F32, K, k)
+        order = np.argsort(-np.abs(W.astype(np.float64)), axis=1, kind="stable")[:, :k]
+        np.testing.assert_array_equal(idx[:, 0, :], np.sort(order, axis=1))
+
+
+def test_prune_invariants_and_nesting():
+    """Exactly k per block, strictly ascending offsets, nnz = M·NB·k, achieved sparsity = 1 - k/B (A7),
+    per-block optimality, and nesting: kept(k') ⊆ kept(k) for k' ≤ k."""
+    M, K, B = 20, 128, 32
+    W = synth.to_numpy(synth.matrix(M, K, "f16", seed=13))
+    masks = {}
+    for k in range(B + 1):
+        vals, idx = oracle.prune(W, oracle.F16, B, k)
+        assert idx.shape == (M, K // B, k)
+        if k > 1:
+            assert np.all(np.diff(idx.astype(np.int64), axis=-1) > 0)
+        m = _mask_from_canonical(idx, M, K, B)
+        assert m.sum() == M * (K // B) * k
+        assert 1 - m.sum() / (M * K) == pytest.approx(1 - k / B)
+        # optimality: min kept |w| >= max dropped |w| in every block
+        a = np.abs(W.astype(np.float64)).reshape(M, K // B, B)
+        mb = m.reshape(M, K // B, B)
+        if 0 < k < B:
+            assert np.all(np.where(mb, a, np.inf).min(-1) >= np.where(mb, -np.inf, a).max(-1))
+        masks[k] = m
+    for k in range(B):
+        assert np.all(masks[k] <= masks[k + 1])
+
+
+def test_prune_sign_invariance():
+    M, K, B = 8, 64, 16
+    W = synth.to_numpy(synth.matrix(M, K, "f32", seed=17))
+    v1, i1 = oracle.prune(W, oracle.F32, B, 5)
+    v2, i2 = oracle.prune(-W, oracle.F32, B, 5)
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_array_equal(v1, -v2)
+
+
+def test_prune_rejects_bad_shapes():
+    W = np.zeros((2, 30), dtype=np.float32)
+    with pytest.raises(ValueError):
+        oracle.prune(W, oracle.F32, 16, 4)  # 30 mod 16 != 0
+    with pytest.raises(ValueError):
+        oracle.prune(np.zeros((2, 32), np.float32), oracle.F32, 16, 17)
+
+
+# ------------------------------------------------------------------ element decoding
+
+def test_half_decoder_all_patterns():
+    """The oracle's own binary16 decoder agrees with numpy on all 65536 bit patterns (NaN as NaN)."""
+    bits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    want = bits.view(np.float16).astype(np.float64)
+    got = oracle.to_double(bits.view(np.float16), oracle.F16)
+    both_nan = np.isnan(want) & np.isnan(got)
+    assert np.all(both_nan | (want == got))
+    assert np.all(np.signbit(want[~np.isnan(want)]) == np.signbit(got[~np.isnan(want)]))
+
+
+def test_bf16_decoder_sample():
+    bits = np.arange(0, 65536, 7, dtype=np.uint32).astype(np.uint16)
+    want = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).to(torch.float64).numpy()
+    got = oracle.to_double(bits, oracle.BF16)
+    assert np.all((np.isnan(want) & np.isnan(got)) | (want == got))
+
+
+# ------------------------------------------------------------------ pack (docs/layout.md)
+
+def test_packed_bytes_closed_form():
+    """fc6 4096x25088, f16, B=32, k=3: every region is 256-aligned, so bytes = 3·nnz exactly."""
+    nnz = 4096 * 784 * 3
+    assert oracle.packed_bytes(4096, 25088, 32, 3, oracle.F16, oracle.SPMV) == 3 * nnz == 28901376
+    assert oracle.packed_bytes(4096, 25088, 32, 3, oracle.F32, oracle.SPMV) == 5 * nnz
+    # 65536², 90%: 402,653,184 nnz -> 1,207,959,552 bytes (f16 + u8)
+    assert oracle.packed_bytes(65536, 65536, 32, 3, oracle.F16, oracle.SPMV) == 3 * 65536 * 2048 * 3
+    # B > 256 -> u16 indices: 4 B per nnz at f16
+    assert oracle.packed_bytes(64, 1024, 512, 8, oracle.F16, oracle.SPMV) == 4 * 64 * 2 * 8
+    # SP24: K/2 values + K/8 metadata bytes per row
+    assert oracle.packed_bytes(4096, 2048, 4, 2, oracle.F16, oracle.SP24) == 4096 * 1024 * 2 + 4096 * 256
+    assert oracle.packed_bytes(4, 30, 4, 2, oracle.F16, oracle.SPMV) == 0  # 30 mod 4 != 0
+    assert oracle.packed_bytes(4, 32, 8, 2, oracle.F16, oracle.SP24) == 0  # SP24 needs B=4,k=2
+
+
+def test_pack_spmv_transpose_closed_form():
+    """B=1, k=1, K=96, f16: NB=96 -> V=2, P=64, one full panel + a 32-block tail. The panel is the
+    32×2 transpose of blocks 0..63 (lane l holds blocks l and 32+l); the tail is blocks 64..95 in order."""
+    K = 96
+    vals = np.arange(K, dtype=np.float16).reshape(1, K, 1)
+    idx = np.zeros((1, K, 1), dtype=np.uint16)
+    buf = oracle.pack(vals, idx, 1, K, 1, 1, oracle.F16, oracle.SPMV)
+    va = buf[:128].view(np.float16)
+    np.testing.assert_array_equal(va, np.arange(64, dtype=np.float16).reshape(2, 32).T.reshape(-1))
+    vb = buf[256:256 + 64].view(np.float16)
+    np.testing.assert_array_equal(vb, np.arange(64, 96, dtype=np.float16))
+
+
+def test_pack_spmv_steps_closed_form():
+    """f32, B=2, k=2 (dense), K=256: NB=128 -> V=4, P=128, one panel, T=0. The step t holds the t-th entry of
+    every block, with lane l owning blocks l, 32+l, 64+l, 96+l (a 4×32 -> 32×4 transpose)."""
+    K, B, k = 256, 2, 2
+    blk = np.arange(128)
+    vals = np.stack([blk * 10 + 0, blk * 10 + 1], axis=-1).astype(np.float32).reshape(1, 128, 2)
+    idx = np.tile(np.array([0, 1], dtype=np.uint16), (1, 128, 1))
+    buf = oracle.pack(vals, idx, 1, K, B, k, oracle.F32, oracle.SPMV)
+    va = buf[:128 * 2 * 4].view(np.float32).reshape(2, 128)
+    for t in range(2):
+        want = (blk.reshape(4, 32).T.reshape(-1) * 10 + t).astype(np.float32)
+        np.testing.assert_array_equal(va[t], want)
+    ia = buf[1024:1024 + 256]
+    np.testing.assert_array_equal(ia.reshape(2, 128), np.array([[0] * 128, [1] * 128], dtype=np.uint8))
+
+
+@pytest.mark.parametrize("layout", [oracle.SPMV, oracle.SPMM])
+@pytest.mark.parametrize("M,K,B,k,dt,dname", [(5, 3008, 32, 3, oracle.F16, "f16"), (3, 1024, 16, 8, oracle.F32, "f32"),
+                                               (2, 2048, 512, 9, oracle.BF16, "bf16"), (4, 64, 4, 2, oracle.F16, "f16")])
+def test_pack_is_a_permutation(layout, M, K, B, k, dt, dname):
+    """The packed value+index pairs are exactly the canonical multiset (no entry lost or duplicated)."""
+    W = synth.to_numpy(synth.matrix(M, K, dname, seed=21))
+    vals, idx = oracle.prune(W, dt, B, k)
+    buf = oracle.pack(vals, idx, M, K, B, k, dt, layout)
+    es = 4 if dt == oracle.F32 else 2
+    isz = 1 if B <= 256 else 2
+    n = M * (K // B) * k
+    NB = K // B
+    vmax = 1 if layout == oracle.SPMM else 16 // es
+    V = 1
+    while V * 2 <= vmax and 64 * V <= NB:
+        V *= 2
+    nA = M * (NB // (32 * V)) * 32 * V * k
+    nB = n - nA
+    a = lambda x: (x + 255) // 256 * 256
+    offs = [0, a(nA * es), a(nA * es) + a(nB * es), a(nA * es) + a(nB * es) + a(nA * isz)]
+    vraw = np.concatenate([buf[offs[0]:offs[0] + nA * es], buf[offs[1]:offs[1] + nB * es]])
+    iraw = np.concatenate([buf[offs[2]:offs[2] + nA * isz], buf[offs[3]:offs[3] + nB * isz]])
+    pv = vraw.view(np.uint32 if es == 4 else np.uint16).astype(np.uint64)
+    pi = iraw.view(np.uint8 if isz == 1 else np.uint16).astype(np.uint64)
+    cv = vals.reshape(-1).view(np.uint32 if es == 4 else np.uint16).astype(np.uint64)
+    ci = idx.reshape(-1).astype(np.uint64)
+    np.testing.assert_array_equal(np.sort(pv << 16 | pi), np.sort(cv << 16 | ci))
+
+
+def test_pack_sp24_metadata():
+    """SP24 (B=4, k=2): values in canonical order; each nibble is idx0 | idx1<<2 with idx0 < idx1 (6 legal patterns)."""
+    M, K = 6, 64
+    W = synth.to_numpy(synth.matrix(M, K, "f16", seed=23))
+    vals, idx = oracle.prune(W, oracle.F16, 4, 2)
+    buf = oracle.pack(vals, idx, M, K, 4, 2, oracle.F16, oracle.SP24)
+    np.testing.assert_array_equal(buf[:M * K].view(np.float16).reshape(vals.shape), vals)
+    meta = buf[256 * ((M * K + 255) // 256):][:M * K // 8]
+    nib = np.stack([meta & 0xF, meta >> 4], axis=-1).reshape(M, K // 4)
+    legal = {0 | 1 << 2, 0 | 2 << 2, 0 | 3 << 2, 1 | 2 << 2, 1 | 3 << 2, 2 | 3 << 2}
+    assert set(np.unique(nib).tolist()) <= legal
+    np.testing.assert_array_equal(nib & 3, idx[..., 0])
+    np.testing.assert_array_equal(nib >> 2, idx[..., 1])
+
+
+# ------------------------------------------------------------------ products (Eq. 1)
+
+def test_spmv_spec_example_S249():
+    g = _gold("spec_examples.json")["spmv_S249"]
+    W = np.array([g["row"]], dtype=np.float32)
+    vals, idx = oracle.prune(W, oracle.F32, g["block"], g["k"])
+    y, bound = oracle.spmv(vals, idx, oracle.F32, 1, 8, g["block"], g["k"], np.array(g["x"], dtype=np.float32))
+    assert y[0] == g["y"] and bound[0] == 2 * 2 + 1 * 7
+
+
+def test_spmv_k0_is_zero():
+    """k = 0 gives W_bs = 0 and y = 0."""
+    W = synth.to_numpy(synth.matrix(4, 64, "f32"))
+    vals, idx = oracle.prune(W, oracle.F32, 16, 0)
+    y, bound = oracle.spmv(vals, idx, oracle.F32, 4, 64, 16, 0, np.ones(64, np.float32))
+    assert np.all(y == 0) and np.all(bound == 0)
+
+
+def test_spmv_dense_case_equals_gemv():
+    """k = B (s = 0) leaves W unchanged, so y is the dense GEMV. Compared with numpy's fp64 matmul."""
+    M, K = 12, 96
+    W = synth.to_numpy(synth.matrix(M, K, "f32", seed=3))
+    x = synth.to_numpy(synth.vector(K, "f32", seed=4))
+    vals, idx = oracle.prune(W, oracle.F32, 32, 32)
+    y, _ = oracle.spmv(vals, idx, oracle.F32, M, K, 32, 32, x)
+    np.testing.assert_allclose(y, W.astype(np.float64) @ x.astype(np.float64), rtol=1e-13, atol=1e-15)
+
+
+def test_spmv_unit_vector_extracts_column():
+    """x = e_j gives y = column j of W_bs exactly (pin (iii)); it catches transposed operands and wrong offsets."""
+    M, K, B, k = 10, 64, 16, 5
+    W = synth.to_numpy(synth.matrix(M, K, "f16", seed=8))
+    vals, idx = oracle.prune(W, oracle.F16, B, k)
+    Wd = oracle.decode(vals, idx, oracle.F16, M, K, B, k)
+    for j in (0, 1, 15, 16, 37, 63):
+        x = np.zeros(K, np.float16)
+        x[j] = 1
+        y, _ = oracle.spmv(vals, idx, oracle.F16, M, K, B, k, x)
+        np.testing.assert_array_equal(y, Wd[:, j])
+        kept = np.zeros(M, bool)
+        for r in range(M):
+            kept[r] = (j % B) in idx[r, j // B].tolist()
+        np.testing.assert_array_equal(y != 0, kept & (W[:, j] != 0))
+
+
+def test_spmv_integer_exact():
+    """W, x in {-1,0,1}: y is an exact integer, checked against Python-int arithmetic on the mask (pin (ii))."""
+    M, K, B, k = 16, 256, 32, 7
+    W = synth.to_numpy(synth.matrix(M, K, "f16", family="intexact", seed=9))
+    x = synth.to_numpy(synth.vector(K, "f16", family="intexact", seed=10))
+    vals, idx = oracle.prune(W, oracle.F16, B, k)
+    y, _ = oracle.spmv(vals, idx, oracle.F16, M, K, B, k, x)
+    mask = _rank_count_keep(W, B, k)
+    Wi = W.astype(np.int64) * mask
+    want = [sum(int(Wi[r, c]) * int(x[c]) for c in range(K)) for r in range(M)]
+    assert y.tolist() == [float(v) for v in want]
+
+
+def test_spmv_sparse_form_equals_dense_masked():
+    """Sum over canonical entries == dense-masked W_bs·x (O-7), up to fp64 rounding."""
+    M, K, B, k = 32, 512, 32, 3
+    W = synth.to_numpy(synth.matrix(M, K, "bf16", seed=12))
+    x = synth.to_numpy(synth.vector(K, "bf16", seed=13))
+    vals, idx = oracle.prune(W, oracle.BF16, B, k)
+    y, bound = oracle.spmv(vals, idx, oracle.BF16, M, K, B, k, x)
+    Wd = oracle.decode(vals, idx, oracle.BF16, M, K, B, k)
+    yd = oracle.gemv_dense(Wd, oracle.to_double(x, oracle.BF16))
+    assert np.all(np.abs(y - yd) <= 1e-12 * bound)
+    assert np.all(bound >= np.abs(y))
+
+
+def test_spmv_row_sampling():
+    M, K, B, k = 40, 256, 32, 4
+    W = synth.to_numpy(synth.matrix(M, K, "f16", seed=14))
+    x = synth.to_numpy(synth.vector(K, "f16", seed=15))
+    vals, idx = oracle.prune(W, oracle.F16, B, k)
+    y, b = oracle.spmv(vals, idx, oracle.F16, M, K, B, k, x)
+    rows = np.array([39, 0, 17], dtype=np.int64)
+    ys, bs = oracle.spmv(vals, idx, oracle.F16, M, K, B, k, x, rows=rows)
+    np.testing.assert_array_equal(ys, y[rows])
+    y2, _ = oracle.spmv_rowslice(vals[rows], idx[rows], oracle.F16, K, B, k, x)
+    np.testing.assert_array_equal(y2, y[rows])
+
+
+def test_spmm_identity_and_columns():
+    """X = I gives Y[n][r] = W_bs[r][n], and every column equals SpMV of that column."""
+    M, K, B, k = 9, 32, 8, 3
+    W = synth.to_numpy(synth.matrix(M, K, "f32", seed=16))
+    vals, idx = oracle.prune(W, oracle.F32, B, k)
+    Wd = oracle.decode(vals, idx, oracle.F32, M, K, B, k)
+    Y, _ = oracle.spmm(vals, idx, oracle.F32, M, K, B, k, np.eye(K, dtype=np.float32))
+    np.testing.assert_array_equal(Y, Wd.T)
+    X = synth.to_numpy(synth.vector(K, "f32", n=5, seed=17))
+    Y, _ = oracle.spmm(vals, idx, oracle.F32, M, K, B, k, X)
+    for n in range(5):
+        y, _ = oracle.spmv(vals, idx, oracle.F32, M, K, B, k, np.ascontiguousarray(X[n]))
+        np.testing.assert_array_equal(Y[n], y)
+    rows = np.array([8, 2], dtype=np.int64)
+    Yr, _ = oracle.spmm(vals, idx, oracle.F32, M, K, B, k, X, rows=rows)
+    np.testing.assert_array_equal(Yr, Y[:, rows])
+
+
+def test_ideal_time_S531():
+    g = _gold("spec_examples.json")["ideal_time_S531"]
+    assert oracle.ideal_time(g["d_time"], g["o_time"], g["sparsity"]) == pytest.approx(g["i_time"], abs=1e-12)
+    assert oracle.ideal_time(50.0, 10.0, 0.0) == 50.0  # s = 0 -> dense time
