@@ -128,13 +128,11 @@ def pack(vals: np.ndarray, idx: np.ndarray, M: int, K: int, block: int, k: int, 
     """Reference permutation pi_L of docs/layout.md: packed bytes (uint8)."""
     vals = _check(vals, dt)
     idx = np.ascontiguousarray(idx, dtype=np.uint16)
-    n = packed_bytes(M, K, block, k, dt, layout)
-    if n == 0:
-        raise ValueError("unsupported layout arguments")
-    out = np.zeros(n, dtype=np.uint8)
+    n = packed_bytes(M, K, block, k, dt, layout)  # 0 for k == 0 (nothing stored) or invalid
+    out = np.zeros(max(n, 1), dtype=np.uint8)
     if lib().orc_pack(_ptr(vals), _ptr(idx), M, K, block, k, dt, layout, _ptr(out)) != 0:
         raise ValueError("orc_pack rejected the arguments")
-    return out
+    return out[:n]
 
 
 def spmv(vals, idx, dt, M, K, block, k, x, rows=None):

@@ -1,0 +1,182 @@
+// bs_api.cu: the C ABI of libbs.so (include/bs.h). It validates arguments and dispatches to the
+// kernels. It never allocates device memory and never synchronises.
+#include <math.h>
+#include <mutex>
+
+#include "bs_common.cuh"
+
+int64_t bsk_spmv_smem_bytes(const bsk::Geom& g);
+
+namespace bsk {
+
+const DevProps& dev_props() {
+  static DevProps props[64];
+  static bool have[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!have[dev]) {
+    DevProps p{};
+    cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&p.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&p.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    if (p.sms <= 0) p.sms = 148;
+    props[dev] = p;
+    have[dev] = true;
+  }
+  return props[dev];
+}
+
+}  // namespace bsk
+
+namespace {
+
+int from_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return BS_OK;
+  if (e == cudaErrorNotSupported || e == cudaErrorInvalidConfiguration) return BS_ERR_UNSUPPORTED;
+  return BS_ERR_CUDA;
+}
+
+bool valid_dt(int dt) { return dt == BS_F32 || dt == BS_F16 || dt == BS_BF16; }
+
+int check_shape(int64_t M, int64_t K, int B, int k) {
+  if (M < 1 || K < 1 || B < 1) return BS_ERR_SHAPE;
+  if (B > 65536) return BS_ERR_UNSUPPORTED;
+  if (K % B != 0) return BS_ERR_SHAPE;
+  if (k < 0 || k > B) return BS_ERR_ARG;
+  return BS_OK;
+}
+
+int matrix_geom(const bs_matrix* A, bsk::Geom* g) {
+  if (!A) return BS_ERR_ARG;
+  if (!valid_dt(A->dt)) return BS_ERR_DTYPE;
+  int st = check_shape(A->M, A->K, A->block, A->k);
+  if (st) return st;
+  if (A->layout != BS_LAYOUT_SPMV && A->layout != BS_LAYOUT_SPMM && A->layout != BS_LAYOUT_SP24)
+    return BS_ERR_ARG;
+  if (!bsk::make_geom(A->M, A->K, A->block, A->k, A->dt, A->layout, g)) return BS_ERR_UNSUPPORTED;
+  if (!A->packed && g->total > 0) return BS_ERR_ARG;  /* k == 0 packs to zero bytes */
+  return BS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bs_k_from_sparsity(int block, double sparsity) {
+  if (block < 1 || !(sparsity >= 0.0) || !(sparsity < 1.0)) return -1;
+  return (int)lround((1.0 - sparsity) * (double)block);
+}
+
+size_t bs_packed_bytes(int64_t M, int64_t K, int block, int k, int dt, int layout) {
+  bsk::Geom g;
+  if (!bsk::make_geom(M, K, block, k, dt, layout, &g)) return 0;
+  return (size_t)g.total;
+}
+
+const char* bs_status_str(int status) {
+  switch (status) {
+    case BS_OK: return "BS_OK";
+    case BS_ERR_ARG: return "BS_ERR_ARG";
+    case BS_ERR_SHAPE: return "BS_ERR_SHAPE";
+    case BS_ERR_DTYPE: return "BS_ERR_DTYPE";
+    case BS_ERR_UNSUPPORTED: return "BS_ERR_UNSUPPORTED";
+    case BS_ERR_CUDA: return "BS_ERR_CUDA";
+    default: return "BS_UNKNOWN";
+  }
+}
+
+const char* bs_version(void) { return "libbs 0.1 sm_100a (balanced sparsity, arXiv 1811.00206)"; }
+
+int bs_prune_k(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block, int k, void* vals,
+               uint16_t* idx, void* stream) {
+  if (!valid_dt(dt)) return BS_ERR_DTYPE;
+  int st = check_shape(M, K, block, k);
+  if (st) return st;
+  if (!W || ldw < K) return BS_ERR_ARG;
+  if (k == 0) return BS_OK;
+  if (!vals || !idx) return BS_ERR_ARG;
+  return from_cuda(bsk_launch_prune(W, dt, M, K, ldw, block, k, vals, idx, (cudaStream_t)stream));
+}
+
+int bs_prune(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block, double sparsity, int* k_out,
+             void* vals, uint16_t* idx, void* stream) {
+  if (!(sparsity >= 0.0) || !(sparsity < 1.0)) return BS_ERR_ARG;
+  if (block < 1) return BS_ERR_SHAPE;
+  const int k = bs_k_from_sparsity(block, sparsity);
+  if (k_out) *k_out = k;
+  return bs_prune_k(W, dt, M, K, ldw, block, k, vals, idx, stream);
+}
+
+int bs_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int block, int k, int dt, int layout,
+            void* packed, void* stream) {
+  if (!valid_dt(dt)) return BS_ERR_DTYPE;
+  int st = check_shape(M, K, block, k);
+  if (st) return st;
+  if (layout != BS_LAYOUT_SPMV && layout != BS_LAYOUT_SPMM && layout != BS_LAYOUT_SP24) return BS_ERR_ARG;
+  bsk::Geom g;
+  if (!bsk::make_geom(M, K, block, k, dt, layout, &g)) return BS_ERR_UNSUPPORTED;
+  if ((!packed && g.total > 0) || (k > 0 && (!vals || !idx))) return BS_ERR_ARG;
+  if (g.total == 0) return BS_OK;
+  return from_cuda(bsk_launch_pack(vals, idx, g, packed, (cudaStream_t)stream));
+}
+
+int bs_unpack(const void* packed, int64_t M, int64_t K, int block, int k, int dt, int layout, void* vals,
+              uint16_t* idx, void* stream) {
+  if (!valid_dt(dt)) return BS_ERR_DTYPE;
+  int st = check_shape(M, K, block, k);
+  if (st) return st;
+  if (layout != BS_LAYOUT_SPMV && layout != BS_LAYOUT_SPMM && layout != BS_LAYOUT_SP24) return BS_ERR_ARG;
+  bsk::Geom g;
+  if (!bsk::make_geom(M, K, block, k, dt, layout, &g)) return BS_ERR_UNSUPPORTED;
+  if ((!packed && g.total > 0) || (k > 0 && (!vals || !idx))) return BS_ERR_ARG;
+  if (k == 0) return BS_OK;
+  return from_cuda(bsk_launch_unpack(packed, g, vals, idx, (cudaStream_t)stream));
+}
+
+int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream) {
+  bsk::Geom g;
+  int st = matrix_geom(A, &g);
+  if (st) return st;
+  if (!x || !y) return BS_ERR_ARG;
+  if (g.layout == BS_LAYOUT_SP24) return BS_ERR_UNSUPPORTED;
+  return from_cuda(bsk_launch_spmv(g, A->packed, x, y, (cudaStream_t)stream));
+}
+
+int bs_spmv_host(const bs_matrix* A, const void* x_host, void* y_host, void* x_dev, void* y_dev, void* stream) {
+  bsk::Geom g;
+  int st = matrix_geom(A, &g);
+  if (st) return st;
+  if (!x_host || !y_host || !x_dev || !y_dev) return BS_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(x_dev, x_host, (size_t)(g.K * g.es), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return BS_ERR_CUDA;
+  st = bs_spmv(A, x_dev, y_dev, stream);
+  if (st) return st;
+  if (cudaMemcpyAsync(y_host, y_dev, (size_t)(g.M * g.es), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return BS_ERR_CUDA;
+  return BS_OK;
+}
+
+int bs_spmm(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, void* Y, int64_t ldy, void* stream) {
+  bsk::Geom g;
+  int st = matrix_geom(A, &g);
+  if (st) return st;
+  if (!X || !Y || N < 1 || ldx < g.K || ldy < g.M) return BS_ERR_ARG;
+  if (g.layout == BS_LAYOUT_SP24) return BS_ERR_UNSUPPORTED;
+  cudaError_t e = bsk_launch_spmm(g, A->packed, X, N, ldx, Y, ldy, (cudaStream_t)stream);
+  if (e != cudaErrorNotSupported) return from_cuda(e);
+  // Column-at-a-time fallback for layouts/shapes the batched kernel does not cover (SPMV layout
+  // with V > 1, or very wide blocks): every column runs the SpMV kernel.
+  const size_t es = (size_t)g.es;
+  for (int64_t n = 0; n < N; ++n) {
+    e = bsk_launch_spmv(g, A->packed, (const char*)X + (size_t)(n * ldx) * es, (char*)Y + (size_t)(n * ldy) * es,
+                        (cudaStream_t)stream);
+    if (e != cudaSuccess) return from_cuda(e);
+  }
+  return BS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// bs_common.cuh: shared device/host definitions of the CUDA path (not shared with oracle/).
+//
+// Geometry of the packed layouts, written from docs/layout.md. The oracle re-derives the same
+// geometry independently from the same text; the tests compare bytes.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bs.h"
+
+namespace bsk {
+
+constexpr int kAlign = 256;
+
+__host__ __device__ inline int64_t align_up(int64_t n, int64_t a) { return (n + a - 1) / a * a; }
+
+inline int dtype_bytes(int dt) { return dt == BS_F32 ? 4 : 2; }
+
+// docs/layout.md "SPMV layout" / "SPMM layout".
+struct Geom {
+  int64_t M, K, NB;
+  int B, k, dt, layout;
+  int es;       // value bytes
+  int is;       // index bytes (1 if B <= 256 else 2)
+  int V;        // lanes own V blocks per panel
+  int64_t P;    // 32*V blocks per panel
+  int64_t NBf;  // full panels per row
+  int64_t T;    // tail blocks per row
+  int64_t offVA, offVB, offIA, offIB, total;
+};
+
+// Returns false on invalid arguments.
+inline bool make_geom(int64_t M, int64_t K, int B, int k, int dt, int layout, Geom* g) {
+  if (M < 1 || K < 1 || B < 1 || B > 65536 || K % B != 0 || k < 0 || k > B) return false;
+  if (dt != BS_F32 && dt != BS_F16 && dt != BS_BF16) return false;
+  g->M = M; g->K = K; g->NB = K / B; g->B = B; g->k = k; g->dt = dt; g->layout = layout;
+  g->es = dtype_bytes(dt);
+  g->is = B <= 256 ? 1 : 2;
+  if (layout == BS_LAYOUT_SPMV || layout == BS_LAYOUT_SPMM) {
+    int vmax = layout == BS_LAYOUT_SPMM ? 1 : 16 / g->es;
+    int V = 1;
+    while (V * 2 <= vmax && 32LL * V * 2 <= g->NB) V *= 2;
+    g->V = V;
+    g->P = 32LL * V;
+    g->NBf = g->NB / g->P;
+    g->T = g->NB - g->NBf * g->P;
+    int64_t nA = M * g->NBf * g->P * k, nB = M * g->T * k;
+    g->offVA = 0;
+    g->offVB = g->offVA + align_up(nA * g->es, kAlign);
+    g->offIA = g->offVB + align_up(nB * g->es, kAlign);
+    g->offIB = g->offIA + align_up(nA * g->is, kAlign);
+    g->total = g->offIB + align_up(nB * g->is, kAlign);
+    return true;
+  }
+  if (layout == BS_LAYOUT_SP24) {
+    if (B != 4 || k != 2 || K % 8 != 0) return false;
+    g->V = 0; g->P = 0; g->NBf = 0; g->T = 0;
+    g->offVA = 0;
+    g->offIA = align_up(M * (K / 2) * g->es, kAlign);
+    g->offVB = g->offIB = 0;
+    g->total = g->offIA + align_up(M * (g->NB / 2), kAlign);
+    return true;
+  }
+  return false;
+}
+
+// Per-device properties cached once per device (the library's only state).
+struct DevProps {
+  int sms;
+  int smem_optin;   // max dynamic smem per block (opt-in)
+  int smem_per_sm;
+};
+const DevProps& dev_props();
+
+}  // namespace bsk
+
+// Launchers implemented in the kernel translation units. All return cudaError_t of the launch.
+cudaError_t bsk_launch_prune(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int B, int k,
+                             void* vals, uint16_t* idx, cudaStream_t s);
+cudaError_t bsk_launch_pack(const void* vals, const uint16_t* idx, const bsk::Geom& g, void* packed,
+                            cudaStream_t s);
+cudaError_t bsk_launch_unpack(const void* packed, const bsk::Geom& g, void* vals, uint16_t* idx,
+                              cudaStream_t s);
+cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y,
+                            cudaStream_t s);
+cudaError_t bsk_launch_spmm(const bsk::Geom& g, const void* packed, const void* X, int64_t N,
+                            int64_t ldx, void* Y, int64_t ldy, cudaStream_t s);

@@ -1,0 +1,139 @@
+// pack.cu: K2 bs_pack / bs_unpack, pure permutations between canonical and packed layouts.
+//
+// The layout is written from docs/layout.md. One thread per packed entry computes the canonical
+// source (gather), so packed writes are coalesced. The paper describes no W layout;
+// the layout choice is explained in DESIGN.md §4.
+#include "bs_common.cuh"
+
+namespace {
+
+struct PackArgs {
+  int64_t M, NB, NBf, T, P;
+  int V, k, es, is;
+};
+
+// Packed entry e of region VA (e < M*NBf*P*k) or VB -> canonical linear position (r*NB + b)*k + t.
+__device__ __forceinline__ int64_t src_of_A(const PackArgs& a, int64_t e) {
+  // e = ((r*NBf + p)*k + t)*P + l*V + v
+  const int64_t lv = e % a.P;
+  const int64_t q = e / a.P;  // (r*NBf + p)*k + t
+  const int t = (int)(q % a.k);
+  const int64_t rp = q / a.k;  // r*NBf + p
+  const int64_t p = rp % a.NBf, r = rp / a.NBf;
+  const int l = (int)(lv / a.V), v = (int)(lv % a.V);
+  const int64_t b = p * a.P + (int64_t)v * 32 + l;
+  return (r * a.NB + b) * a.k + t;
+}
+
+__device__ __forceinline__ int64_t src_of_B(const PackArgs& a, int64_t e) {
+  // e = (r*k + t)*T + v*32 + l
+  const int64_t vl = e % a.T;
+  const int64_t q = e / a.T;
+  const int t = (int)(q % a.k);
+  const int64_t r = q / a.k;
+  const int64_t b = a.NBf * a.P + vl;  // v*32 + l == vl
+  return (r * a.NB + b) * a.k + t;
+}
+
+template <typename VT>
+__global__ void pack_kernel(const VT* __restrict__ vals, const uint16_t* __restrict__ idx, PackArgs a,
+                            VT* __restrict__ VA, VT* __restrict__ VB, uint8_t* __restrict__ IA,
+                            uint8_t* __restrict__ IB, int64_t nA, int64_t nB, bool unpack,
+                            VT* __restrict__ out_vals, uint16_t* __restrict__ out_idx) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nA + nB; e += stride) {
+    const bool inA = e < nA;
+    const int64_t ee = inA ? e : e - nA;
+    const int64_t src = inA ? src_of_A(a, ee) : src_of_B(a, ee);
+    VT* vdst = inA ? VA : VB;
+    uint8_t* idst = inA ? IA : IB;
+    if (!unpack) {
+      vdst[ee] = vals[src];
+      const uint16_t o = idx[src];
+      if (a.is == 1) idst[ee] = (uint8_t)o;
+      else { idst[2 * ee] = (uint8_t)(o & 0xff); idst[2 * ee + 1] = (uint8_t)(o >> 8); }
+    } else {
+      out_vals[src] = vdst[ee];
+      out_idx[src] = a.is == 1 ? (uint16_t)idst[ee] : (uint16_t)(idst[2 * ee] | (idst[2 * ee + 1] << 8));
+    }
+  }
+}
+
+// SP24 metadata: byte (r, c) holds blocks b = 2c, 2c+1 of row r as nibbles idx0 | idx1 << 2.
+__global__ void sp24_meta_kernel(const uint16_t* __restrict__ idx, int64_t nbytes, uint8_t* __restrict__ meta,
+                                 bool unpack, uint16_t* __restrict__ out_idx) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbytes; i += stride) {
+    // canonical positions of the two blocks: (2i)*2 and (2i+1)*2 (k = 2)
+    if (!unpack) {
+      const uint16_t* p = idx + 4 * i;
+      meta[i] = (uint8_t)((p[0] | (p[1] << 2)) | ((p[2] | (p[3] << 2)) << 4));
+    } else {
+      const uint8_t m = meta[i];
+      uint16_t* p = out_idx + 4 * i;
+      p[0] = m & 3; p[1] = (m >> 2) & 3; p[2] = (m >> 4) & 3; p[3] = (m >> 6) & 3;
+    }
+  }
+}
+
+cudaError_t zero_gap(uint8_t* base, int64_t from, int64_t to, cudaStream_t s) {
+  if (to > from) return cudaMemsetAsync(base + from, 0, (size_t)(to - from), s);
+  return cudaSuccess;
+}
+
+cudaError_t run(const bsk::Geom& g, const void* vals, const uint16_t* idx, void* packed, bool unpack,
+                void* out_vals, uint16_t* out_idx, cudaStream_t s) {
+  uint8_t* base = (uint8_t*)packed;
+  const int sms = bsk::dev_props().sms;
+  cudaError_t err;
+  if (g.layout == BS_LAYOUT_SP24) {
+    const int64_t nv = g.M * (g.K / 2);
+    const int64_t nmeta = g.M * (g.NB / 2);
+    if (!unpack) {
+      if ((err = cudaMemcpyAsync(base, vals, (size_t)(nv * g.es), cudaMemcpyDeviceToDevice, s))) return err;
+      if ((err = zero_gap(base, nv * g.es, g.offIA, s))) return err;
+      if ((err = zero_gap(base, g.offIA + nmeta, g.total, s))) return err;
+    } else {
+      if ((err = cudaMemcpyAsync(out_vals, base, (size_t)(nv * g.es), cudaMemcpyDeviceToDevice, s))) return err;
+    }
+    int64_t blocks = (nmeta + 255) / 256;
+    if (blocks > (int64_t)sms * 32) blocks = (int64_t)sms * 32;
+    if (blocks < 1) blocks = 1;
+    sp24_meta_kernel<<<(unsigned)blocks, 256, 0, s>>>(idx, nmeta, base + g.offIA, unpack, out_idx);
+    return cudaGetLastError();
+  }
+  PackArgs a;
+  a.M = g.M; a.NB = g.NB; a.NBf = g.NBf; a.T = g.T; a.P = g.P; a.V = g.V; a.k = g.k; a.es = g.es; a.is = g.is;
+  const int64_t nA = g.M * g.NBf * g.P * g.k, nB = g.M * g.T * g.k;
+  if (!unpack) {
+    if ((err = zero_gap(base, nA * g.es, g.offVB, s))) return err;
+    if ((err = zero_gap(base, g.offVB + nB * g.es, g.offIA, s))) return err;
+    if ((err = zero_gap(base, g.offIA + nA * g.is, g.offIB, s))) return err;
+    if ((err = zero_gap(base, g.offIB + nB * g.is, g.total, s))) return err;
+  }
+  if (nA + nB == 0) return cudaSuccess;
+  int64_t blocks = (nA + nB + 255) / 256;
+  if (blocks > (int64_t)sms * 32) blocks = (int64_t)sms * 32;
+  if (g.es == 4) {
+    pack_kernel<uint32_t><<<(unsigned)blocks, 256, 0, s>>>(
+        (const uint32_t*)vals, idx, a, (uint32_t*)(base + g.offVA), (uint32_t*)(base + g.offVB),
+        base + g.offIA, base + g.offIB, nA, nB, unpack, (uint32_t*)out_vals, out_idx);
+  } else {
+    pack_kernel<uint16_t><<<(unsigned)blocks, 256, 0, s>>>(
+        (const uint16_t*)vals, idx, a, (uint16_t*)(base + g.offVA), (uint16_t*)(base + g.offVB),
+        base + g.offIA, base + g.offIB, nA, nB, unpack, (uint16_t*)out_vals, out_idx);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t bsk_launch_pack(const void* vals, const uint16_t* idx, const bsk::Geom& g, void* packed,
+                            cudaStream_t s) {
+  return run(g, vals, idx, packed, false, nullptr, nullptr, s);
+}
+
+cudaError_t bsk_launch_unpack(const void* packed, const bsk::Geom& g, void* vals, uint16_t* idx,
+                              cudaStream_t s) {
+  return run(g, nullptr, nullptr, const_cast<void*>(packed), true, vals, idx, s);
+}

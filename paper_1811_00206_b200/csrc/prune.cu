@@ -1,0 +1,208 @@
+// prune.cu: K1 bs_prune, one balance-aware pruning step (Alg. 1 inner loop).
+//
+// For each (row, block) the kernel keeps the k entries of largest magnitude, ties to the lower
+// offset. A NaN ranks above +Inf and all NaNs are equal (docs/layout.md "Canonical form"). Alg. 1
+// "sorts elements". Any selection that yields the same top-k set is equivalent,
+// so the GPU selects by rank instead of sorting:
+//   1. Map every element to an unsigned magnitude key: the abs bit pattern, with every NaN folded
+//      onto one key just above Inf. For IEEE formats the unsigned order of these keys is the
+//      magnitude order.
+//   2. Find T, the k-th largest key, with a bitwise radix select. Each bit costs one warp ballot (or
+//      one warp sum for wide blocks): T = max{t : #{key >= t} >= k}.
+//   3. Keep every key > T, plus the first (k - #{key > T}) keys equal to T in offset order.
+//   4. Compact the kept offsets in ascending order with a warp prefix count.
+// Values are copied bit for bit. The result is a pure integer decision, so it matches the oracle
+// bit-exactly.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "bs_common.cuh"
+
+namespace {
+
+template <int DT>
+struct KeyOf;
+template <>
+struct KeyOf<BS_F32> {
+  using raw_t = uint32_t;
+  static constexpr int kBits = 31;
+  __device__ static uint32_t key(uint32_t u) {
+    uint32_t a = u & 0x7fffffffu;
+    return a > 0x7f800000u ? 0x7f800001u : a;
+  }
+};
+template <>
+struct KeyOf<BS_F16> {
+  using raw_t = uint16_t;
+  static constexpr int kBits = 15;
+  __device__ static uint32_t key(uint32_t u) {
+    uint32_t a = u & 0x7fffu;
+    return a > 0x7c00u ? 0x7c01u : a;
+  }
+};
+template <>
+struct KeyOf<BS_BF16> {
+  using raw_t = uint16_t;
+  static constexpr int kBits = 15;
+  __device__ static uint32_t key(uint32_t u) {
+    uint32_t a = u & 0x7fffu;
+    return a > 0x7f80u ? 0x7f81u : a;
+  }
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Narrow blocks (B <= 32): a warp holds floor(32/B) blocks, one element per lane. Each segment of B
+// lanes runs its own radix select through ballots masked to the segment. Each warp iteration covers
+// `nseg` consecutive flattened blocks gid = r*NB + b.
+template <int DT>
+__global__ void __launch_bounds__(256) prune_narrow(const typename KeyOf<DT>::raw_t* __restrict__ W,
+                                                    int64_t M, int64_t NB, int64_t ldw, int B, int k,
+                                                    typename KeyOf<DT>::raw_t* __restrict__ vals,
+                                                    uint16_t* __restrict__ idx) {
+  using raw_t = typename KeyOf<DT>::raw_t;
+  const int lane = threadIdx.x & 31;
+  const int nseg = 32 / B;
+  const int seg = lane / B;
+  const int j = lane - seg * B;  // block-local offset held by this lane
+  const bool lane_used = seg < nseg;
+  const uint32_t segmask = lane_used ? ((B == 32) ? 0xffffffffu : (((1u << B) - 1u) << (seg * B))) : 0u;
+  const uint32_t lt = lanemask_lt();
+  const int64_t nblocks = M * NB;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (int64_t g0 = wid * nseg; g0 < nblocks; g0 += warps * nseg) {
+    const int64_t gid = g0 + seg;
+    const bool valid = lane_used && gid < nblocks;
+    raw_t raw = 0;
+    if (valid) {
+      const int64_t r = gid / NB, b = gid - r * NB;
+      raw = W[r * ldw + b * B + j];
+    }
+    const uint32_t key = KeyOf<DT>::key((uint32_t)raw);
+    uint32_t T = 0;
+#pragma unroll
+    for (int bit = KeyOf<DT>::kBits - 1; bit >= 0; --bit) {
+      const uint32_t cand = T | (1u << bit);
+      const uint32_t bal = __ballot_sync(0xffffffffu, valid && key >= cand);
+      if (__popc(bal & segmask) >= k) T = cand;
+    }
+    const bool gt = valid && key > T;
+    const bool eq = valid && key == T;
+    const int ngt = __popc(__ballot_sync(0xffffffffu, gt) & segmask);
+    const uint32_t eqmask = __ballot_sync(0xffffffffu, eq) & segmask;
+    const bool keep = gt || (eq && __popc(eqmask & lt) < k - ngt);
+    const uint32_t keepmask = __ballot_sync(0xffffffffu, keep) & segmask;
+    if (keep) {
+      const int pos = __popc(keepmask & lt);
+      vals[gid * k + pos] = raw;
+      idx[gid * k + pos] = (uint16_t)j;
+    }
+  }
+}
+
+__device__ __forceinline__ int warp_sum(int v) { return __reduce_add_sync(0xffffffffu, v); }
+
+__device__ __forceinline__ int warp_excl_scan(int v, int lane) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x - v;
+}
+
+// Wide blocks (B > 32): one warp per block. Lane l owns the contiguous offsets [l*E, min(l*E+E, B))
+// with E = ceil(B/32), so lane order is offset order. Counts are warp sums, and the tie rank and
+// output slots are exclusive warp scans. Elements are re-read through L1 on every radix step.
+template <int DT>
+__global__ void __launch_bounds__(256) prune_wide(const typename KeyOf<DT>::raw_t* __restrict__ W,
+                                                  int64_t M, int64_t NB, int64_t ldw, int B, int k,
+                                                  typename KeyOf<DT>::raw_t* __restrict__ vals,
+                                                  uint16_t* __restrict__ idx) {
+  using raw_t = typename KeyOf<DT>::raw_t;
+  const int lane = threadIdx.x & 31;
+  const int E = (B + 31) / 32;
+  const int j0 = min(lane * E, B), j1 = min(j0 + E, B);
+  const int64_t nblocks = M * NB;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t gid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gid < nblocks; gid += warps) {
+    const int64_t r = gid / NB, b = gid - r * NB;
+    const raw_t* src = W + r * ldw + b * B;
+    uint32_t T = 0;
+    for (int bit = KeyOf<DT>::kBits - 1; bit >= 0; --bit) {
+      const uint32_t cand = T | (1u << bit);
+      int c = 0;
+      for (int j = j0; j < j1; ++j) c += KeyOf<DT>::key((uint32_t)__ldg(src + j)) >= cand;
+      if (warp_sum(c) >= k) T = cand;
+    }
+    int cgt = 0, ceq = 0;
+    for (int j = j0; j < j1; ++j) {
+      const uint32_t key = KeyOf<DT>::key((uint32_t)__ldg(src + j));
+      cgt += key > T;
+      ceq += key == T;
+    }
+    const int need = k - warp_sum(cgt);
+    int eq_before = warp_excl_scan(ceq, lane);
+    // kept count per lane, then output slots
+    int ckeep = 0;
+    {
+      int e = eq_before;
+      for (int j = j0; j < j1; ++j) {
+        const uint32_t key = KeyOf<DT>::key((uint32_t)__ldg(src + j));
+        if (key > T) ++ckeep;
+        else if (key == T) { ckeep += e < need; ++e; }
+      }
+    }
+    int pos = warp_excl_scan(ckeep, lane);
+    int e = eq_before;
+    for (int j = j0; j < j1; ++j) {
+      const raw_t raw = __ldg(src + j);
+      const uint32_t key = KeyOf<DT>::key((uint32_t)raw);
+      bool keep = key > T;
+      if (key == T) { keep = e < need; ++e; }
+      if (keep) {
+        vals[gid * k + pos] = raw;
+        idx[gid * k + pos] = (uint16_t)j;
+        ++pos;
+      }
+    }
+  }
+}
+
+template <int DT>
+cudaError_t launch_prune_t(const void* W, int64_t M, int64_t K, int64_t ldw, int B, int k, void* vals,
+                           uint16_t* idx, cudaStream_t s) {
+  using raw_t = typename KeyOf<DT>::raw_t;
+  const int64_t NB = K / B;
+  const int threads = 256;
+  const int sms = bsk::dev_props().sms;
+  if (B <= 32) {
+    const int nseg = 32 / B;
+    const int64_t warps_needed = (M * NB + nseg - 1) / nseg;
+    int64_t blocks = (warps_needed + 7) / 8;
+    blocks = blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16;
+    prune_narrow<DT><<<(unsigned)blocks, threads, 0, s>>>((const raw_t*)W, M, NB, ldw, B, k, (raw_t*)vals, idx);
+  } else {
+    int64_t blocks = (M * NB + 7) / 8;
+    blocks = blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16;
+    prune_wide<DT><<<(unsigned)blocks, threads, 0, s>>>((const raw_t*)W, M, NB, ldw, B, k, (raw_t*)vals, idx);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t bsk_launch_prune(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int B, int k,
+                             void* vals, uint16_t* idx, cudaStream_t s) {
+  switch (dt) {
+    case BS_F32: return launch_prune_t<BS_F32>(W, M, K, ldw, B, k, vals, idx, s);
+    case BS_F16: return launch_prune_t<BS_F16>(W, M, K, ldw, B, k, vals, idx, s);
+    default: return launch_prune_t<BS_BF16>(W, M, K, ldw, B, k, vals, idx, s);
+  }
+}

@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle, on the same seeded inputs.
+
+Bar (BASELINE.json north_star):
+  - pruning masks (canonical idx and value bits) and packed bytes: bit-exact;
+  - y: |y_gpu - y_ref| <= tau * sum|w||x| per element, tau = 1e-4 (f32), 1e-2 (f16/bf16);
+  - integer-exact inputs and row sharding: bit-identical.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DT = {"f32": oracle.F32, "f16": oracle.F16, "bf16": oracle.BF16}
+
+
+@pytest.fixture(scope="module")
+def bs():
+    import paper_1811_00206_b200 as bs
+    return bs
+
+
+def _idx_np(idx: torch.Tensor) -> np.ndarray:
+    return idx.cpu().numpy().view(np.uint16)
+
+
+def _raw(t: torch.Tensor) -> np.ndarray:
+    a = synth.to_numpy(t)
+    return a.view(np.uint32 if a.itemsize == 4 else np.uint16)
+
+
+def _prune_parity(bs, W: torch.Tensor, dname: str, B: int, k: int):
+    vals, idx, k2 = bs.prune(W.cuda(), B, k=k)
+    assert k2 == k
+    Wn = synth.to_numpy(W)
+    ov, oi = oracle.prune(Wn, DT[dname], B, k)
+    np.testing.assert_array_equal(_idx_np(idx), oi)
+    np.testing.assert_array_equal(_raw(vals), ov.view(np.uint32 if ov.itemsize == 4 else np.uint16))
+    return vals, idx, ov, oi
+
+
+# (M, K, B, k, dtype, family): small shapes that span several panels, a ragged tail, NB < 32,
+# B > 256 (u16 indices), odd B, the 2:4 shape and every dtype.
+SMALL = [
+    (64, 64, 16, 8, "f32", "gaussian"),        # cfg0 tiny (BJ.configs[0])
+    (96, 3008, 32, 3, "f16", "gaussian"),      # PTB row width (NB = 94 < 256: tail only)
+    (70, 25088, 32, 3, "f16", "gaussian"),     # fc6 row width: 3 panels + 16-block tail
+    (33, 25088, 32, 1, "bf16", "gaussian"),
+    (50, 4096, 32, 16, "f32", "gaussian"),     # fc7 width, f32: V = 4
+    (40, 8192, 32, 2, "bf16", "ties"),
+    (48, 2048, 4, 2, "f16", "gaussian"),       # 2:4 shape on the generic path
+    (31, 1024, 32, 4, "f16", "sameoffset"),    # CTC W_hh width, NB = 32
+    (29, 2048, 512, 9, "f16", "gaussian"),     # B > 256: u16 indices
+    (17, 1000, 25, 8, "f32", "ties"),          # odd B (Table brange balance range 25)
+    (65, 640, 20, 0, "f16", "gaussian"),       # k = 0
+    (8, 256, 16, 16, "bf16", "gaussian"),      # k = B (dense)
+    (3, 96, 1, 1, "f16", "gaussian"),          # B = 1
+]
+
+
+@pytest.mark.parametrize("M,K,B,k,dname,family", SMALL)
+def test_prune_pack_spmv_small(bs, M, K, B, k, dname, family):
+    W = synth.matrix(M, K, dname, family=family, seed=synth.seed_for(0, M + K + B), B=B)
+    vals, idx, ov, oi = _prune_parity(bs, W, dname, B, k)
+    x = synth.vector(K, dname, seed=synth.seed_for(0, 7))
+    for layout, olay in (("spmv", oracle.SPMV), ("spmm", oracle.SPMM)):
+        A = bs.pack(vals, idx, K, B, layout=layout)
+        assert A.nbytes == oracle.packed_bytes(M, K, B, k, DT[dname], olay)
+        np.testing.assert_array_equal(A.packed.cpu().numpy(), oracle.pack(ov, oi, M, K, B, k, DT[dname], olay))
+        uv, ui = bs.unpack(A)
+        np.testing.assert_array_equal(_raw(uv), _raw(vals))
+        np.testing.assert_array_equal(_idx_np(ui), oi)
+        y = bs.spmv(A, x.cuda())
+        torch.cuda.synchronize()
+        yr, bound = oracle.spmv(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(x))
+        ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(y), DT[dname]), yr, bound, oracle.TAU[DT[dname]])
+        assert ok, f"{layout}: worst |err|/bound = {worst}"
+
+
+def test_prune_special_values(bs):
+    for dname in ("f32", "f16", "bf16"):
+        W = synth.special_block_matrix(dname)
+        for k in range(0, 17):
+            if k == 0:
+                continue
+            _prune_parity(bs, W, dname, 16, k)
+
+
+@pytest.mark.parametrize("dname", ["f16", "bf16", "f32"])
+def test_spmv_integer_exact_bit_identical(bs, dname):
+    """W, x in {-1,0,1}: every partial sum is an exact integer, so y must equal the oracle bit for bit."""
+    M, K, B, k = 300, 6144, 32, 5
+    W = synth.matrix(M, K, dname, family="intexact", seed=41)
+    x = synth.vector(K, dname, family="intexact", seed=42)
+    vals, idx, ov, oi = _prune_parity(bs, W, dname, B, k)
+    A = bs.pack(vals, idx, K, B)
+    y = bs.spmv(A, x.cuda())
+    yr, _ = oracle.spmv(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(x))
+    assert np.all(np.abs(yr) <= 256)  # representable in every D
+    np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(y), DT[dname]), yr)
+
+
+def test_spmv_unit_vectors(bs):
+    """x = e_j returns column j of W_bs exactly (catches wrong offsets, banks or transposes)."""
+    M, K, B, k = 40, 8192 + 512, 32, 3
+    W = synth.matrix(M, K, "f16", seed=43)
+    vals, idx, ov, oi = _prune_parity(bs, W, "f16", B, k)
+    A = bs.pack(vals, idx, K, B)
+    Wd = oracle.decode(ov, oi, oracle.F16, M, K, B, k)
+    for j in (0, 1, 31, 32, 33, 1023, 1024, 8191, 8192, K - 1):
+        x = torch.zeros(K, dtype=torch.float16)
+        x[j] = 1
+        y = bs.spmv(A, x.cuda())
+        np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(y), oracle.F16), Wd[:, j])
+
+
+def test_row_sharding_bit_identical(bs):
+    """Rows packed and multiplied in P slices concatenate to the unsharded y bit for bit (O-9)."""
+    M, K, B, k = 1000, 25088, 32, 3
+    W = synth.matrix(M, K, "f16", seed=44).cuda()
+    x = synth.vector(K, "f16", seed=45).cuda()
+    vals, idx, _ = bs.prune(W, B, k=k)
+    y1 = bs.spmv(bs.pack(vals, idx, K, B), x)
+    from paper_1811_00206_b200.dist import row_range
+    for P in (2, 3, 8):
+        parts = []
+        for r in range(P):
+            r0, r1 = row_range(M, P, r)
+            Ws = synth.matrix(r1 - r0, K, "f16", seed=44, row0=r0).cuda()  # regenerated slice
+            v, i, _ = bs.prune(Ws, B, k=k)
+            parts.append(bs.spmv(bs.pack(v, i, K, B), x))
+        assert torch.equal(torch.cat(parts), y1)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 8, 13, 32, 64])
+@pytest.mark.parametrize("dname", ["f16", "bf16", "f32"])
+def test_spmm_small(bs, N, dname):
+    M, K, B, k = 77, 3072 + 96, 32, 4
+    W = synth.matrix(M, K, dname, seed=46)
+    X = synth.vector(K, dname, seed=47, n=N)
+    vals, idx, ov, oi = _prune_parity(bs, W, dname, B, k)
+    for layout in ("spmm", "spmv"):
+        A = bs.pack(vals, idx, K, B, layout=layout)
+        Y = bs.spmm(A, X.cuda())
+        Yr, bound = oracle.spmm(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(X))
+        ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y), DT[dname]), Yr, bound, oracle.TAU[DT[dname]])
+        assert ok, f"{layout} N={N}: worst {worst}"
+
+
+def test_spmm_column_independence(bs):
+    """Column n of Y does not depend on N (batch sharding is bit-identical)."""
+    M, K, B, k = 200, 4096, 32, 4
+    W = synth.matrix(M, K, "f16", seed=48).cuda()
+    X = synth.vector(K, "f16", seed=49, n=64).cuda()
+    vals, idx, _ = bs.prune(W, B, k=k)
+    A = bs.pack(vals, idx, K, B, layout="spmm")
+    Y64 = bs.spmm(A, X)
+    for n0, n1 in ((0, 1), (5, 13), (8, 40), (63, 64)):
+        assert torch.equal(bs.spmm(A, X[n0:n1].contiguous()), Y64[n0:n1])
+
+
+def test_spmv_host_e2e(bs):
+    M, K, B, k = 512, 4096, 32, 3
+    W = synth.matrix(M, K, "f16", seed=50)
+    x = synth.vector(K, "f16", seed=51)
+    vals, idx, ov, oi = _prune_parity(bs, W, "f16", B, k)
+    A = bs.pack(vals, idx, K, B)
+    xh = x.pin_memory()
+    yh = torch.empty(M, dtype=torch.float16).pin_memory()
+    xd = torch.empty(K, dtype=torch.float16, device="cuda")
+    yd = torch.empty(M, dtype=torch.float16, device="cuda")
+    bs.spmv_host(A, xh, yh, xd, yd)
+    torch.cuda.synchronize()
+    assert torch.equal(yh, bs.spmv(A, x.cuda()).cpu())
+
+
+def test_errors(bs):
+    W = torch.zeros((4, 30), dtype=torch.float16, device="cuda")
+    with pytest.raises(bs.BSError) as e:
+        bs.prune(W, 16, k=4)
+    assert e.value.status == bs.BS_ERR_SHAPE
+    with pytest.raises(bs.BSError) as e:
+        bs.prune(torch.zeros((4, 32), dtype=torch.float16, device="cuda"), 16, k=17)
+    assert e.value.status == bs.BS_ERR_ARG
+    v, i, _ = bs.prune(torch.zeros((4, 32), dtype=torch.float16, device="cuda"), 8, k=2)
+    with pytest.raises(bs.BSError) as e:
+        bs.pack(v, i, 32, 8, layout="sp24")
+    assert e.value.status == bs.BS_ERR_UNSUPPORTED
+
+
+# ---------------------------------------------------------------- full-size configs (BASELINE configs)
+
+FULL = [
+    ("ptb", 6000, 3008, 32, 3, "f16"),      # configs[1]: 6000x3000 padded to 3008 (A5)
+    ("fc6", 4096, 25088, 32, 3, "f16"),     # configs[2]
+    ("fc7", 4096, 4096, 32, 1, "bf16"),
+    ("fc7f32", 4096, 4096, 32, 16, "f32"),
+    ("ctc_ih", 4096, 2048, 32, 4, "f16"),   # configs[3], 87.5%
+    ("ctc_hh", 4096, 1024, 32, 4, "f16"),
+]
+
+
+@pytest.mark.parametrize("name,M,K,B,k,dname", FULL)
+def test_full_configs(bs, name, M, K, B, k, dname):
+    W = synth.matrix(M, K, dname, seed=synth.seed_for(2, 0))
+    x = synth.vector(K, dname, seed=synth.seed_for(2, 1))
+    vals, idx, ov, oi = _prune_parity(bs, W, dname, B, k)
+    A = bs.pack(vals, idx, K, B)
+    np.testing.assert_array_equal(A.packed.cpu().numpy(), oracle.pack(ov, oi, M, K, B, k, DT[dname], oracle.SPMV))
+    y = bs.spmv(A, x.cuda())
+    yr, bound = oracle.spmv(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(x))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(y), DT[dname]), yr, bound, oracle.TAU[DT[dname]])
+    assert ok, worst
+
+
+def test_full_fc6_spmm32(bs):
+    M, K, B, k, N = 4096, 25088, 32, 3, 32
+    W = synth.matrix(M, K, "f16", seed=synth.seed_for(2, 2))
+    X = synth.vector(K, "f16", seed=synth.seed_for(2, 3), n=N)
+    vals, idx, _ = bs.prune(W.cuda(), B, k=k)
+    A = bs.pack(vals, idx, K, B, layout="spmm")
+    Y = bs.spmm(A, X.cuda())
+    rows = np.random.default_rng(0).choice(M, 256, replace=False).astype(np.int64)
+    ov, oi = synth.to_numpy(vals), _idx_np(idx)
+    Yr, bound = oracle.spmm(ov, oi, oracle.F16, M, K, B, k, synth.to_numpy(X), rows=rows)
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y[:, rows].contiguous()), oracle.F16), Yr, bound, 1e-2)
+    assert ok, worst
+
+
+@pytest.mark.slow
+def test_big_65536_sampled_rows(bs):
+    """configs[4]: 65536x65536 at 90% (k = 3 of 32), exactly as bench.py runs it; checked on sampled rows."""
+    M = K = 65536
+    B, k = 32, 3
+    W = synth.matrix(M, K, "f16", seed=synth.seed_for(4, 0), device="cuda")
+    x = synth.vector(K, "f16", seed=synth.seed_for(4, 1), device="cuda")
+    vals, idx, _ = bs.prune(W, B, k=k)
+    A = bs.pack(vals, idx, K, B)
+    y = bs.spmv(A, x)
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([rng.choice(M, 2048, replace=False), [0, M - 1, 8191, 8192, 32767, 32768]]))
+    rt = torch.from_numpy(rows).cuda()
+    Wr = synth.to_numpy(W[rt])
+    ov, oi = oracle.prune(Wr, oracle.F16, B, k)
+    np.testing.assert_array_equal(_idx_np(idx[rt]), oi)
+    np.testing.assert_array_equal(_raw(vals[rt]), ov.view(np.uint16))
+    yr, bound = oracle.spmv_rowslice(ov, oi, oracle.F16, K, B, k, synth.to_numpy(x))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(y[rt]), oracle.F16), yr, bound, 1e-2)
+    assert ok, worst

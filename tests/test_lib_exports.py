@@ -1,0 +1,70 @@
+"""CPU checks of the C-ABI library: it builds, loads, exports every symbol include/bs.h declares, and its
+pure host helpers agree with the oracle's independent geometry. No device compute is called here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "bs.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(bs_[a-z0-9_]+)\s*\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def bs():
+    from paper_1811_00206_b200 import build
+    build.build()
+    import paper_1811_00206_b200 as bs
+    return bs
+
+
+def test_header_declares_the_boundary():
+    syms = _declared_symbols()
+    for s in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_host", "bs_spmm",
+              "bs_packed_bytes", "bs_k_from_sparsity", "bs_status_str", "bs_version"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(bs):
+    L = ctypes.CDLL(bs.LIB_PATH)
+    for s in _declared_symbols():
+        assert hasattr(L, s), f"{s} not exported"
+    assert set(bs.EXPORTS) == set(_declared_symbols())
+
+
+def test_version_names_sm100a(bs):
+    assert "sm_100a" in bs.version()
+
+
+def test_k_matches_oracle(bs):
+    for B in (1, 4, 16, 25, 32, 100, 1024):
+        for s in (0.0, 0.1, 0.5, 0.7, 0.75, 0.875, 0.9, 0.95, 0.97, 0.999):
+            assert bs.k_from_sparsity(B, s) == oracle.k_from_sparsity(B, s)
+    assert bs.k_from_sparsity(32, 1.0) == -1
+
+
+def test_packed_bytes_matches_oracle(bs):
+    import torch
+    tdt = {oracle.F32: torch.float32, oracle.F16: torch.float16, oracle.BF16: torch.bfloat16}
+    lay = {oracle.SPMV: "spmv", oracle.SPMM: "spmm", oracle.SP24: "sp24"}
+    for M, K, B, k in ((64, 64, 16, 8), (6000, 3008, 32, 3), (4096, 25088, 32, 3), (7, 2048, 512, 9), (5, 96, 1, 1),
+                       (65536, 65536, 32, 3), (33, 1000, 25, 8), (9, 64, 4, 2), (4, 30, 4, 2)):
+        for dt in tdt:
+            for L in lay:
+                assert bs.packed_bytes(M, K, B, k, tdt[dt], lay[L]) == oracle.packed_bytes(M, K, B, k, dt, L)
+
+
+def test_no_oracle_in_product_path():
+    """The product package never imports, links or runs anything under oracle/."""
+    pkg = os.path.join(ROOT, "paper_1811_00206_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text and "liboracle" not in text, f
