@@ -168,8 +168,8 @@ static int64_t align256(int64_t n) { return (n + 255) / 256 * 256; }
 
 typedef struct {
   int64_t V, P, NBf, T;
-  int es, is;                      /* value bytes, index bytes */
-  int64_t offVA, offVB, offIA, offIB, total;
+  int es, is;                 /* value bytes, index bytes */
+  int64_t offA, offB, offC, total;  /* SP24: offA = values, offB = metadata */
 } orc_geom;
 
 static int geom(int64_t M, int64_t K, int B, int k, int dt, int layout, orc_geom* g) {
@@ -186,21 +186,19 @@ static int geom(int64_t M, int64_t K, int B, int k, int dt, int layout, orc_geom
     g->P = 32 * V;
     g->NBf = NB / g->P;
     g->T = NB - g->NBf * g->P;
-    int64_t nA = M * g->NBf * g->P * k, nB = M * g->T * k;
-    g->offVA = 0;
-    g->offVB = g->offVA + align256(nA * g->es);
-    g->offIA = g->offVB + align256(nB * g->es);
-    g->offIB = g->offIA + align256(nA * g->is);
-    g->total = g->offIB + align256(nB * g->is);
+    g->offA = 0;
+    g->offB = align256(M * g->NBf * k * g->P * (g->es + g->is));
+    g->offC = g->offB + align256(M * k * g->T * g->es);
+    g->total = g->offC + align256(M * k * g->T * g->is);
     return 0;
   }
   if (layout == ORC_SP24) {
     if (B != 4 || k != 2 || K % 8 != 0) return -1;
     g->V = g->P = g->NBf = g->T = 0;
-    g->offVA = 0;
-    g->offIA = align256(M * (K / 2) * g->es);
-    g->offVB = g->offIB = 0;
-    g->total = g->offIA + align256(M * (NB / 2));
+    g->offA = 0;
+    g->offB = align256(M * (K / 2) * g->es);
+    g->offC = 0;
+    g->total = g->offB + align256(M * (NB / 2));
     return 0;
   }
   return -1;
@@ -217,7 +215,7 @@ static void put_index(unsigned char* dst, int is, uint16_t v) {
   if (is == 2) dst[1] = (unsigned char)(v >> 8);
 }
 
-/* Reference permutation pi_L(canonical) -> packed bytes. Padding bytes are zero. */
+/* Reference permutation pi_L(canonical) -> packed bytes (docs/layout.md). Padding bytes are zero. */
 int orc_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int B, int k, int dt,
              int layout, void* packed) {
   orc_geom g;
@@ -230,34 +228,39 @@ int orc_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int B,
     for (int64_t r = 0; r < M; ++r)
       for (int64_t b = 0; b < NB; ++b) {
         int64_t pos = (r * NB + b) * 2;
-        memcpy(out + g.offVA + pos * g.es, in + pos * g.es, 2 * g.es);
+        memcpy(out + g.offA + pos * g.es, in + pos * g.es, 2 * g.es);
         int nib = idx[pos] | (idx[pos + 1] << 2);
-        out[g.offIA + r * (NB / 2) + b / 2] |= (unsigned char)(nib << (4 * (b % 2)));
+        out[g.offB + r * (NB / 2) + b / 2] |= (unsigned char)(nib << (4 * (b % 2)));
       }
     return 0;
   }
+  int64_t step_bytes = g.P * (g.es + g.is);
   for (int64_t r = 0; r < M; ++r) {
-    /* full panels: element (r, p, t, l, v) <- canonical (r, b = p*P + v*32 + l, t) */
+    /* region A: step (r, p, t) = P values then P indices; entry (l, v) at position l*V + v,
+     * holding canonical (r, b = p*P + v*32 + l, t) */
     for (int64_t p = 0; p < g.NBf; ++p)
-      for (int t = 0; t < k; ++t)
+      for (int t = 0; t < k; ++t) {
+        unsigned char* step = out + g.offA + ((r * g.NBf + p) * k + t) * step_bytes;
         for (int l = 0; l < 32; ++l)
           for (int64_t v = 0; v < g.V; ++v) {
             int64_t b = p * g.P + v * 32 + l;
             int64_t src = (r * NB + b) * k + t;
-            int64_t dst = ((r * g.NBf + p) * k + t) * g.P + l * g.V + v;
-            memcpy(out + g.offVA + dst * g.es, in + src * g.es, g.es);
-            put_index(out + g.offIA + dst * g.is, g.is, idx[src]);
+            int64_t pos = l * g.V + v;
+            memcpy(step + pos * g.es, in + src * g.es, g.es);
+            put_index(step + g.P * g.es + pos * g.is, g.is, idx[src]);
           }
-    /* tail: element (r, t, v, l) <- canonical (r, b = NBf*P + v*32 + l, t), for v*32 + l < T */
+      }
+    /* regions B (values) and C (indices): entry (r, t, v, l) at element r*k*T + t*T + v*32 + l
+     * (v*32 + l < T), holding canonical (r, b = NBf*P + v*32 + l, t) */
     for (int t = 0; t < k; ++t)
       for (int64_t v = 0; v * 32 < g.T; ++v)
         for (int l = 0; l < 32; ++l) {
           if (v * 32 + l >= g.T) continue;
           int64_t b = g.NBf * g.P + v * 32 + l;
           int64_t src = (r * NB + b) * k + t;
-          int64_t dst = (r * k + t) * g.T + v * 32 + l;
-          memcpy(out + g.offVB + dst * g.es, in + src * g.es, g.es);
-          put_index(out + g.offIB + dst * g.is, g.is, idx[src]);
+          int64_t pos = r * k * g.T + t * g.T + v * 32 + l;
+          memcpy(out + g.offB + pos * g.es, in + src * g.es, g.es);
+          put_index(out + g.offC + pos * g.is, g.is, idx[src]);
         }
   }
   return 0;

@@ -27,7 +27,7 @@ struct Geom {
   int64_t P;    // 32*V blocks per panel
   int64_t NBf;  // full panels per row
   int64_t T;    // tail blocks per row
-  int64_t offVA, offVB, offIA, offIB, total;
+  int64_t offA, offB, offC, total;  // SPMV/SPMM: panel steps, tail values, tail indices. SP24: values, metadata.
 };
 
 // Returns false on invalid arguments.
@@ -45,21 +45,20 @@ inline bool make_geom(int64_t M, int64_t K, int B, int k, int dt, int layout, Ge
     g->P = 32LL * V;
     g->NBf = g->NB / g->P;
     g->T = g->NB - g->NBf * g->P;
-    int64_t nA = M * g->NBf * g->P * k, nB = M * g->T * k;
-    g->offVA = 0;
-    g->offVB = g->offVA + align_up(nA * g->es, kAlign);
-    g->offIA = g->offVB + align_up(nB * g->es, kAlign);
-    g->offIB = g->offIA + align_up(nA * g->is, kAlign);
-    g->total = g->offIB + align_up(nB * g->is, kAlign);
+    // region A: M·NBf·k steps of P·(es + is) bytes; B / C: tail values / indices (M·k·T each)
+    g->offA = 0;
+    g->offB = align_up(M * g->NBf * k * g->P * (g->es + g->is), kAlign);
+    g->offC = g->offB + align_up(M * k * g->T * g->es, kAlign);
+    g->total = g->offC + align_up(M * k * g->T * g->is, kAlign);
     return true;
   }
   if (layout == BS_LAYOUT_SP24) {
     if (B != 4 || k != 2 || K % 8 != 0) return false;
     g->V = 0; g->P = 0; g->NBf = 0; g->T = 0;
-    g->offVA = 0;
-    g->offIA = align_up(M * (K / 2) * g->es, kAlign);
-    g->offVB = g->offIB = 0;
-    g->total = g->offIA + align_up(M * (g->NB / 2), kAlign);
+    g->offA = 0;
+    g->offB = align_up(M * (K / 2) * g->es, kAlign);
+    g->offC = 0;
+    g->total = g->offB + align_up(M * (g->NB / 2), kAlign);
     return true;
   }
   return false;

@@ -1,8 +1,8 @@
 // pack.cu: K2 bs_pack / bs_unpack, pure permutations between canonical and packed layouts.
 //
 // The layout is written from docs/layout.md. One thread per packed entry computes the canonical
-// source (gather), so packed writes are coalesced. The paper describes no W layout;
-// the layout choice is explained in DESIGN.md §4.
+// source (gather), so packed writes are close to coalesced. The paper describes no W layout (SURVEY
+// A12); the layout choice is explained in DESIGN.md §4.
 #include "bs_common.cuh"
 
 namespace {
@@ -10,51 +10,50 @@ namespace {
 struct PackArgs {
   int64_t M, NB, NBf, T, P;
   int V, k, es, is;
+  int64_t offA, offB, offC;
 };
-
-// Packed entry e of region VA (e < M*NBf*P*k) or VB -> canonical linear position (r*NB + b)*k + t.
-__device__ __forceinline__ int64_t src_of_A(const PackArgs& a, int64_t e) {
-  // e = ((r*NBf + p)*k + t)*P + l*V + v
-  const int64_t lv = e % a.P;
-  const int64_t q = e / a.P;  // (r*NBf + p)*k + t
-  const int t = (int)(q % a.k);
-  const int64_t rp = q / a.k;  // r*NBf + p
-  const int64_t p = rp % a.NBf, r = rp / a.NBf;
-  const int l = (int)(lv / a.V), v = (int)(lv % a.V);
-  const int64_t b = p * a.P + (int64_t)v * 32 + l;
-  return (r * a.NB + b) * a.k + t;
-}
-
-__device__ __forceinline__ int64_t src_of_B(const PackArgs& a, int64_t e) {
-  // e = (r*k + t)*T + v*32 + l
-  const int64_t vl = e % a.T;
-  const int64_t q = e / a.T;
-  const int t = (int)(q % a.k);
-  const int64_t r = q / a.k;
-  const int64_t b = a.NBf * a.P + vl;  // v*32 + l == vl
-  return (r * a.NB + b) * a.k + t;
-}
 
 template <typename VT>
 __global__ void pack_kernel(const VT* __restrict__ vals, const uint16_t* __restrict__ idx, PackArgs a,
-                            VT* __restrict__ VA, VT* __restrict__ VB, uint8_t* __restrict__ IA,
-                            uint8_t* __restrict__ IB, int64_t nA, int64_t nB, bool unpack,
+                            uint8_t* __restrict__ base, int64_t nA, int64_t nB, bool unpack,
                             VT* __restrict__ out_vals, uint16_t* __restrict__ out_idx) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t step_bytes = a.P * (a.es + a.is);
+  const int64_t kT = (int64_t)a.k * a.T;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nA + nB; e += stride) {
-    const bool inA = e < nA;
-    const int64_t ee = inA ? e : e - nA;
-    const int64_t src = inA ? src_of_A(a, ee) : src_of_B(a, ee);
-    VT* vdst = inA ? VA : VB;
-    uint8_t* idst = inA ? IA : IB;
-    if (!unpack) {
-      vdst[ee] = vals[src];
-      const uint16_t o = idx[src];
-      if (a.is == 1) idst[ee] = (uint8_t)o;
-      else { idst[2 * ee] = (uint8_t)(o & 0xff); idst[2 * ee + 1] = (uint8_t)(o >> 8); }
+    int64_t src;
+    uint8_t* vdst;
+    uint8_t* idst;
+    if (e < nA) {
+      // region A: step s = (r·NBf + p)·k + t holds P values then P indices; position l·V + v
+      const int64_t s = e / a.P, pos = e - s * a.P;
+      const int t = (int)(s % a.k);
+      const int64_t rp = s / a.k;  // r·NBf + p
+      const int64_t p = rp % a.NBf, r = rp / a.NBf;
+      const int l = (int)(pos / a.V), v = (int)(pos % a.V);
+      const int64_t b = p * a.P + (int64_t)v * 32 + l;
+      src = (r * a.NB + b) * a.k + t;
+      uint8_t* step = base + a.offA + s * step_bytes;
+      vdst = step + pos * a.es;
+      idst = step + a.P * a.es + pos * a.is;
     } else {
-      out_vals[src] = vdst[ee];
-      out_idx[src] = a.is == 1 ? (uint16_t)idst[ee] : (uint16_t)(idst[2 * ee] | (idst[2 * ee + 1] << 8));
+      // regions B / C: tail values / indices; element r·k·T + t·T + (v·32 + l)
+      const int64_t f = e - nA;
+      const int64_t r = f / kT, q = f - r * kT;
+      const int t = (int)(q / a.T);
+      const int64_t b = a.NBf * a.P + (q - (int64_t)t * a.T);
+      src = (r * a.NB + b) * a.k + t;
+      vdst = base + a.offB + f * a.es;
+      idst = base + a.offC + f * a.is;
+    }
+    if (!unpack) {
+      *(VT*)vdst = vals[src];
+      const uint16_t o = idx[src];
+      idst[0] = (uint8_t)(o & 0xff);
+      if (a.is == 2) idst[1] = (uint8_t)(o >> 8);
+    } else {
+      out_vals[src] = *(const VT*)vdst;
+      out_idx[src] = a.is == 1 ? (uint16_t)idst[0] : (uint16_t)(idst[0] | (idst[1] << 8));
     }
   }
 }
@@ -91,37 +90,35 @@ cudaError_t run(const bsk::Geom& g, const void* vals, const uint16_t* idx, void*
     const int64_t nmeta = g.M * (g.NB / 2);
     if (!unpack) {
       if ((err = cudaMemcpyAsync(base, vals, (size_t)(nv * g.es), cudaMemcpyDeviceToDevice, s))) return err;
-      if ((err = zero_gap(base, nv * g.es, g.offIA, s))) return err;
-      if ((err = zero_gap(base, g.offIA + nmeta, g.total, s))) return err;
+      if ((err = zero_gap(base, nv * g.es, g.offB, s))) return err;
+      if ((err = zero_gap(base, g.offB + nmeta, g.total, s))) return err;
     } else {
       if ((err = cudaMemcpyAsync(out_vals, base, (size_t)(nv * g.es), cudaMemcpyDeviceToDevice, s))) return err;
     }
     int64_t blocks = (nmeta + 255) / 256;
     if (blocks > (int64_t)sms * 32) blocks = (int64_t)sms * 32;
     if (blocks < 1) blocks = 1;
-    sp24_meta_kernel<<<(unsigned)blocks, 256, 0, s>>>(idx, nmeta, base + g.offIA, unpack, out_idx);
+    sp24_meta_kernel<<<(unsigned)blocks, 256, 0, s>>>(idx, nmeta, base + g.offB, unpack, out_idx);
     return cudaGetLastError();
   }
   PackArgs a;
   a.M = g.M; a.NB = g.NB; a.NBf = g.NBf; a.T = g.T; a.P = g.P; a.V = g.V; a.k = g.k; a.es = g.es; a.is = g.is;
+  a.offA = g.offA; a.offB = g.offB; a.offC = g.offC;
   const int64_t nA = g.M * g.NBf * g.P * g.k, nB = g.M * g.T * g.k;
   if (!unpack) {
-    if ((err = zero_gap(base, nA * g.es, g.offVB, s))) return err;
-    if ((err = zero_gap(base, g.offVB + nB * g.es, g.offIA, s))) return err;
-    if ((err = zero_gap(base, g.offIA + nA * g.is, g.offIB, s))) return err;
-    if ((err = zero_gap(base, g.offIB + nB * g.is, g.total, s))) return err;
+    if ((err = zero_gap(base, nA * (g.es + g.is), g.offB, s))) return err;
+    if ((err = zero_gap(base, g.offB + nB * g.es, g.offC, s))) return err;
+    if ((err = zero_gap(base, g.offC + nB * g.is, g.total, s))) return err;
   }
   if (nA + nB == 0) return cudaSuccess;
   int64_t blocks = (nA + nB + 255) / 256;
   if (blocks > (int64_t)sms * 32) blocks = (int64_t)sms * 32;
   if (g.es == 4) {
-    pack_kernel<uint32_t><<<(unsigned)blocks, 256, 0, s>>>(
-        (const uint32_t*)vals, idx, a, (uint32_t*)(base + g.offVA), (uint32_t*)(base + g.offVB),
-        base + g.offIA, base + g.offIB, nA, nB, unpack, (uint32_t*)out_vals, out_idx);
+    pack_kernel<uint32_t><<<(unsigned)blocks, 256, 0, s>>>((const uint32_t*)vals, idx, a, base, nA, nB, unpack,
+                                                          (uint32_t*)out_vals, out_idx);
   } else {
-    pack_kernel<uint16_t><<<(unsigned)blocks, 256, 0, s>>>(
-        (const uint16_t*)vals, idx, a, (uint16_t*)(base + g.offVA), (uint16_t*)(base + g.offVB),
-        base + g.offIA, base + g.offIB, nA, nB, unpack, (uint16_t*)out_vals, out_idx);
+    pack_kernel<uint16_t><<<(unsigned)blocks, 256, 0, s>>>((const uint16_t*)vals, idx, a, base, nA, nB, unpack,
+                                                          (uint16_t*)out_vals, out_idx);
   }
   return cudaGetLastError();
 }

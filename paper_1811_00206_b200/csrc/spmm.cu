@@ -21,10 +21,9 @@ constexpr int kThreads = 256;
 constexpr int kRT = 32;  // rows per CTA tile
 
 struct SpmmArgs {
-  const uint8_t* VA;
-  const uint8_t* VB;
-  const uint8_t* IA;
-  const uint8_t* IB;
+  const uint8_t* A;   // panel steps: 32 values then 32 indices per step (V = 1)
+  const uint8_t* Bt;  // tail values (element r·k·T + t·T + lane)
+  const uint8_t* Ct;  // tail indices (same order)
   const void* X;
   void* Y;
   int64_t M, K, NB, NBf, T, N, ldx, ldy;
@@ -132,15 +131,16 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpmmArgs a) {
         const uint32_t sl = sx + lane * 16;
         if (!tail_chunk) {
           const int64_t s_begin = p0 * a.k, s_end = (p0 + ng) * a.k;
-          const raw_t* vp = (const raw_t*)a.VA + r * S * 32 + lane;
-          const uint8_t* ip = a.IA + (r * S * 32 + lane) * IS;
+          constexpr int STEPB = 32 * (ES + IS);
+          const raw_t* vp = (const raw_t*)(a.A + r * S * STEPB) + lane;        // + s·STEPB bytes
+          const uint8_t* ip = a.A + r * S * STEPB + 32 * ES + lane * IS;
           for (int64_t s0 = s_begin; s0 < s_end; s0 += U) {
             uint32_t wv[U], iv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               if (s0 + u < s_end) {
-                wv[u] = vp[(s0 + u) * 32];
-                iv[u] = IS == 1 ? (uint32_t)ip[(s0 + u) * 32] : (uint32_t)((const uint16_t*)ip)[(s0 + u) * 32];
+                wv[u] = *(const raw_t*)((const uint8_t*)vp + (s0 + u) * STEPB);
+                iv[u] = IS == 1 ? (uint32_t)ip[(s0 + u) * STEPB] : (uint32_t)*(const uint16_t*)(ip + (s0 + u) * STEPB);
               }
             }
 #pragma unroll
@@ -162,8 +162,8 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpmmArgs a) {
             }
           }
         } else {
-          const raw_t* vb = (const raw_t*)a.VB + r * a.k * a.T;
-          const uint8_t* ib = a.IB + r * a.k * a.T * IS;
+          const raw_t* vb = (const raw_t*)a.Bt + r * a.k * a.T;
+          const uint8_t* ib = a.Ct + r * a.k * a.T * IS;
           if (lane < a.T) {
             for (int t = 0; t < a.k; ++t) {
               const uint32_t w = vb[t * a.T + lane];
@@ -241,7 +241,7 @@ cudaError_t bsk_launch_spmm(const bsk::Geom& g, const void* packed, const void* 
   if (smem > bsk::dev_props().smem_optin) return cudaErrorNotSupported;
   SpmmArgs a;
   const uint8_t* base = (const uint8_t*)packed;
-  a.VA = base + g.offVA; a.VB = base + g.offVB; a.IA = base + g.offIA; a.IB = base + g.offIB;
+  a.A = base + g.offA; a.Bt = base + g.offB; a.Ct = base + g.offC;
   a.X = X; a.Y = Y;
   a.M = g.M; a.K = g.K; a.NB = g.NB; a.NBf = g.NBf; a.T = g.T; a.N = N; a.ldx = ldx; a.ldy = ldy;
   a.B = g.B; a.k = g.k; a.CP = CP;

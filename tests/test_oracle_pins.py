@@ -273,12 +273,12 @@ def test_pack_spmv_steps_closed_form():
     vals = np.stack([blk * 10 + 0, blk * 10 + 1], axis=-1).astype(np.float32).reshape(1, 128, 2)
     idx = np.tile(np.array([0, 1], dtype=np.uint16), (1, 128, 1))
     buf = oracle.pack(vals, idx, 1, K, B, k, oracle.F32, oracle.SPMV)
-    va = buf[:128 * 2 * 4].view(np.float32).reshape(2, 128)
+    assert buf.size == 1280  # 2 steps x (128 values x 4 B + 128 indices x 1 B), 256-aligned
     for t in range(2):
+        step = buf[t * 640:(t + 1) * 640]  # a step = its 128 values, then its 128 indices
         want = (blk.reshape(4, 32).T.reshape(-1) * 10 + t).astype(np.float32)
-        np.testing.assert_array_equal(va[t], want)
-    ia = buf[1024:1024 + 256]
-    np.testing.assert_array_equal(ia.reshape(2, 128), np.array([[0] * 128, [1] * 128], dtype=np.uint8))
+        np.testing.assert_array_equal(step[:512].view(np.float32), want)
+        np.testing.assert_array_equal(step[512:], np.full(128, t, dtype=np.uint8))
 
 
 @pytest.mark.parametrize("layout", [oracle.SPMV, oracle.SPMM])
@@ -297,12 +297,18 @@ def test_pack_is_a_permutation(layout, M, K, B, k, dt, dname):
     V = 1
     while V * 2 <= vmax and 64 * V <= NB:
         V *= 2
-    nA = M * (NB // (32 * V)) * 32 * V * k
+    P = 32 * V
+    nA = M * (NB // P) * P * k
     nB = n - nA
+    T = NB - (NB // P) * P
     a = lambda x: (x + 255) // 256 * 256
-    offs = [0, a(nA * es), a(nA * es) + a(nB * es), a(nA * es) + a(nB * es) + a(nA * isz)]
-    vraw = np.concatenate([buf[offs[0]:offs[0] + nA * es], buf[offs[1]:offs[1] + nB * es]])
-    iraw = np.concatenate([buf[offs[2]:offs[2] + nA * isz], buf[offs[3]:offs[3] + nB * isz]])
+    A = buf[:nA * (es + isz)].reshape(-1, P * (es + isz))           # steps: P values then P indices
+    offB = a(nA * (es + isz))
+    offC = offB + a(nB * es)
+    assert buf.size == offC + a(nB * isz)
+    vraw = np.concatenate([A[:, :P * es].reshape(-1), buf[offB:offB + nB * es]])   # tail values (region B)
+    iraw = np.concatenate([A[:, P * es:].reshape(-1), buf[offC:offC + nB * isz]])  # tail indices (region C)
+    assert T * M * k == nB
     pv = vraw.view(np.uint32 if es == 4 else np.uint16).astype(np.uint64)
     pi = iraw.view(np.uint8 if isz == 1 else np.uint16).astype(np.uint64)
     cv = vals.reshape(-1).view(np.uint32 if es == 4 else np.uint16).astype(np.uint64)

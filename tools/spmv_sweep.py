@@ -11,7 +11,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-SHAPES = [("big", 65536, 65536), ("fc6", 4096, 25088), ("fc7", 4096, 4096), ("ptb", 6000, 3008)]
+SHAPES = [("big", 65536, 65536), ("fc6", 4096, 25088), ("fc7", 4096, 4096), ("ptb", 6000, 3008), ("ctc_ih", 4096, 2048), ("ctc_hh", 4096, 1024)]
 SPARS = [0.5, 0.9, 0.97]
 
 
@@ -21,11 +21,11 @@ def child():
     import synth
     dev = torch.device("cuda", 0)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    shapes = [s for s in SHAPES if s[0] in os.environ.get("SHAPES", "big,fc6,fc7,ptb").split(",")]
+    shapes = [s for s in SHAPES if s[0] in os.environ.get("SHAPES", "big,fc6,fc7,ptb,ctc_ih,ctc_hh").split(",")]
     for name, M, K in shapes:
         W = synth.matrix(M, K, "f16", seed=1, device=dev)
         x = synth.vector(K, "f16", seed=2, device=dev)
-        for s in SPARS:
+        for s in (SPARS if not name.startswith("ctc") else [0.875]):
             k = bs.k_from_sparsity(32, s)
             v, i, _ = bs.prune(W, 32, k=k)
             A = bs.pack(v, i, K, 32)
