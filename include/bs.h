@@ -105,7 +105,8 @@ int bs_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int blo
 int bs_unpack(const void* packed, int64_t M, int64_t K, int block, int k, int dt, int layout,
               void* vals, uint16_t* idx, void* stream);
 
-/* bs_spmv: y = W_bs · x (Eq. 1, with B = 0; batch 1). A must be in layout SPMV or SPMM.
+/* bs_spmv: y = W_bs · x (Eq. 1, with B = 0; batch 1). A must be in layout SPMV
+ * (BS_ERR_UNSUPPORTED otherwise).
  *   x  device, K elements of A->dt;  y  device out, M elements of A->dt.
  * Products are exact in fp32 for f16/bf16, and accumulation is fp32 in a fixed order that does not
  * depend on the row range (so row-sharded results are bit-identical). y is rounded to nearest even.
@@ -123,9 +124,10 @@ int bs_spmv_host(const bs_matrix* A, const void* x_host, void* y_host, void* x_d
 /* bs_spmm: Y = W_bs · X for a batch of N columns (Fig. `benchmark`(b), "batchsize = 8").
  *   X  device, column n at X + n·ldx (K elements each), i.e. torch [N, K] with row stride ldx
  *   Y  device out, column n at Y + n·ldy (M elements each), i.e. torch [N, M]
- * A must be in layout SPMM or SPMV. Column n of Y depends only on column n of X, with an order of
- * fp32 accumulation that does not depend on N or on the position of the column in the batch. So
- * batch-sharded SpMM reproduces the unsharded columns bit for bit.
+ * Layout SPMM (128-row tiles): f16/bf16 with B dividing 64 run on the tensor cores (tcgen05.mma,
+ * decompressed W tiles, fp32 accumulate in tensor memory); other cases use CUDA cores. Layout SPMV:
+ * one SpMV per column. Column n of Y depends only on column n of X, with a fixed order of fp32
+ * accumulation over K, so batch-sharded SpMM reproduces the unsharded columns.
  * Errors: BS_ERR_ARG if N < 1, ldx < K or ldy < M. */
 int bs_spmm(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, void* Y, int64_t ldy,
             void* stream);

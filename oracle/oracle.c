@@ -166,6 +166,13 @@ int orc_decode(const void* vals, const uint16_t* idx, int dt, int64_t M, int64_t
 
 static int64_t align256(int64_t n) { return (n + 255) / 256 * 256; }
 
+static int64_t pad16(int64_t n) { return (n + 15) / 16 * 16; }
+
+/* bytes of one SPMM blob: mt rows x cb blocks x k entries, values then indices, each 16-padded */
+static int64_t blob_bytes(int64_t mt, int64_t cb, int k, int es, int is) {
+  return pad16(mt * cb * k * es) + pad16(mt * cb * k * is);
+}
+
 typedef struct {
   int64_t V, P, NBf, T;
   int es, is;                 /* value bytes, index bytes */
@@ -178,8 +185,23 @@ static int geom(int64_t M, int64_t K, int B, int k, int dt, int layout, orc_geom
   int64_t NB = K / B;
   g->es = dtype_size(dt);
   g->is = B <= 256 ? 1 : 2;
-  if (layout == ORC_SPMV || layout == ORC_SPMM) {
-    int64_t vmax = layout == ORC_SPMM ? 1 : 16 / g->es;
+  if (layout == ORC_SPMM) {
+    /* docs/layout.md SPMM: 128-row tiles x CB-block chunks, one 16-byte-padded blob each */
+    g->V = B <= 64 ? (64 + B - 1) / B : 1; /* CB (chunk blocks) kept in V */
+    g->P = (M + 127) / 128;                /* MT */
+    g->NBf = (NB + g->V - 1) / g->V;       /* NC */
+    g->T = 0;
+    int64_t mt_last = M - 128 * (g->P - 1), cb_last = NB - g->V * (g->NBf - 1);
+    int64_t tb_full = (g->NBf - 1) * blob_bytes(128, g->V, k, g->es, g->is) + blob_bytes(128, cb_last, k, g->es, g->is);
+    int64_t tb_last = (g->NBf - 1) * blob_bytes(mt_last, g->V, k, g->es, g->is) + blob_bytes(mt_last, cb_last, k, g->es, g->is);
+    g->offA = 0;
+    g->offB = tb_full; /* tile stride */
+    g->offC = 0;
+    g->total = align256((g->P - 1) * tb_full + tb_last);
+    return 0;
+  }
+  if (layout == ORC_SPMV) {
+    int64_t vmax = 16 / g->es;
     int64_t V = 1;
     while (V * 2 <= vmax && 32 * V * 2 <= NB) V *= 2;
     g->V = V;
@@ -232,6 +254,26 @@ int orc_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int B,
         int nib = idx[pos] | (idx[pos + 1] << 2);
         out[g.offB + r * (NB / 2) + b / 2] |= (unsigned char)(nib << (4 * (b % 2)));
       }
+    return 0;
+  }
+  if (layout == ORC_SPMM) {
+    int64_t CB = g.V, MT = g.P, NC = g.NBf;
+    for (int64_t t = 0; t < MT; ++t) {
+      int64_t mt = M - 128 * t < 128 ? M - 128 * t : 128;
+      for (int64_t c = 0; c < NC; ++c) {
+        int64_t cb = NB - CB * c < CB ? NB - CB * c : CB;
+        unsigned char* blob = out + t * g.offB + c * blob_bytes(mt, CB, k, g.es, g.is);
+        int64_t nvb = pad16(mt * cb * k * g.es);
+        for (int64_t r = 0; r < mt; ++r)
+          for (int64_t j = 0; j < cb; ++j)
+            for (int tt = 0; tt < k; ++tt) {
+              int64_t pos = (r * cb + j) * k + tt;
+              int64_t src = ((128 * t + r) * NB + CB * c + j) * k + tt;
+              memcpy(blob + pos * g.es, in + src * g.es, g.es);
+              put_index(blob + nvb + pos * g.is, g.is, idx[src]);
+            }
+      }
+    }
     return 0;
   }
   int64_t step_bytes = g.P * (g.es + g.is);

@@ -141,7 +141,7 @@ int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream) {
   int st = matrix_geom(A, &g);
   if (st) return st;
   if (!x || !y) return BS_ERR_ARG;
-  if (g.layout == BS_LAYOUT_SP24) return BS_ERR_UNSUPPORTED;
+  if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;  // SPMM tiles / SP24 feed bs_spmm
   return from_cuda(bsk_launch_spmv(g, A->packed, x, y, (cudaStream_t)stream));
 }
 
@@ -168,8 +168,9 @@ int bs_spmm(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, void* Y, 
   if (g.layout == BS_LAYOUT_SP24) return BS_ERR_UNSUPPORTED;
   cudaError_t e = bsk_launch_spmm(g, A->packed, X, N, ldx, Y, ldy, (cudaStream_t)stream);
   if (e != cudaErrorNotSupported) return from_cuda(e);
-  // Column-at-a-time fallback for layouts/shapes the batched kernel does not cover (SPMV layout
-  // with V > 1, or very wide blocks): every column runs the SpMV kernel.
+  // SPMV layout: passes of 8 batch columns through the SpMV kernel (16-bit), or one SpMV per column
+  e = bsk_launch_spmv_batch(g, A->packed, X, N, ldx, Y, ldy, (cudaStream_t)stream);
+  if (e != cudaErrorNotSupported) return from_cuda(e);
   const size_t es = (size_t)g.es;
   for (int64_t n = 0; n < N; ++n) {
     e = bsk_launch_spmv(g, A->packed, (const char*)X + (size_t)(n * ldx) * es, (char*)Y + (size_t)(n * ldy) * es,

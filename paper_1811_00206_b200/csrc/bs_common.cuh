@@ -37,8 +37,28 @@ inline bool make_geom(int64_t M, int64_t K, int B, int k, int dt, int layout, Ge
   g->M = M; g->K = K; g->NB = K / B; g->B = B; g->k = k; g->dt = dt; g->layout = layout;
   g->es = dtype_bytes(dt);
   g->is = B <= 256 ? 1 : 2;
-  if (layout == BS_LAYOUT_SPMV || layout == BS_LAYOUT_SPMM) {
-    int vmax = layout == BS_LAYOUT_SPMM ? 1 : 16 / g->es;
+  if (layout == BS_LAYOUT_SPMM) {
+    // docs/layout.md SPMM: 128-row tiles x CB-block chunks; V holds CB, P the row tiles, NBf the
+    // chunks, offB the byte stride of a full row tile.
+    const int64_t CB = B <= 64 ? (64 + B - 1) / B : 1;
+    g->V = (int)CB;
+    g->P = (M + 127) / 128;
+    g->NBf = (g->NB + CB - 1) / CB;
+    g->T = 0;
+    const int64_t mt_last = M - 128 * (g->P - 1), cb_last = g->NB - CB * (g->NBf - 1);
+    auto blob = [&](int64_t mt, int64_t cb) {
+      return align_up(mt * cb * k * g->es, 16) + align_up(mt * cb * k * g->is, 16);
+    };
+    const int64_t tb_full = (g->NBf - 1) * blob(128, CB) + blob(128, cb_last);
+    const int64_t tb_last = (g->NBf - 1) * blob(mt_last, CB) + blob(mt_last, cb_last);
+    g->offA = 0;
+    g->offB = tb_full;
+    g->offC = 0;
+    g->total = align_up((g->P - 1) * tb_full + tb_last, kAlign);
+    return true;
+  }
+  if (layout == BS_LAYOUT_SPMV) {
+    int vmax = 16 / g->es;
     int V = 1;
     while (V * 2 <= vmax && 32LL * V * 2 <= g->NB) V *= 2;
     g->V = V;
@@ -83,5 +103,7 @@ cudaError_t bsk_launch_unpack(const void* packed, const bsk::Geom& g, void* vals
                               cudaStream_t s);
 cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y,
                             cudaStream_t s);
+cudaError_t bsk_launch_spmv_batch(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,
+                                  void* Y, int64_t ldy, cudaStream_t s);
 cudaError_t bsk_launch_spmm(const bsk::Geom& g, const void* packed, const void* X, int64_t N,
                             int64_t ldx, void* Y, int64_t ldy, cudaStream_t s);

@@ -75,6 +75,42 @@ __global__ void sp24_meta_kernel(const uint16_t* __restrict__ idx, int64_t nbyte
   }
 }
 
+// SPMM layout (docs/layout.md): one thread per canonical entry src = (r·NB + b)·k + t'; its blob is
+// (tile r/128, chunk b/CB), position ((r mod 128)·cb + b mod CB)·k + t'.
+template <typename VT>
+__global__ void pack_spmm_kernel(const VT* __restrict__ vals, const uint16_t* __restrict__ idx, int64_t M, int64_t NB,
+                                 int k, int CB, int is, int64_t tile_stride, uint8_t* __restrict__ base, bool unpack,
+                                 VT* __restrict__ out_vals, uint16_t* __restrict__ out_idx) {
+  constexpr int es = sizeof(VT);
+  const int64_t n = M * NB * k;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t NCh = (NB + CB - 1) / CB;
+  for (int64_t src = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; src < n; src += stride) {
+    const int tp = (int)(src % k);
+    const int64_t rb = src / k;
+    const int64_t b = rb % NB, r = rb / NB;
+    const int64_t t = r / 128, rl = r - t * 128;
+    const int64_t mt = (M - 128 * t) < 128 ? (M - 128 * t) : 128;
+    const int64_t c = b / CB, j = b - c * CB;
+    const int64_t cb = (NB - CB * c) < CB ? (NB - CB * c) : CB;
+    const int64_t blobCB = bsk::align_up(mt * CB * k * es, 16) + bsk::align_up(mt * CB * k * is, 16);
+    uint8_t* blob = base + t * tile_stride + c * blobCB;
+    const int64_t pos = (rl * cb + j) * k + tp;
+    uint8_t* vdst = blob + pos * es;
+    uint8_t* idst = blob + bsk::align_up(mt * cb * k * es, 16) + pos * is;
+    (void)NCh;
+    if (!unpack) {
+      *(VT*)vdst = vals[src];
+      const uint16_t o = idx[src];
+      idst[0] = (uint8_t)(o & 0xff);
+      if (is == 2) idst[1] = (uint8_t)(o >> 8);
+    } else {
+      out_vals[src] = *(const VT*)vdst;
+      out_idx[src] = is == 1 ? (uint16_t)idst[0] : (uint16_t)(idst[0] | (idst[1] << 8));
+    }
+  }
+}
+
 cudaError_t zero_gap(uint8_t* base, int64_t from, int64_t to, cudaStream_t s) {
   if (to > from) return cudaMemsetAsync(base + from, 0, (size_t)(to - from), s);
   return cudaSuccess;
@@ -99,6 +135,20 @@ cudaError_t run(const bsk::Geom& g, const void* vals, const uint16_t* idx, void*
     if (blocks > (int64_t)sms * 32) blocks = (int64_t)sms * 32;
     if (blocks < 1) blocks = 1;
     sp24_meta_kernel<<<(unsigned)blocks, 256, 0, s>>>(idx, nmeta, base + g.offB, unpack, out_idx);
+    return cudaGetLastError();
+  }
+  if (g.layout == BS_LAYOUT_SPMM) {
+    if (!unpack && (err = cudaMemsetAsync(base, 0, (size_t)g.total, s))) return err;  // blob padding
+    const int64_t n = g.M * g.NB * g.k;
+    if (n == 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > (int64_t)sms * 32) blocks = (int64_t)sms * 32;
+    if (g.es == 4)
+      pack_spmm_kernel<uint32_t><<<(unsigned)blocks, 256, 0, s>>>((const uint32_t*)vals, idx, g.M, g.NB, g.k, g.V, g.is,
+                                                                 g.offB, base, unpack, (uint32_t*)out_vals, out_idx);
+    else
+      pack_spmm_kernel<uint16_t><<<(unsigned)blocks, 256, 0, s>>>((const uint16_t*)vals, idx, g.M, g.NB, g.k, g.V, g.is,
+                                                                 g.offB, base, unpack, (uint16_t*)out_vals, out_idx);
     return cudaGetLastError();
   }
   PackArgs a;

@@ -1,542 +1,20 @@
-// spmv.cu: K3 bs_spmv, y = W_bs · x for a balanced-sparse W in the SPMV (or SPMM) layout.
-//
-// Paper design (Fig. 3): one thread per block partition; every thread gets the same
-// work because every block keeps k entries; x is "rearranged and stored in shared memory to
-// avoid bank conflicts". The B200 version:
-//   - A warp walks a contiguous range of rows. Lane l owns the blocks b ≡ l (mod 32), V of them per
-//     panel of 32·V blocks (docs/layout.md). A row's panel steps are contiguous in HBM, each step
-//     being 32·V values followed by their 32·V indices.
-//   - Steps reach shared memory through the TMA bulk-copy engine (cp.async.bulk, SASS UBLKCP): each
-//     warp owns a ring of NS stages of up to Q steps, one bulk copy per stage. Lane 0 refills a stage
-//     as soon as the warp has consumed it, and mbarriers with transaction counts signal arrival. So
-//     the bytes in flight do not depend on register pressure or on the compute phase
-//     (tools/membench.cu: >= 6.9 TB/s at 64 KB in flight per SM).
-//   - x is staged per CTA in a block-interleaved order of 32-bit slots: element (b, o) of a chunk
-//     goes to word (gl·B + o)·32 + (b & 31), with gl = (b>>5) - first group of the chunk. 16-bit
-//     values sit zero-extended in the low half. Lane l only ever touches bank l, whatever the
-//     indices are, so every gather is conflict-free by construction. The slot address is one
-//     IMAD of the index byte (extracted by one PRMT): 4 instructions per nonzero including the
-//     FHFMA. Staging is lane-per-block too, so its stores are conflict-free; all of a lane's loads
-//     are issued before its stores.
-//   - K is processed in chunks of whole panels when x does not fit in shared memory (65536 columns
-//     of 16-bit x take 256 KB as slots). Each (row, chunk) partial is reduced by the warp and added
-//     in chunk order. The tail blocks (T < 32·V per row) follow through the same ring.
-//   - f16/bf16 products are one FHFMA (exact 16x16 product, fp32 accumulate). Each lane keeps V
-//     independent accumulators. They are summed in a fixed order and reduced with a warp butterfly.
-//     Chunking depends only on (K, B, dtype), never on the row range, so row-sharded results are
-//     bit-identical to unsharded ones.
-//   - The grid is persistent, one CTA per SM. Each CTA owns a contiguous, balanced row range.
-#include "bs_common.cuh"
-#include "bs_device.cuh"
+// spmv.cu: host side of K3 bs_spmv and of the batched (8 columns per pass) variant: argument set-up,
+// K-chunking and dispatch to the per-dtype instantiations (spmv_f16.cu, spmv_bf16.cu, spmv_f32.cu).
+// The kernel and its design notes are in spmv_impl.cuh.
+#include "spmv_impl.cuh"
 
-#include <stdlib.h>
+using bsk_spmv::SpmvArgs;
+using bsk_spmv::kXBudget;
+using bsk_spmv::kMaxChunks;
 
-#ifdef BS_TRACE
-// Debug timeline (tools/trace_probe.py): %globaltimer at phase boundaries, per (CTA, warp).
-__device__ unsigned long long g_bs_trace[1024 * 16 * 8];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define BS_MARK(i)                                                                                       \
-  do {                                                                                                   \
-    if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < 16)                                              \
-      g_bs_trace[(blockIdx.x * 16 + (threadIdx.x >> 5)) * 8 + (i)] = gtime();                            \
-  } while (0)
-extern "C" int bs_trace_read(void* host, int n) {
-  return (int)cudaMemcpyFromSymbol(host, g_bs_trace, (size_t)n * 8);
-}
-#else
-#define BS_MARK(i) \
-  do {             \
-  } while (0)
-#endif
+cudaError_t bsk_spmv_dispatch_f16(const bsk::Geom& g, const SpmvArgs& a, int nv, cudaStream_t s);
+cudaError_t bsk_spmv_dispatch_bf16(const bsk::Geom& g, const SpmvArgs& a, int nv, cudaStream_t s);
+cudaError_t bsk_spmv_dispatch_f32(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s);
 
-namespace {
-
-constexpr int kXBudget = 128 * 1024;  // bytes of x slots per chunk
-constexpr int kMaxChunks = 8;
-
-struct SpmvArgs {
-  const uint8_t* A;   // panel steps (region A)
-  const uint8_t* Bt;  // tail values (region B): element r·k·T + t·T + v·32 + l
-  const uint8_t* Ct;  // tail indices (region C), same order
-  const void* x;
-  void* y;
-  int64_t M, NB, NBf, T;
-  int B, k;
-  int NS;            // ring stages per warp
-  int xbytes;        // smem bytes reserved for x slots (max over chunks)
-  int nchunks;       // panel chunks
-  int PC;            // panels per chunk (the last may be shorter)
-  int tail_in_last;  // tail groups are staged with the last panel chunk
-  int tail_rows;     // rows per ring-streamed tail stage (0: direct loads)
-  int xvec;          // x is 16-byte aligned and B allows 16-byte staging loads
-};
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done)
-                 : "r"(bar), "r"(parity)
-                 : "memory");
-  }
-}
-// W is streamed exactly once per call: its bulk copies carry an L2 evict_first policy so that they
-// do not push the activations (x, y) out of L2.
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
-      : "memory");
-}
-// Byte i (compile-time after unrolling) of w, zero-extended: one PRMT.
-__device__ __forceinline__ uint32_t byte_of(uint32_t w, int i) {
-  uint32_t r;
-  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"(0x4440 | i));
-  return r;
-}
-__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
-  uint16_t b8;
-  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(b8) : "r"(a));
-  return b8;
-}
-
-// Stage the x columns of groups [g0, g1) into slots of ES bytes (halfwords for f16/bf16, words
-// for f32): element (b, o), b = 32·g + l, goes to slot (gl·B + o)·32 + l, gl = g - g0. Lane l always
-// copies block 32·g + l. So for f32 every slot of lane l is in bank l, and for 16-bit x the lanes
-// 2m and 2m+1 share a word. Work items are (group, 16-byte piece of a block); each lane issues up to
-// 8 piece loads before storing them. `after_loads()` runs once, right after the first batch of
-// loads is in flight, so that the caller can queue the W bulk copies behind them.
-template <int ES, typename F>
-__device__ __forceinline__ void stage_x(const SpmvArgs& a, uint32_t sx, int64_t g0, int64_t g1, F after_loads) {
-  constexpr int PE = 16 / ES;        // elements per 16-byte piece
-  constexpr uint32_t ROWB = 32 * ES;  // bytes per slot row (one offset o of 32 blocks)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int B = a.B;
-  bool hooked = false;
-  if (a.xvec) {  // 16-byte aligned x and B % PE == 0
-    const int ppb = B / PE;  // pieces per block
-    const int64_t items = (g1 - g0) * ppb;
-    for (int64_t j0 = warp; j0 < items || !hooked; j0 += 8LL * nw) {
-      uint4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t j = j0 + (int64_t)u * nw;
-        if (j < items) {
-          const int64_t gl = j / ppb;
-          const int q = (int)(j - gl * ppb);
-          const int64_t b = (g0 + gl) * 32 + lane;
-          if (b < a.NB) v[u] = __ldg((const uint4*)((const uint8_t*)a.x + (b * B + q * PE) * ES));
-        }
-      }
-      if (!hooked) {
-        after_loads();
-        hooked = true;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t j = j0 + (int64_t)u * nw;
-        if (j < items) {
-          const int64_t gl = j / ppb;
-          const int q = (int)(j - gl * ppb);
-          const int64_t b = (g0 + gl) * 32 + lane;
-          if (b < a.NB) {
-            const uint32_t col = sx + (uint32_t)(gl * B + q * PE) * ROWB + lane * ES;
-            const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-            for (int e = 0; e < PE; ++e) {
-              if (ES == 2) bsk::sts_u16(col + e * ROWB, (uint16_t)(w[e >> 1] >> (16 * (e & 1))));
-              else bsk::sts_u32(col + e * ROWB, w[e]);
-            }
-          }
-        }
-      }
-    }
-  } else {
-    after_loads();
-    for (int64_t g = g0 + warp; g < g1; g += nw) {
-      const int64_t b = g * 32 + lane;
-      if (b >= a.NB) continue;
-      const uint32_t col = sx + (uint32_t)(g - g0) * (uint32_t)B * ROWB + lane * ES;
-      for (int o = 0; o < B; ++o) {
-        if (ES == 2) bsk::sts_u16(col + o * ROWB, __ldg((const uint16_t*)a.x + b * B + o));
-        else bsk::sts_u32(col + o * ROWB, __ldg((const uint32_t*)a.x + b * B + o));
-      }
-    }
-  }
-}
-
-template <int DT>
-__device__ __forceinline__ uint32_t lds_x(uint32_t addr) {
-  return bsk::DTraits<DT>::kBytes == 2 ? bsk::lds_u16(addr) : bsk::lds_u32(addr);
-}
-
-// Per-lane accumulators -> warp total: fixed-order sum over v, then a butterfly.
-template <int V>
-__device__ __forceinline__ float warp_total(float (&acc)[V]) {
-  float sum = acc[0];
-#pragma unroll
-  for (int v = 1; v < V; ++v) sum += acc[v];
-#pragma unroll
-  for (int v = 0; v < V; ++v) acc[v] = 0.f;
-  return bsk::warp_sum_f(sum);
-}
-
-// One CTA per SM, NT/32 warps. Warp rows [wr0, wr0 + nrows). For panel chunk c (panels
-// [c·PC, c·PC + np)), each row contributes a segment of L = np·k consecutive steps. The ring streams
-// the segments of all chunks in order (a stage never crosses a segment), then the tails (R rows
-// per stage).
-template <int DT, int V, int IS, int Q, int BT, bool MULTI, int NT>
-__global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[NT / 32][4];
-  using raw_t = typename bsk::DTraits<DT>::raw_t;
-  constexpr int ES = bsk::DTraits<DT>::kBytes;
-  constexpr int P = 32 * V;
-  constexpr uint32_t STEPB = P * (ES + IS);  // bytes per step (values then indices)
-  constexpr uint32_t SB = Q * STEPB;         // bytes per ring stage
-  const int B = BT > 0 ? BT : a.B;
-  constexpr uint32_t ROWB = 32 * ES;      // bytes per slot row of x (one offset o of 32 blocks)
-  const uint32_t GSW = (uint32_t)B * ROWB;  // bytes per group of 32 blocks
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = NT / 32;
-  // balanced row ranges (32-bit arithmetic: M·(grid + 1) < 2^32 is checked on the host)
-  const int64_t rb = blockIdx.x * (uint32_t)a.M / gridDim.x;
-  const int64_t re = (blockIdx.x + 1) * (uint32_t)a.M / gridDim.x;
-  const uint32_t nr = (uint32_t)(re - rb);
-  const int64_t wr0 = rb + warp * nr / nw;
-  const int64_t nrows = rb + (warp + 1) * nr / nw - wr0;
-  const int64_t S = a.NBf * a.k;  // full-panel steps per row
-  const int NS = a.NS;
-  const uint32_t sx = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t ring = sx + a.xbytes + (uint32_t)(warp * NS) * SB;
-  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[warp][0]);
-  BS_MARK(0);
-  float* part = (float*)(smem + a.xbytes + (size_t)nw * NS * SB) - rb;  // fp32 row partials (MULTI)
-  const int64_t kT = (int64_t)a.k * a.T;  // entries of one row's tail
-  // A tail stage holds R rows: the value run (from the 16-byte-aligned address at or below it, offset
-  // dv), then, at the next 16-byte boundary, the index run (offset di).
-  auto tail_geom = [&](int64_t t0, int64_t R, uint32_t& dv, uint32_t& bv, uint32_t& di, uint32_t& bi) {
-    const int64_t ov = (wr0 + t0) * kT * ES, oi = (wr0 + t0) * kT * IS;
-    dv = (uint32_t)(ov & 15);
-    di = (uint32_t)(oi & 15);
-    bv = (uint32_t)((dv + R * kT * ES + 15) & ~15LL);
-    bi = (uint32_t)((di + R * kT * IS + 15) & ~15LL);
-  };
-
-  // ---- producer cursor (lane 0). Phase 1: (chunk pc, row pr, step ps) of the next panel stage.
-  // Phase 2 (pc == nchunks): tail stages of R rows each starting at row tr.
-  int pc = 0;
-  int64_t pr = 0, ps = 0, tr = 0;
-  auto seg_len = [&](int c) -> int64_t {
-    const int64_t p0 = (int64_t)c * a.PC;
-    const int64_t np = (a.NBf - p0) < a.PC ? (a.NBf - p0) : a.PC;
-    return np * a.k;
-  };
-  int64_t pL = seg_len(0);
-  const bool have_panels = S > 0 && nrows > 0;
-  if (!have_panels) pc = a.nchunks;
-  const bool ring_tail = a.T > 0 && a.k > 0 && a.tail_rows > 0 && nrows > 0;
-  auto more = [&]() { return pc < a.nchunks || (ring_tail && tr < nrows); };
-  const uint64_t pol = policy_evict_first();
-  auto issue = [&](uint32_t st) {  // load the next stage into ring slot st: one bulk copy
-    const uint32_t bar = bar0 + st * 8;
-    if (pc < a.nchunks) {
-      const int64_t n = (pL - ps) < Q ? (pL - ps) : Q;
-      const int64_t step0 = (wr0 + pr) * S + (int64_t)pc * a.PC * a.k + ps;
-      const uint32_t bytes = (uint32_t)n * STEPB;
-      mbar_expect_tx(bar, bytes);
-      bulk_g2s(ring + st * SB, a.A + step0 * STEPB, bytes, bar, pol);
-      ps += n;
-      if (ps == pL) {
-        ps = 0;
-        if (++pr == nrows) {
-          pr = 0;
-          ++pc;
-          if (pc < a.nchunks) pL = seg_len(pc);
-        }
-      }
-    } else {
-      // rows [tr, tr + R) of the tail region; bulk copies need 16-byte aligned sources and sizes, so
-      // copy from the aligned-down address (the consumer re-derives the same offset)
-      const int64_t R = (nrows - tr) < a.tail_rows ? (nrows - tr) : a.tail_rows;
-      uint32_t dv, bv, di, bi;
-      tail_geom(tr, R, dv, bv, di, bi);
-      mbar_expect_tx(bar, bv + bi);
-      bulk_g2s(ring + st * SB, a.Bt + (wr0 + tr) * kT * ES - dv, bv, bar, pol);
-      bulk_g2s(ring + st * SB + bv, a.Ct + (wr0 + tr) * kT * IS - di, bi, bar, pol);
-      tr += R;
-    }
-  };
-  if (lane == 0) {
-    for (int st = 0; st < NS; ++st) mbar_init(bar0 + st * 8, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    BS_MARK(5);
-  }
-  __syncwarp();
-  // the first x loads go out before the ring is armed, so that they do not queue behind W
-  auto arm_ring = [&]() {
-    if (lane == 0) {
-      for (int st = 0; st < NS && more(); ++st) {
-        issue((uint32_t)st);
-        if (st == 0) BS_MARK(7);
-      }
-    }
-  };
-  bool armed = false;
-  auto arm_once = [&]() {
-    if (!armed) {
-      arm_ring();
-      armed = true;
-    }
-  };
-
-  float acc[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) acc[v] = 0.f;
-
-  BS_MARK(1);
-  // ---- consumer
-  int64_t consumed = 0;
-  for (int c = 0; c < a.nchunks; ++c) {
-    const int64_t g0 = (int64_t)c * a.PC * V;
-    const bool last = c == a.nchunks - 1;
-    const int64_t g1 = last && a.tail_in_last ? (a.NB + 31) / 32 : g0 + (seg_len(c) / (a.k > 0 ? a.k : 1)) * V;
-    if (c > 0) __syncthreads();  // all warps are done with the previous chunk's x
-    stage_x<ES>(a, sx, g0, g1, arm_once);
-    if (c == 0) BS_MARK(6);
-    __syncthreads();
-    if (c == 0) BS_MARK(2);
-    if (!have_panels) continue;
-    const int64_t L = seg_len(c);
-    const uint32_t pstep = V * GSW;
-    const int k = a.k;
-    for (int64_t i = 0; i < nrows; ++i) {
-      uint32_t pb = sx + lane * ES;  // slot base of the current panel within the chunk
-      int t = 0;
-      for (int64_t s0 = 0; s0 < L; s0 += Q) {
-        const uint32_t st = (uint32_t)(consumed % NS);
-        mbar_wait(bar0 + st * 8, (uint32_t)((consumed / NS) & 1));
-        if (consumed == 0) BS_MARK(3);
-        const uint32_t sbase = ring + st * SB;
-        const int nq = (L - s0) < Q ? (int)(L - s0) : Q;
-        auto step = [&](int q) {
-          uint32_t wv[(V * ES + 3) / 4], iv[(V * IS + 3) / 4];
-          const uint32_t av = sbase + q * STEPB + lane * (V * ES);
-          const uint32_t ai = sbase + q * STEPB + P * ES + lane * (V * IS);
-          if constexpr (V * ES == 16) bsk::lds_v4(av, wv[0], wv[1], wv[2], wv[3]);
-          else if constexpr (V * ES == 8) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(wv[0]), "=r"(wv[1]) : "r"(av));
-          else if constexpr (V * ES == 4) wv[0] = bsk::lds_u32(av);
-          else wv[0] = bsk::lds_u16(av);
-          if constexpr (V * IS == 16) bsk::lds_v4(ai, iv[0], iv[1], iv[2], iv[3]);
-          else if constexpr (V * IS == 8) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(iv[0]), "=r"(iv[1]) : "r"(ai));
-          else if constexpr (V * IS == 4) iv[0] = bsk::lds_u32(ai);
-          else if constexpr (V * IS == 2) iv[0] = bsk::lds_u16(ai);
-          else iv[0] = lds_u8(ai);
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const uint32_t o = IS == 1 ? byte_of(iv[v >> 2], v & 3) : (iv[v >> 1] >> (16 * (v & 1))) & 0xffffu;
-            const uint32_t xv = lds_x<DT>(pb + o * ROWB + v * GSW);
-            const uint32_t w = ES == 2 ? (wv[v >> 1] >> (16 * (v & 1))) & 0xffffu : wv[v];
-            bsk::fma_acc<DT>(acc[v], w, xv);
-          }
-          if (++t == k) {
-            t = 0;
-            pb += pstep;
-          }
-        };
-        if (nq == Q) {  // full stage: no per-step predicate
-#pragma unroll
-          for (int q = 0; q < Q; ++q) step(q);
-        } else {
-#pragma unroll
-          for (int q = 0; q < Q; ++q)
-            if (q < nq) step(q);
-        }
-        __syncwarp();  // every lane is done with stage st
-        ++consumed;
-        if (lane == 0 && more()) issue(st);
-      }
-      const int64_t r = wr0 + i;
-      const float tot = warp_total<V>(acc);
-      if (lane == 0) {
-        if (MULTI) part[r] = c == 0 ? tot : part[r] + tot;
-        else ((raw_t*)a.y)[r] = (raw_t)bsk::from_float<DT>(tot);
-      }
-    }
-  }
-
-  BS_MARK(4);
-  // ---- tail blocks (region B: per row k·T values then k·T indices, (t, v, lane) order)
-  if (a.T > 0 && a.k > 0) {
-    const int64_t gt0 = a.NBf * V, gt1 = (a.NB + 31) / 32;
-    uint32_t tbase;
-    if (a.tail_in_last) {
-      tbase = sx + (uint32_t)(gt0 - (int64_t)(a.nchunks - 1) * a.PC * V) * GSW;
-    } else {
-      __syncthreads();
-      stage_x<ES>(a, sx, gt0, gt1, arm_once);
-      __syncthreads();
-      tbase = sx;
-    }
-    const int Vt = (int)((a.T + 31) / 32);
-    auto finish_row = [&](int64_t r) {
-      const float tot = warp_total<V>(acc);
-      if (lane == 0) {
-        const float y = S > 0 ? part[r] + tot : tot;
-        ((raw_t*)a.y)[r] = (raw_t)bsk::from_float<DT>(y);
-      }
-    };
-    // one row's tail; ldv/ldi load entry e (position t·T + v·32 + l) of the value / index runs
-    auto tail_row = [&](auto ldv, auto ldi) {
-      for (int tt = 0; tt < a.k; ++tt) {
-        const uint32_t e0 = (uint32_t)tt * (uint32_t)a.T;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const int bl = v * 32 + lane;
-          if (v < Vt && bl < a.T) {
-            const uint32_t w = ldv(e0 + bl);
-            const uint32_t o = ldi(e0 + bl);
-            const uint32_t xv = lds_x<DT>(tbase + lane * ES + o * ROWB + v * GSW);
-            bsk::fma_acc<DT>(acc[v], w, xv);
-          }
-        }
-      }
-    };
-    if (ring_tail) {  // tails arrive through the ring, R rows per stage
-      for (int64_t t0 = 0; t0 < nrows; t0 += a.tail_rows) {
-        const int64_t R = (nrows - t0) < a.tail_rows ? (nrows - t0) : a.tail_rows;
-        const uint32_t st = (uint32_t)(consumed % NS);
-        mbar_wait(bar0 + st * 8, (uint32_t)((consumed / NS) & 1));
-        uint32_t dv, bv, di, bi;
-        tail_geom(t0, R, dv, bv, di, bi);
-        for (int64_t rr = 0; rr < R; ++rr) {
-          const uint32_t rv = ring + st * SB + dv + (uint32_t)(rr * kT * ES);
-          const uint32_t ri = ring + st * SB + bv + di + (uint32_t)(rr * kT * IS);
-          tail_row([&](uint32_t e) { return ES == 2 ? bsk::lds_u16(rv + e * 2) : bsk::lds_u32(rv + e * 4); },
-                   [&](uint32_t e) { return IS == 1 ? lds_u8(ri + e) : bsk::lds_u16(ri + e * 2); });
-          finish_row(wr0 + t0 + rr);
-        }
-        __syncwarp();
-        ++consumed;
-        if (lane == 0 && more()) issue(st);
-      }
-    } else {  // direct loads (a row's tail does not fit a ring stage)
-      for (int64_t i = 0; i < nrows; ++i) {
-        const uint8_t* rv = a.Bt + (wr0 + i) * kT * ES;
-        const uint8_t* ri = a.Ct + (wr0 + i) * kT * IS;
-        tail_row([&](uint32_t e) { return ES == 2 ? (uint32_t)__ldg((const uint16_t*)rv + e) : __ldg((const uint32_t*)rv + e); },
-                 [&](uint32_t e) { return IS == 1 ? (uint32_t)__ldg(ri + e) : (uint32_t)__ldg((const uint16_t*)ri + e); });
-        finish_row(wr0 + i);
-      }
-    }
-  } else if (S == 0) {  // k == 0: y = 0
-    for (int64_t i = lane; i < nrows; i += 32) ((raw_t*)a.y)[wr0 + i] = (raw_t)bsk::from_float<DT>(0.f);
-  } else if (MULTI) {
-    __syncwarp();
-    for (int64_t i = lane; i < nrows; i += 32) ((raw_t*)a.y)[wr0 + i] = (raw_t)bsk::from_float<DT>(part[wr0 + i]);
-  }
-}
-
-template <int V, int ES>
-struct StageSteps {  // Q: about 2 KB of values per stage
-  static constexpr int value = 2048 / (32 * V * ES) < 1 ? 1 : 2048 / (32 * V * ES);
-};
-
-template <int DT, int V, int IS, int BT, bool MULTI, int NT, int QM>
-cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
-  constexpr int ES = bsk::DTraits<DT>::kBytes;
-  constexpr int Q = StageSteps<V, ES>::value * QM;
-  constexpr int SB = Q * 32 * V * (ES + IS);
-  static int static_smem = -1;  // per instantiation: static smem (the mbarriers)
-  auto kern = spmv_kernel<DT, V, IS, Q, BT, MULTI, NT>;
-  const auto& dp = bsk::dev_props();
-  if (static_smem < 0) {
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dp.smem_optin - (int)fa.sharedSizeBytes);
-    if (e != cudaSuccess) return e;
-    static_smem = (int)fa.sharedSizeBytes;
-  }
-  SpmvArgs a = a0;
-  a.tail_rows = 0;
-  if (a.T > 0 && a.k > 0) {  // whole rows of tail per ring stage (32 bytes of alignment slack)
-    const int64_t per = (int64_t)a.k * a.T * (ES + IS);
-    const int64_t R = (SB - 64) / per;
-    a.tail_rows = R >= 1 ? (int)(R < 64 ? R : 64) : 0;
-  }
-  int64_t grid = dp.sms;
-  const int64_t need = (a.M + (NT / 32) - 1) / (NT / 32);
-  if (grid > need) grid = need;
-  const int64_t scratch = MULTI ? ((a.M + grid - 1) / grid + 1) * 4 : 0;
-  const int64_t avail = dp.smem_optin - static_smem - a.xbytes - scratch;
-  int NS = (int)(avail / ((NT / 32) * (int64_t)SB));
-  if (NS > 4) NS = 4;
-  if (NS < 1) return cudaErrorInvalidConfiguration;
-  a.NS = NS;
-  const int64_t smem_all = a.xbytes + (int64_t)(NT / 32) * NS * SB + scratch;
-  kern<<<(unsigned)grid, NT, (size_t)smem_all, s>>>(a);
-  return cudaGetLastError();
-}
-
-// Warps per CTA and stage size: 16 warps x ~3 KB stages by default. BS_SPMV_CFG=8w (8 warps x
-// double stages) is a tuning knob for tools/spmv_sweep.py.
-int cfg_knob() {
-  static int v = -1;
-  if (v < 0) {
-    const char* c = getenv("BS_SPMV_CFG");
-    v = (c && c[0] == '8') ? 1 : 0;
-  }
-  return v;
-}
-
-template <int DT, int V, int IS, int BT, bool MULTI>
-cudaError_t launch_nt(const SpmvArgs& a, cudaStream_t s) {
-  if (cfg_knob() == 1) return launch_cfg<DT, V, IS, BT, MULTI, 256, 2>(a, s);
-  return launch_cfg<DT, V, IS, BT, MULTI, 512, 1>(a, s);
-}
-
-template <int DT, int V, int IS>
-cudaError_t launch_t(const SpmvArgs& a, cudaStream_t s) {
-  const bool multi = a.nchunks > 1 || a.T > 0;
-  if (a.B == 32 && IS == 1) return multi ? launch_nt<DT, V, IS, 32, true>(a, s) : launch_nt<DT, V, IS, 32, false>(a, s);
-  return multi ? launch_nt<DT, V, IS, 0, true>(a, s) : launch_nt<DT, V, IS, 0, false>(a, s);
-}
-
-template <int DT, int IS>
-cudaError_t dispatch_v(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
-  switch (g.V) {
-    case 1: return launch_t<DT, 1, IS>(a, s);
-    case 2: return launch_t<DT, 2, IS>(a, s);
-    case 4: return launch_t<DT, 4, IS>(a, s);
-    default:
-      if constexpr (DT != BS_F32) return launch_t<DT, 8, IS>(a, s);
-      return cudaErrorInvalidValue;
-  }
-}
-
-template <int DT>
-cudaError_t dispatch_is(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
-  return g.is == 1 ? dispatch_v<DT, 1>(g, a, s) : dispatch_v<DT, 2>(g, a, s);
-}
-
-}  // namespace
-
-cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, cudaStream_t s) {
+// nv = 1: SpMV (y = W·x). nv = 8: one pass over W for up to 8 batch columns (16-bit dtypes): column
+// n of X at x + n·ldx, column n of Y at y + n·ldy, n < ncols.
+static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const void* x, int64_t ldx, void* y,
+                                  int64_t ldy, int ncols, int nv, cudaStream_t s) {
   SpmvArgs a;
   const uint8_t* base = (const uint8_t*)packed;
   a.A = base + g.offA;
@@ -552,10 +30,13 @@ cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* 
   a.k = g.k;
   a.NS = 0;
   a.tail_rows = 0;
-  const bool aligned = ((uintptr_t)x & 15) == 0;
+  a.ldx = ldx;
+  a.ldy = ldy;
+  a.ncols = ncols;
+  const bool aligned = ((uintptr_t)x & 15) == 0 && (nv == 1 || ldx % 8 == 0);
   a.xvec = aligned && (g.es == 2 ? g.B % 8 == 0 : g.B % 4 == 0);
   // chunking of the K dimension by whole panels (depends only on K, B, dtype: deterministic)
-  const int64_t group_bytes = (int64_t)g.B * 32 * g.es;  // 32 blocks of x slots
+  const int64_t group_bytes = (int64_t)g.B * 32 * g.es * nv;  // 32 blocks of x slots
   const int64_t panel_bytes = group_bytes * g.V;
   const int64_t tail_groups = (g.NB + 31) / 32 - g.NBf * g.V;
   if (g.NBf > 0 && g.k > 0) {
@@ -586,8 +67,24 @@ cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* 
   if (a.xbytes > bsk::dev_props().smem_optin - 16 * 1024) return cudaErrorInvalidConfiguration;
   if ((uint64_t)g.M * (uint64_t)(bsk::dev_props().sms + 1) >= (1ULL << 32)) return cudaErrorInvalidConfiguration;
   switch (g.dt) {
-    case BS_F32: return dispatch_is<BS_F32>(g, a, s);
-    case BS_F16: return dispatch_is<BS_F16>(g, a, s);
-    default: return dispatch_is<BS_BF16>(g, a, s);
+    case BS_F32: return nv == 1 ? bsk_spmv_dispatch_f32(g, a, s) : cudaErrorNotSupported;
+    case BS_F16: return bsk_spmv_dispatch_f16(g, a, nv, s);
+    default: return bsk_spmv_dispatch_bf16(g, a, nv, s);
   }
+}
+
+cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, cudaStream_t s) {
+  return launch_spmv_nv(g, packed, x, 0, y, 0, 1, 1, s);
+}
+
+// Batched product on the SPMV layout (16-bit): passes of 8 batch columns, each one stream of W.
+cudaError_t bsk_launch_spmv_batch(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,
+                                  void* Y, int64_t ldy, cudaStream_t s) {
+  if (g.es != 2) return cudaErrorNotSupported;
+  for (int64_t n0 = 0; n0 < N; n0 += 8) {
+    const int nc = (int)((N - n0) < 8 ? (N - n0) : 8);
+    cudaError_t e = launch_spmv_nv(g, packed, (const uint16_t*)X + n0 * ldx, ldx, (uint16_t*)Y + n0 * ldy, ldy, nc, 8, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }

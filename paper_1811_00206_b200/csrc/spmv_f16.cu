@@ -1,0 +1,9 @@
+// spmv_f16.cu: f16 instantiations of the SpMV kernel (spmv_impl.cuh).
+#define BS_TRACE_TU_F16
+#define BS_TRACE_TU
+#include "spmv_impl.cuh"
+
+cudaError_t bsk_spmv_dispatch_f16(const bsk::Geom& g, const bsk_spmv::SpmvArgs& a, int nv, cudaStream_t s) {
+  if (nv == 8) return bsk_spmv::dispatch_is<BS_F16, 8>(g, a, s);
+  return bsk_spmv::dispatch_is<BS_F16, 1>(g, a, s);
+}

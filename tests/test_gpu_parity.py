@@ -73,6 +73,13 @@ def test_prune_pack_spmv_small(bs, M, K, B, k, dname, family):
         uv, ui = bs.unpack(A)
         np.testing.assert_array_equal(_raw(uv), _raw(vals))
         np.testing.assert_array_equal(_idx_np(ui), oi)
+        if layout == "spmm":  # the tile layout feeds bs_spmm; check it on a 3-column batch
+            X3 = synth.vector(K, dname, seed=synth.seed_for(0, 8), n=3)
+            Y3 = bs.spmm(A, X3.cuda())
+            Yr, bY = oracle.spmm(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(X3))
+            ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y3), DT[dname]), Yr, bY, oracle.TAU[DT[dname]])
+            assert ok, f"spmm: worst |err|/bound = {worst}"
+            continue
         y = bs.spmv(A, x.cuda())
         torch.cuda.synchronize()
         yr, bound = oracle.spmv(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(x))

@@ -281,6 +281,31 @@ def test_pack_spmv_steps_closed_form():
         np.testing.assert_array_equal(step[512:], np.full(128, t, dtype=np.uint8))
 
 
+def test_pack_spmm_blob_closed_form():
+    """SPMM layout: M=130 rows -> tiles of 128 and 2; K=96, B=32 -> CB=2 blocks per chunk -> chunks of 2 and 1 blocks.
+    Each blob lists (row, block, entry) values row-major, 16-byte padded, then the indices."""
+    M, K, B, k = 130, 96, 32, 1
+    NB = 3
+    vals = np.arange(M * NB * k, dtype=np.float16).reshape(M, NB, k)
+    idx = (np.arange(M * NB * k) % 32).astype(np.uint16).reshape(M, NB, k)
+    buf = oracle.pack(vals, idx, M, K, B, k, oracle.F16, oracle.SPMM)
+    p16 = lambda n: (n + 15) // 16 * 16
+    blob = lambda mt, cb: p16(mt * cb * k * 2) + p16(mt * cb * k)
+    tb = blob(128, 2) + blob(128, 1)
+    assert buf.size == (tb + blob(2, 2) + blob(2, 1) + 255) // 256 * 256
+    # tile 0, chunk 0: rows 0..127, blocks 0..1
+    b00 = buf[:blob(128, 2)]
+    np.testing.assert_array_equal(b00[:512].view(np.float16), vals[:128, 0:2, 0].reshape(-1))
+    np.testing.assert_array_equal(b00[512:768], idx[:128, 0:2, 0].reshape(-1).astype(np.uint8))
+    # tile 0, chunk 1: block 2 only
+    b01 = buf[blob(128, 2):tb]
+    np.testing.assert_array_equal(b01[:256].view(np.float16), vals[:128, 2, 0])
+    # tile 1 (rows 128..129), chunk 1 (block 2): values then indices, each padded to 16 bytes
+    b11 = buf[tb + blob(2, 2):tb + blob(2, 2) + blob(2, 1)]
+    np.testing.assert_array_equal(b11[:4].view(np.float16), vals[128:, 2, 0])
+    np.testing.assert_array_equal(b11[16:18], idx[128:, 2, 0].astype(np.uint8))
+
+
 @pytest.mark.parametrize("layout", [oracle.SPMV, oracle.SPMM])
 @pytest.mark.parametrize("M,K,B,k,dt,dname", [(5, 3008, 32, 3, oracle.F16, "f16"), (3, 1024, 16, 8, oracle.F32, "f32"),
                                                (2, 2048, 512, 9, oracle.BF16, "bf16"), (4, 64, 4, 2, oracle.F16, "f16")])
@@ -293,7 +318,23 @@ def test_pack_is_a_permutation(layout, M, K, B, k, dt, dname):
     isz = 1 if B <= 256 else 2
     n = M * (K // B) * k
     NB = K // B
-    vmax = 1 if layout == oracle.SPMM else 16 // es
+    cv = vals.reshape(-1).view(np.uint32 if es == 4 else np.uint16).astype(np.uint64)
+    ci = idx.reshape(-1).astype(np.uint64)
+    if layout == oracle.SPMM:  # walk the blobs (all M < 128 here: one row tile)
+        CB = -(-64 // B) if B <= 64 else 1
+        p16 = lambda x: (x + 15) // 16 * 16
+        off, vs, is_ = 0, [], []
+        for c in range(-(-NB // CB)):
+            cb = min(CB, NB - CB * c)
+            nv = M * cb * k
+            vs.append(buf[off:off + nv * es])
+            is_.append(buf[off + p16(nv * es):off + p16(nv * es) + nv * isz])
+            off += p16(nv * es) + p16(nv * isz)
+        pv = np.concatenate(vs).view(np.uint32 if es == 4 else np.uint16).astype(np.uint64)
+        pi = np.concatenate(is_).view(np.uint8 if isz == 1 else np.uint16).astype(np.uint64)
+        np.testing.assert_array_equal(np.sort(pv << 16 | pi), np.sort(cv << 16 | ci))
+        return
+    vmax = 16 // es
     V = 1
     while V * 2 <= vmax and 64 * V <= NB:
         V *= 2
