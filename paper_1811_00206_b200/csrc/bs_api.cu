@@ -141,7 +141,9 @@ int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream) {
   int st = matrix_geom(A, &g);
   if (st) return st;
   if (!x || !y) return BS_ERR_ARG;
-  if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;  // SPMM tiles / SP24 feed bs_spmm
+  if (g.layout == BS_LAYOUT_SP24)  // 2:4: CUDA-core path with 2-bit metadata
+    return from_cuda(bsk_launch_sp24(g, A->packed, x, 1, g.K, y, g.M, (cudaStream_t)stream));
+  if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;  // SPMM tiles feed bs_spmm
   return from_cuda(bsk_launch_spmv(g, A->packed, x, y, (cudaStream_t)stream));
 }
 
@@ -165,7 +167,8 @@ int bs_spmm(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, void* Y, 
   int st = matrix_geom(A, &g);
   if (st) return st;
   if (!X || !Y || N < 1 || ldx < g.K || ldy < g.M) return BS_ERR_ARG;
-  if (g.layout == BS_LAYOUT_SP24) return BS_ERR_UNSUPPORTED;
+  if (g.layout == BS_LAYOUT_SP24)  // 2:4: sparse tensor cores (tcgen05.mma.sp) or CUDA cores
+    return from_cuda(bsk_launch_sp24(g, A->packed, X, N, ldx, Y, ldy, (cudaStream_t)stream));
   cudaError_t e = bsk_launch_spmm(g, A->packed, X, N, ldx, Y, ldy, (cudaStream_t)stream);
   if (e != cudaErrorNotSupported) return from_cuda(e);
   // SPMV layout: passes of 8 batch columns through the SpMV kernel (16-bit), or one SpMV per column

@@ -105,5 +105,7 @@ cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* 
                             cudaStream_t s);
 cudaError_t bsk_launch_spmv_batch(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,
                                   void* Y, int64_t ldy, cudaStream_t s);
+cudaError_t bsk_launch_sp24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
+                            int64_t ldy, cudaStream_t s);
 cudaError_t bsk_launch_spmm(const bsk::Geom& g, const void* packed, const void* X, int64_t N,
                             int64_t ldx, void* Y, int64_t ldy, cudaStream_t s);

@@ -1,0 +1,324 @@
+// spmm24.cu: K5, the 2:4 path (B = 4, k = 2: the shape of Fig. 2, at 50%) on Blackwell sparse
+// tensor cores, plus its CUDA-core SpMV/SpMM (2-bit metadata, 2.25 B per nonzero at f16).
+//
+// The SP24 layout (docs/layout.md) is already the operand format of a 2:4 sparse MMA: the kept values
+// form the compressed A (M × K/2, row-major) and the block nibbles idx0 | idx1 << 2 form the metadata
+// (M × K/8 bytes). Per CTA: a 128-row tile of W and BN batch columns; K in chunks of 128 columns.
+//   - One producer lane issues TMA tensor copies (cp.async.bulk.tensor.2d, 128-byte swizzle): the
+//     compressed A chunk (128 rows × 64 values) and the X chunk (BN rows × 2 atoms of 64 columns).
+//   - 128 threads (thread = row) copy their 16 metadata bytes of the chunk into tensor memory with
+//     tcgen05.st (one 32-bit column per K = 32 step, 16-bit halves exchanged between rows r and r ^ 8).
+//   - One thread issues 4 × tcgen05.mma.sp.cta_group::1.kind::f16 (M = 128, N = BN, K = 32) into an
+//     fp32 accumulator in tensor memory; tcgen05.commit releases the stage.
+//   - Epilogue: tcgen05.ld → Y [N][M].
+// No decompression: the tensor core consumes the packed bytes directly.
+#include <cuda.h>
+
+#include "bs_common.cuh"
+#include "bs_device.cuh"
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int KCH = 128;  // original columns per chunk (64 compressed values: one 128-byte swizzle atom)
+constexpr int NST = 4;    // pipeline stages
+constexpr int kThreads = 192;
+
+struct Sp24Args {
+  const uint8_t* meta;  // M × K/8 bytes
+  void* Y;
+  int64_t M, K, N, ldy;
+  int BN, NC;           // batch columns per CTA (multiple of 16), chunks
+  uint32_t idesc;
+  int tmem_cols, meta_col;
+  int mstride;          // TMEM columns between the metadata of consecutive K = 32 steps
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(bar), "r"(parity)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)2 << 61);
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_constant__ CUtensorMap tA,
+                                                             const __grid_constant__ CUtensorMap tX, Sp24Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[3 * NST + 1];
+  __shared__ uint32_t tmem_holder;
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t ASZ = BM * 128;                 // compressed A chunk: 128 rows × 128 B
+  const uint32_t BSZ = 2u * (uint32_t)a.BN * 128;  // X chunk: 2 atoms of BN rows × 128 B
+  const uint32_t sA = smem_u32(smem), sB = sA + NST * ASZ;
+  const uint32_t full = smem_u32(&bars[0]), empty = smem_u32(&bars[NST]), meta_ok = smem_u32(&bars[2 * NST]);
+  const uint32_t acc_full = smem_u32(&bars[3 * NST]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t mt = (a.M - m0) < BM ? (a.M - m0) : BM;
+  const int64_t n0 = (int64_t)blockIdx.y * a.BN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full + 8 * s, 1);
+      mbar_init(empty + 8 * s, 1);
+      mbar_init(meta_ok + 8 * s, 128);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tX) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_holder)),
+                 "r"(a.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      for (int c = 0; c < a.NC; ++c) {
+        const int s = c % NST;
+        if (c >= NST) mbar_wait(empty + 8 * s, (uint32_t)(((c / NST) - 1) & 1));
+        mbar_expect_tx(full + 8 * s, ASZ + BSZ);
+        tma_2d(sA + s * ASZ, &tA, c * (KCH / 2), (int)m0, full + 8 * s);
+        tma_2d(sB + s * BSZ, &tX, c * KCH, (int)n0, full + 8 * s);
+        tma_2d(sB + s * BSZ + (uint32_t)a.BN * 128, &tX, c * KCH + 64, (int)n0, full + 8 * s);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- sparse MMA issuer
+      for (int c = 0; c < a.NC; ++c) {
+        const int s = c % NST;
+        const uint32_t par = (uint32_t)((c / NST) & 1);
+        mbar_wait(full + 8 * s, par);
+        mbar_wait(meta_ok + 8 * s, par);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint64_t da = sw128_desc(sA + s * ASZ);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          // A: 16 compressed values (32 B) per K = 32 step; B: 32 columns (64 B) per step, atom j / 2
+          const uint64_t db = sw128_desc(sB + s * BSZ + (uint32_t)(j >> 1) * (uint32_t)a.BN * 128) + (uint64_t)((j & 1) * 4);
+          const uint32_t te = tmem + (uint32_t)a.meta_col + (uint32_t)((s * 4 + j) * a.mstride);
+          const uint32_t acc = (c > 0 || j > 0) ? 1u : 0u;
+          asm volatile(
+              "{ .reg .pred p; setp.ne.b32 p, %5, 0;\n\t"
+              "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, p; }" ::"r"(tmem),
+              "l"(da + (uint64_t)(j * 2)), "l"(db), "r"(te), "r"(a.idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty + 8 * s)
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(acc_full)
+                   : "memory");
+    }
+  } else {
+    // ---- metadata → tensor memory (thread = row u); then the epilogue
+    const int u = threadIdx.x - 64;
+    const int q = warp & 3;  // TMEM lane quarter of this warp: rows 32q .. 32q + 31
+    const int64_t row = 32 * q + lane;
+    const uint8_t* mrow = a.meta + (m0 + row) * (a.K / 8);
+    (void)u;
+    for (int c = 0; c < a.NC; ++c) {
+      const int s = c % NST;
+      if (c >= NST) mbar_wait(empty + 8 * s, (uint32_t)(((c / NST) - 1) & 1));
+      uint4 m = make_uint4(0u, 0u, 0u, 0u);
+      if (row < mt) m = __ldg((const uint4*)(mrow + c * 16));
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)a.meta_col + (uint32_t)(s * 4 * a.mstride);
+      const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // The sparse MMA reads the metadata of row r, K-half h (16 bits: 4 groups) from TMEM lane
+        // (r % 8) + 8·h + 16·(r / 16), halfword (r / 8) % 2 (measured: tools/sp24_probe.py). So rows r
+        // and r ^ 8 (lanes of this warp) swap halves: lane r % 16 < 8 keeps both rows' K-half 0, the
+        // other lane both rows' K-half 1.
+        const uint32_t oth = __shfl_xor_sync(0xffffffffu, mw[j], 8);
+        const uint32_t w = (lane & 8) ? ((oth >> 16) | (mw[j] & 0xFFFF0000u)) : ((mw[j] & 0xFFFFu) | (oth << 16));
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr + (uint32_t)(j * a.mstride)),
+                     "r"(w)
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(meta_ok + 8 * s);
+    }
+    mbar_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    using raw_t = uint16_t;
+    for (int nb = 0; nb < a.BN; nb += 8) {
+      uint32_t r[8];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)nb));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < mt) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int64_t ng = n0 + nb + e;
+          if (ng < a.N) ((raw_t*)a.Y)[ng * a.ldy + m0 + row] = (raw_t)bsk::from_float<DT>(__uint_as_float(r[e]));
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
+  }
+}
+
+// CUDA-core 2:4 product (any N, any dtype): warp per (row, batch column); lane l walks block pairs.
+template <int DT>
+__global__ void sp24_cc_kernel(const uint8_t* __restrict__ vals, const uint8_t* __restrict__ meta,
+                               const void* __restrict__ X, void* __restrict__ Y, int64_t M, int64_t K, int64_t N,
+                               int64_t ldx, int64_t ldy) {
+  using raw_t = typename bsk::DTraits<DT>::raw_t;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t NB = K / 4;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < M * N; w += nwarps) {
+    const int64_t r = w % M, n = w / M;
+    const raw_t* vr = (const raw_t*)vals + r * (K / 2);
+    const uint8_t* mr = meta + r * (NB / 2);
+    const raw_t* xn = (const raw_t*)X + n * ldx;
+    float acc = 0.f;
+    for (int64_t b = lane; b < NB; b += 32) {
+      const uint32_t nib = (mr[b >> 1] >> (4 * (b & 1))) & 0xF;
+      bsk::fma_acc<DT>(acc, vr[2 * b], xn[4 * b + (nib & 3)]);
+      bsk::fma_acc<DT>(acc, vr[2 * b + 1], xn[4 * b + (nib >> 2)]);
+    }
+    acc = bsk::warp_sum_f(acc);
+    if (lane == 0) ((raw_t*)Y)[n * ldy + r] = (raw_t)bsk::from_float<DT>(acc);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeFn)p;
+  }
+  return fn;
+}
+
+// 2-D tensor map of a row-major [rows][cols] 16-bit matrix with row stride `ld` elements; box
+// (bc columns, br rows), 128-byte swizzle, zero fill out of bounds.
+bool make_map(CUtensorMap* m, int dt, const void* base, int64_t cols, int64_t rows, int64_t ld, int bc, int br) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
+  cuuint32_t es[2] = {1, 1};
+  const CUtensorMapDataType t = dt == BS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  return fn(m, t, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+template <int DT>
+cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
+                        int64_t ldy, cudaStream_t s) {
+  int BN = (int)((N + 15) / 16 * 16);
+  if (BN > 64) BN = N >= 192 ? 128 : 64;  // more CTAs along N for big batches
+  CUtensorMap tA, tX;
+  const uint8_t* base = (const uint8_t*)packed;
+  if (!make_map(&tA, DT, base + g.offA, g.K / 2, g.M, g.K / 2, 64, BM)) return cudaErrorNotSupported;
+  if (!make_map(&tX, DT, X, g.K, N, ldx, 64, BN)) return cudaErrorNotSupported;
+  Sp24Args a;
+  a.meta = base + g.offB;
+  a.Y = Y;
+  a.M = g.M; a.K = g.K; a.N = N; a.ldy = ldy;
+  a.BN = BN;
+  a.NC = (int)(g.K / KCH);
+  const uint32_t fmt = DT == BS_BF16 ? 1u : 0u;
+  // sparse flag (bit 2), f32 accumulate, K-major A and B, N = BN, M = 128
+  a.idesc = (1u << 2) | (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  a.mstride = 4;  // the metadata address of each K = 32 step must be 4-column aligned (stride 1 faults)
+  int p2 = 32;
+  while (p2 < BN) p2 <<= 1;
+  int mcols = 16 * a.mstride;
+  int tot = p2 + mcols;
+  int cols = 32;
+  while (cols < tot) cols <<= 1;
+  a.meta_col = p2;
+  a.tmem_cols = cols;
+  if (a.tmem_cols > 512) return cudaErrorNotSupported;
+  const int64_t smem = 1024 + (int64_t)NST * (BM * 128 + 2LL * BN * 128);
+  auto kern = spmm24_kernel<DT>;
+  static int configured = 0;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         bsk::dev_props().smem_optin - 1024);
+    if (e != cudaSuccess) return e;
+    configured = 1;
+  }
+  if (smem > bsk::dev_props().smem_optin - 1024) return cudaErrorNotSupported;
+  dim3 grid((unsigned)((g.M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
+  kern<<<grid, kThreads, (size_t)smem, s>>>(tA, tX, a);
+  return cudaGetLastError();
+}
+
+template <int DT>
+cudaError_t launch_cc24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
+                        int64_t ldy, cudaStream_t s) {
+  const uint8_t* base = (const uint8_t*)packed;
+  int64_t blocks = (g.M * N + 7) / 8;
+  if (blocks > (int64_t)bsk::dev_props().sms * 16) blocks = (int64_t)bsk::dev_props().sms * 16;
+  sp24_cc_kernel<DT><<<(unsigned)blocks, 256, 0, s>>>(base + g.offA, base + g.offB, X, Y, g.M, g.K, N, ldx, ldy);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Y = W·X for W in SP24 layout. The tensor path needs f16/bf16, K % 128 == 0, 16-byte aligned X rows and
+// N >= 2 (batch 1 is memory-bound: the CUDA-core kernel serves it).
+cudaError_t bsk_launch_sp24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
+                            int64_t ldy, cudaStream_t s) {
+  const bool tc = g.es == 2 && g.K % KCH == 0 && N >= 2 && ((uintptr_t)X & 15) == 0 && (ldx % 8) == 0;
+  if (tc) {
+    cudaError_t e = g.dt == BS_BF16 ? launch_tc24<BS_BF16>(g, packed, X, N, ldx, Y, ldy, s)
+                                    : launch_tc24<BS_F16>(g, packed, X, N, ldx, Y, ldy, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  switch (g.dt) {
+    case BS_F32: return launch_cc24<BS_F32>(g, packed, X, N, ldx, Y, ldy, s);
+    case BS_F16: return launch_cc24<BS_F16>(g, packed, X, N, ldx, Y, ldy, s);
+    default: return launch_cc24<BS_BF16>(g, packed, X, N, ldx, Y, ldy, s);
+  }
+}

@@ -257,3 +257,35 @@ def test_big_65536_sampled_rows(bs):
     yr, bound = oracle.spmv_rowslice(ov, oi, oracle.F16, K, B, k, synth.to_numpy(x))
     ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(y[rt]), oracle.F16), yr, bound, 1e-2)
     assert ok, worst
+
+
+# ---------------------------------------------------------------- 2:4 (B = 4, k = 2): SP24 layout
+
+@pytest.mark.parametrize("N", [1, 2, 8, 16, 64, 200])
+@pytest.mark.parametrize("dname", ["f16", "bf16"])
+def test_sp24_spmm(bs, N, dname):
+    """2:4 on the sparse tensor cores (N >= 2) and the CUDA-core path (N = 1) vs the oracle."""
+    M, K = 300, 1024  # 3 row tiles (the last one partial), 8 chunks of 128 columns
+    W = synth.matrix(M, K, dname, seed=60 + N)
+    X = synth.vector(K, dname, seed=61, n=N)
+    vals, idx, ov, oi = _prune_parity(bs, W, dname, 4, 2)
+    A = bs.pack(vals, idx, K, 4, layout="sp24")
+    np.testing.assert_array_equal(A.packed.cpu().numpy(), oracle.pack(ov, oi, M, K, 4, 2, DT[dname], oracle.SP24))
+    Y = bs.spmm(A, X.cuda())
+    Yr, bound = oracle.spmm(ov, oi, DT[dname], M, K, 4, 2, synth.to_numpy(X))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y), DT[dname]), Yr, bound, 1e-2)
+    assert ok, f"sp24 N={N}: worst {worst}"
+
+
+def test_sp24_spmv_and_integer_exact(bs):
+    M, K = 257, 2048
+    W = synth.matrix(M, K, "f16", family="intexact", seed=62)
+    X = synth.vector(K, "f16", family="intexact", seed=63, n=16)
+    vals, idx, ov, oi = _prune_parity(bs, W, "f16", 4, 2)
+    A = bs.pack(vals, idx, K, 4, layout="sp24")
+    y = bs.spmv(A, X[0].contiguous().cuda())
+    yr, _ = oracle.spmv(ov, oi, oracle.F16, M, K, 4, 2, synth.to_numpy(X[0].contiguous()))
+    np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(y), oracle.F16), yr)
+    Y = bs.spmm(A, X.cuda())  # tensor cores, integer-exact: bit-identical
+    Yr, _ = oracle.spmm(ov, oi, oracle.F16, M, K, 4, 2, synth.to_numpy(X))
+    np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(Y), oracle.F16), Yr)
