@@ -1,0 +1,74 @@
+// bs_tc.cuh: Blackwell async-pipeline helpers shared by the tensor-core kernels (spmm.cu K6,
+// spmm24.cu K5): mbarriers, bulk / tensor (TMA) copies, UMMA shared-memory descriptors, tensor maps.
+#pragma once
+
+#include <cuda.h>
+#include <stdint.h>
+
+#include "bs_common.cuh"
+
+namespace bsk_tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(bar), "r"(parity)
+                 : "memory");
+  }
+}
+
+// global -> shared bulk copy (16-byte aligned source, destination and size), completes on `bar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// 2-D tensor copy (TMA) of one box at coordinates (c0 = inner / column, c1 = row)
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B: 8-row × 128-byte atoms, SBO = 1024 B between
+// 8-row groups, LBO unused (1), version 1 (bits 46-47), layout type 2 (bits 61-63). Advancing K by 16
+// 16-bit elements inside the atom adds 2 (32 bytes >> 4) to the start address field.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)2 << 61);
+}
+
+// byte offset of 16-bit element (row, col) in a K-major SWIZZLE_128B tile of 64 columns
+__device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t col) {
+  return row * 128 + ((((col >> 3) ^ (row & 7)) & 7) << 4) + (col & 7) * 2;
+}
+
+// kind::f16 instruction descriptor: fp32 accumulate (bit 4), A/B format f16 (0) or bf16 (1) at bits
+// 7 / 10, K-major A and B, N >> 3 at bit 17, M >> 4 at bit 24; bit 2 selects the sparse (.sp) form.
+__host__ __device__ inline uint32_t idesc_f16(int dt_bf16, int M, int N, bool sparse) {
+  const uint32_t fmt = dt_bf16 ? 1u : 0u;
+  return (sparse ? (1u << 2) : 0u) | (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+}  // namespace bsk_tc
+
+// 2-D tensor map of a row-major [rows][cols] 16-bit matrix (dt f16 / bf16) with row stride `ld`
+// elements; box of bc columns × br rows, 128-byte swizzle, zero fill out of bounds. Returns false if
+// the driver entry point is missing or the encoding is rejected (alignment, strides).
+bool bsk_make_map_2d(CUtensorMap* m, int dt, const void* base, int64_t cols, int64_t rows, int64_t ld, int bc, int br);

@@ -1,122 +1,123 @@
 // spmm.cu: bs_spmm, Y = W_bs · X for a batch of N columns (Fig. `benchmark`(b), batch 8).
 //
-// K6, tensor cores (f16/bf16, SPMM layout, B | 64). Per CTA: one 128-row tile of W and up to 256
-// batch columns, streamed over K in chunks of 64 columns.
-//   - A producer lane bulk-copies each (tile, chunk) blob of packed W (docs/layout.md SPMM) into a
-//     shared-memory ring (cp.async.bulk + mbarrier).
-//   - Four "decompress" warps rebuild the dense 128×64 A tile in shared memory. Thread r owns row r:
-//     it clears the row, then scatters the row's kept values to their columns (the paper's balanced
-//     rows make this the same work for every thread). The same warps stage the 64-column
-//     chunk of X as the N×64 B tile. Both tiles are in the canonical K-major SWIZZLE_128B layout of
-//     the UMMA descriptors. A fence.proxy.async makes the stores visible to the tensor core.
-//   - One elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = padded batch,
-//     K = 16, ×4 per chunk) with the fp32 accumulator in tensor memory. A/B are double-buffered, and
-//     tcgen05.commit → mbarrier hands buffers back.
-//   - The epilogue warps read the accumulator with tcgen05.ld (32x32b) and store Y rows [N][M] in D.
-// Dense flops are spent on the decompressed tile, but only packed bytes cross HBM.
-// Column n of Y depends only on column n of X, and the accumulation order over K is fixed.
+// K6, tensor cores (f16/bf16, SPMM layout, B | 64). Per CTA: one 128-row tile of W, up to 256 batch
+// columns, and a contiguous range of the 64-column K chunks (split-K over a thread-block cluster).
+//   - Warp 0, one lane: per chunk, a bulk copy of the packed (tile, chunk) blob (docs/layout.md SPMM)
+//     and a TMA tensor copy of the BN × 64 X tile (128-byte swizzle, zero fill past N and K) into an
+//     NSB-stage ring (mbarrier complete_tx), 4..16 stages deep.
+//   - Warps 2..17: two groups of 8 warps, alternating chunks, rebuild the dense 128 × 64 A tile in one
+//     of NA = 4 buffers: a linear zero fill, a named barrier, then an entry-parallel scatter: thread
+//     t takes blob entries t, t+256, ... (consecutive lanes read consecutive values and indices:
+//     conflict-free; four entries' loads in flight before their stores) and stores each value
+//     at (row, (entry's block)·B + index) of the K-major SWIZZLE_128B tile. The balanced rows give every
+//     chunk the same entry count per row, so (row, block) follow from the entry number by a
+//     running quotient. fence.proxy.async publishes the stores to the tensor core.
+//   - Warp 1, one lane: 4 × tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = BN, K = 16) per chunk into
+//     the fp32 accumulator in tensor memory; tcgen05.commit frees the blob/X stage and the A buffer.
+//   - Epilogue: tcgen05.ld (32x32b) → Y [N][M]. With split-K (cluster of S CTAs along K), each CTA
+//     parks its fp32 partial tile in shared memory, and after a cluster barrier CTA j sums slice j of
+//     the tile over the S partials in rank order through distributed shared memory (ld.shared::cluster).
+// S depends only on M and K (never on N), and the accumulation order over K is fixed, so column n of Y
+// depends only on column n of X: batch sharding reproduces the unsharded columns bit for bit.
+// Dense flops are spent on the decompressed tile; only packed bytes cross HBM.
 //
-// CUDA-core fallback (f32, or B not dividing 64): one thread per (row, batch column) walks the row's
-// blobs in chunk order with fp32 FMAs.
+// CUDA-core fallback (f32, B not dividing 64, unaligned X): one thread per (row, batch column) walks
+// the row's blobs in chunk order with fp32 FMAs.
 #include "bs_common.cuh"
 #include "bs_device.cuh"
+#include "bs_tc.cuh"
 
 namespace {
 
-constexpr int BM = 128;     // rows per tile (MMA M)
-constexpr int KC = 64;      // columns per chunk (one SWIZZLE_128B atom of 16-bit values)
-constexpr int NSB = 4;      // blob ring stages
-constexpr int kThreads = 192;  // warp 0 producer, warp 1 MMA/TMEM, warps 2..5 decompress + epilogue
+using namespace bsk_tc;
+
+constexpr int BM = 128;          // rows per tile (MMA M)
+constexpr int KC = 64;           // columns per chunk (one SWIZZLE_128B atom of 16-bit values)
+constexpr int NA = 4;            // dense A tile buffers
+constexpr int kMaxStages = 16;   // blob + X tile ring stages (runtime NSB: even, 4..16)
+constexpr int kDecomp = 256;     // threads per decompress group (8 warps)
+constexpr int kGroups = 2;       // decompress groups, alternating chunks
+constexpr int kThreads = 64 + kGroups * kDecomp;
+constexpr int kMaxCluster = 8;   // split-K factor (portable cluster size)
 
 struct TcArgs {
   const uint8_t* W;   // packed SPMM layout
-  const void* X;
   void* Y;
-  int64_t M, K, NB, N, ldx, ldy;
-  int B, k, CB, NC;   // block width, kept per block, blocks per chunk, chunks
-  int is;             // index bytes
+  int64_t M, NB, N, ldy;
+  int B, k, CB, NC;   // block width, kept per block, blocks per chunk, chunks per row tile
   int64_t tile_stride;
-  int BN;             // padded batch columns handled per CTA (multiple of 16, <= 256)
-  int blob_max;       // bytes of one full blob (128 rows, CB blocks)
-  int xvec;           // X rows 16-byte aligned (LDG.128 staging)
-  uint32_t idesc;     // tcgen05 instruction descriptor
+  int BN, S, NSB;     // batch columns per CTA (multiple of 16), split-K cluster size, ring stages
+  int blob_max;       // bytes of a full blob (128 rows, CB blocks)
+  uint32_t idesc;
   int tmem_cols;
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(bar), "r"(count));
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done)
-                 : "r"(bar), "r"(parity)
-                 : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
+__device__ __forceinline__ float4 ld_cluster_f4(uint32_t local_addr, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
+  return v;
 }
 
-// UMMA shared-memory descriptor, K-major SWIZZLE_128B: 8-row x 128-byte atoms, SBO = 1024 B between
-// 8-row groups, LBO unused (1), version 1 (bits 46-47), layout type 2 (bits 61-63).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
-         ((uint64_t)2 << 61);
-}
-// byte offset of element (row, col) in a K-major SWIZZLE_128B tile of 64 16-bit columns
-__device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t col) {
-  return row * 128 + ((((col >> 3) ^ (row & 7)) & 7) << 4) + (col & 7) * 2;
-}
-
-template <int DT, int IS>
-__global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(TcArgs a) {
+template <int DT>
+__global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_constant__ CUtensorMap tX, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bars[2 * NSB + 5];
+  __shared__ __align__(8) uint64_t bars[2 * kMaxStages + 2 * NA + 1];
   __shared__ uint32_t tmem_holder;
+  __shared__ uint8_t ctab[64];  // entry number within a row's chunk run -> block offset (entry / k)·B
   using raw_t = uint16_t;
   constexpr int ES = 2;
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sA = smem_u32(smem);                         // 2 x 16 KB
-  const uint32_t sB = sA + 2 * BM * 128;                      // 2 x BN*128
-  const uint32_t sR = sB + 2 * a.BN * 128;                    // NSB x blob_max
-  const uint32_t b_full = smem_u32(&bars[0]), b_empty = smem_u32(&bars[NSB]);
-  const uint32_t a_full = smem_u32(&bars[2 * NSB]), m_done = smem_u32(&bars[2 * NSB + 2]);
-  const uint32_t acc_full = smem_u32(&bars[2 * NSB + 4]);
+  const int NSB = a.NSB;
+  const uint32_t sA = smem_u32(smem);                          // NA × 16 KB dense A tiles
+  const uint32_t XSZ = (uint32_t)a.BN * 128;                   // X tile: BN rows × 128 B
+  const uint32_t sX = sA + NA * BM * 128;                      // NSB × XSZ
+  const uint32_t sR = sX + (uint32_t)NSB * XSZ;                // NSB × blob_max
+  const uint32_t full = smem_u32(&bars[0]), empty = smem_u32(&bars[kMaxStages]);
+  const uint32_t a_full = smem_u32(&bars[2 * kMaxStages]), a_empty = smem_u32(&bars[2 * kMaxStages + NA]);
+  const uint32_t acc_full = smem_u32(&bars[2 * kMaxStages + 2 * NA]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tile = blockIdx.x;
+  const int S = a.S;
+  const int rank = S > 1 ? (int)cluster_rank() : 0;
+  const int64_t tile = blockIdx.x / S;
   const int64_t m0 = tile * BM;
   const int64_t mt = (a.M - m0) < BM ? (a.M - m0) : BM;
   const int64_t n0 = (int64_t)blockIdx.y * a.BN;
+  const int c0 = (int)((int64_t)rank * a.NC / S), c1 = (int)((int64_t)(rank + 1) * a.NC / S);
+  const int nloc = c1 - c0;  // >= 1 (S <= NC)
   const uint8_t* tile_base = a.W + tile * a.tile_stride;
+  const int k = a.k;
   auto blob_bytes = [&](int64_t cb) {
-    return (uint32_t)(bsk::align_up(mt * cb * a.k * ES, 16) + bsk::align_up(mt * cb * a.k * IS, 16));
+    return (uint32_t)(bsk::align_up(mt * cb * k * ES, 16) + bsk::align_up(mt * cb * k, 16));
   };
   const uint32_t blobCB = blob_bytes(a.CB);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSB; ++s) {
-      mbar_init(b_full + 8 * s, 1);
-      mbar_init(b_empty + 8 * s, 128);
+      mbar_init(full + 8 * s, 1);
+      mbar_init(empty + 8 * s, 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(a_full + 8 * s, 128);
-      mbar_init(m_done + 8 * s, 1);
+    for (int s = 0; s < NA; ++s) {
+      mbar_init(a_full + 8 * s, kDecomp);  // one decompress group
+      mbar_init(a_empty + 8 * s, 1);
     }
     mbar_init(acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {  // tensor-memory accumulator: 128 lanes x tmem_cols fp32 columns
+  if (threadIdx.x >= 64 && threadIdx.x < 128) {
+    const int q = threadIdx.x - 64;
+    ctab[q] = (uint8_t)(q < a.CB * k ? (q / k) * a.B : 0);
+  }
+  if (warp == 1) {  // tensor-memory accumulator: 128 lanes × tmem_cols fp32 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_holder)),
                  "r"(a.tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -127,115 +128,163 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(TcArgs a) {
   const uint32_t tmem_d = tmem_holder;
 
   if (warp == 0) {
-    // ---- producer: bulk-copy blobs (tile, chunk) into the ring
-    if (lane == 0) {
-      for (int c = 0; c < a.NC; ++c) {
-        const int s = c % NSB;
-        if (c >= NSB) mbar_wait(b_empty + 8 * s, (uint32_t)(((c / NSB) - 1) & 1));
+    if (lane == 0) {  // ---- producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tX) : "memory");
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nloc; ++i) {
+        const int c = c0 + i;
+        if (i >= NSB) mbar_wait(empty + 8 * s, ph ^ 1u);
         const int64_t cb = (a.NB - (int64_t)a.CB * c) < a.CB ? (a.NB - (int64_t)a.CB * c) : a.CB;
         const uint32_t bytes = blob_bytes(cb);
-        mbar_expect_tx(b_full + 8 * s, bytes);
-        bulk_g2s(sR + s * a.blob_max, tile_base + (int64_t)c * blobCB, bytes, b_full + 8 * s);
+        mbar_expect_tx(full + 8 * s, bytes + XSZ);
+        bulk_g2s(sR + (uint32_t)s * (uint32_t)a.blob_max, tile_base + (int64_t)c * blobCB, bytes, full + 8 * s);
+        tma_2d(sX + (uint32_t)s * XSZ, &tX, c * KC, (int)n0, full + 8 * s);
+        if (++s == NSB) { s = 0; ph ^= 1u; }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer: one elected thread
-    if (lane == 0) {
-      for (int c = 0; c < a.NC; ++c) {
-        const int ab = c & 1;
-        mbar_wait(a_full + 8 * ab, (uint32_t)((c >> 1) & 1));
+    if (lane == 0) {  // ---- MMA issuer
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nloc; ++i) {
+        const int ab = i & (NA - 1);
+        mbar_wait(full + 8 * s, ph);
+        mbar_wait(a_full + 8 * ab, (uint32_t)(i / NA) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint64_t da = sw128_desc(sA + ab * BM * 128), db = sw128_desc(sB + ab * a.BN * 128);
+        const uint64_t da = sw128_desc(sA + (uint32_t)ab * BM * 128), db = sw128_desc(sX + (uint32_t)s * XSZ);
 #pragma unroll
         for (int kk = 0; kk < KC / 16; ++kk) {
-          const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
-          // advance 16 elements (32 bytes = 2 units of 16 B) along K inside the swizzle atom
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
           asm volatile(
               "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem_d),
               "l"(da + 2 * kk), "l"(db + 2 * kk), "r"(a.idesc), "r"(acc));
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(m_done + 8 * ab)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty + 8 * s)
                      : "memory");
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(a_empty + 8 * ab)
+                     : "memory");
+        if (++s == NSB) { s = 0; ph ^= 1u; }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(acc_full)
                    : "memory");
     }
   } else {
-    // ---- decompress + stage X (128 threads, u = row of the tile)
-    const int u = threadIdx.x - 64;
-    for (int c = 0; c < a.NC; ++c) {
-      const int s = c % NSB, ab = c & 1;
-      const int64_t cb = (a.NB - (int64_t)a.CB * c) < a.CB ? (a.NB - (int64_t)a.CB * c) : a.CB;
-      if (c >= 2) mbar_wait(m_done + 8 * ab, (uint32_t)(((c >> 1) - 1) & 1));  // MMA done with buffer ab
-      mbar_wait(b_full + 8 * s, (uint32_t)((c / NSB) & 1));
-      // A row u: clear, then scatter the row's cb·k kept values
-      const uint32_t arow = sA + ab * BM * 128;
+    // ---- decompress: group grp (8 warps) rebuilds chunks i = grp, grp + 2, ...; thread t = 0..255.
+    // Entry e of a chunk sits in row e / rk at run position e % rk (rk = entries per row); thread t
+    // walks e = t, t + 256, ... keeping (row, position) by a running quotient. Full chunks and the
+    // last (shorter) chunk of the row tile each get their constants once.
+    const int grp = (threadIdx.x - 64) / kDecomp, t = (threadIdx.x - 64) % kDecomp;
+    struct CG {
+      int rk, dq, dr, r0, e0, n_e, ioff;
+    };
+    auto mk = [&](int rk) {
+      CG g;
+      g.rk = rk; g.dq = kDecomp / rk; g.dr = kDecomp % rk; g.r0 = t / rk; g.e0 = t % rk;
+      g.n_e = (int)mt * rk; g.ioff = (int)bsk::align_up((int64_t)g.n_e * ES, 16);
+      return g;
+    };
+    const CG gF = mk(a.CB * k), gL = mk((int)(a.NB - (int64_t)a.CB * (a.NC - 1)) * k);
+    const int ilast = a.NC - 1 - c0;  // local index of the row tile's last chunk (may be >= nloc)
+    uint8_t* const ring = smem + (sR - sA);
+    int s = grp;  // ring stage of chunk i (NSB is even, so group grp keeps stages of its parity)
+    uint32_t ph = 0;
+    for (int i = grp; i < nloc; i += kGroups) {
+      const int ab = i & (NA - 1);
+      const uint32_t aph = (uint32_t)(i / NA) & 1u;
+      const uint32_t aT = sA + (uint32_t)ab * BM * 128;
+      uint8_t* const aTp = smem + ab * BM * 128;
+      if (i >= NA) mbar_wait(a_empty + 8 * ab, aph ^ 1u);  // MMA done with this A tile
 #pragma unroll
-      for (int j = 0; j < 8; ++j) bsk::sts_v4(arow + u * 128 + j * 16, 0u, 0u, 0u, 0u);
-      if (u < mt) {
-        const uint32_t bv = sR + s * a.blob_max;
-        const uint32_t bi = bv + (uint32_t)bsk::align_up(mt * cb * a.k * ES, 16);
-        const int n_e = (int)cb * a.k;
-        for (int e = 0; e < n_e; ++e) {
-          const uint32_t pos = (uint32_t)u * n_e + e;
-          const uint32_t w = bsk::lds_u16(bv + pos * 2);
-          uint32_t o;
-          if (IS == 1) {
-            uint16_t b8;
-            asm volatile("ld.shared.u8 %0, [%1];" : "=h"(b8) : "r"(bi + pos));
-            o = b8;
-          } else {
-            o = bsk::lds_u16(bi + pos * 2);
-          }
-          const uint32_t col = (uint32_t)(e / a.k) * a.B + o;
-          bsk::sts_u16(arow + sw128_off(u, col), (uint16_t)w);
-        }
-      }
-      // B tile: X columns [c·64, c·64 + 64) of batch rows n0 .. n0 + BN (zeros outside X)
-      const uint32_t brow = sB + ab * a.BN * 128;
-      const int64_t kc0 = (int64_t)c * KC;
-      const int64_t kvalid = (a.K - kc0) < KC ? (a.K - kc0) : KC;
-      for (int p = u; p < a.BN * 8; p += 128) {
-        const int n = p >> 3, j = p & 7;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        const int64_t ng = n0 + n;
-        if (ng < a.N) {
-          const raw_t* xs = (const raw_t*)a.X + ng * a.ldx + kc0 + j * 8;
-          if (a.xvec && j * 8 + 8 <= kvalid) {
-            v = __ldg((const uint4*)xs);
-          } else {
-            uint32_t h[8];
+      for (int q = 0; q < 4; ++q) bsk::sts_v4(aT + q * 4096 + t * 16, 0u, 0u, 0u, 0u);
+      const CG& G = i == ilast ? gL : gF;
+      const int rk = G.rk, dq = G.dq, dr = G.dr, n_e = G.n_e;
+      int r = G.r0, rem = G.e0;
+      mbar_wait(full + 8 * s, ph);
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kDecomp) : "memory");  // zero fill before any scatter
+      const uint8_t* blob = ring + s * a.blob_max;
+      const uint16_t* bv = (const uint16_t*)blob;
+      const uint8_t* bi = blob + G.ioff;
+      for (int e0 = t; e0 < n_e; e0 += 4 * kDecomp) {
+        uint16_t w[4];
+        uint8_t o[4];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) h[e] = (j * 8 + e < kvalid) ? (uint32_t)__ldg(xs + e) : 0u;
-            v = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
-          }
+        for (int u = 0; u < 4; ++u) {  // loads first: four entries in flight
+          const int e = e0 + u * kDecomp;
+          w[u] = e < n_e ? bv[e] : (uint16_t)0;
+          o[u] = e < n_e ? bi[e] : (uint8_t)0;
         }
-        bsk::sts_v4(brow + n * 128 + ((((uint32_t)j ^ (uint32_t)(n & 7)) & 7) << 4), v.x, v.y, v.z, v.w);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (e0 + u * kDecomp < n_e) {
+            const uint32_t col = (uint32_t)ctab[rem] + o[u];
+            *(uint16_t*)(aTp + sw128_off((uint32_t)r, col)) = w[u];
+          }
+          rem += dr;
+          r += dq;
+          if (rem >= rk) { rem -= rk; ++r; }
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core
       mbar_arrive(a_full + 8 * ab);
-      mbar_arrive(b_empty + 8 * s);
+      s += kGroups;
+      if (s >= NSB) { s -= NSB; ph ^= 1u; }
     }
-    // ---- epilogue: TMEM -> registers -> Y (row m = 32·(warp % 4) + lane)
+    // ---- epilogue: TMEM -> registers. Warp w reads lane quarter w % 4 (rows 32·(w % 4) + lane) and
+    // column part (w - 2) / 4 of NP parts.
     mbar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const int q = warp & 3;
-    const int64_t m = 32 * q + lane;
-    for (int nb = 0; nb < a.BN; nb += 8) {
-      uint32_t r[8];
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                   : "r"(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)nb));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (m < mt) {
+    const int q = warp & 3, part = (warp - 2) >> 2;
+    const int NP = a.BN % 32 == 0 ? 4 : 2;  // parts of BN / NP columns, a multiple of 8
+    const int m = 32 * q + lane;
+    float* red = (float*)smem;  // split-K partial tile [BN][128] (the rings are idle now)
+    if (part < NP) {
+      const int pw = a.BN / NP;
+      for (int nb = part * pw; nb < (part + 1) * pw; nb += 8) {
+        uint32_t rr[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]), "=r"(rr[7])
+                     : "r"(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)nb));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (S > 1) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int64_t ng = n0 + nb + e;
-          if (ng < a.N) ((raw_t*)a.Y)[ng * a.ldy + m0 + m] = (raw_t)bsk::from_float<DT>(__uint_as_float(r[e]));
+          for (int e = 0; e < 8; ++e) red[(nb + e) * BM + m] = __uint_as_float(rr[e]);
+        } else if (m < mt) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int64_t ng = n0 + nb + e;
+            if (ng < a.N) ((raw_t*)a.Y)[ng * a.ldy + m0 + m] = (raw_t)bsk::from_float<DT>(__uint_as_float(rr[e]));
+          }
         }
       }
     }
+  }
+  if (S > 1) {
+    cluster_sync_all();  // every partial tile is parked
+    if (warp >= 2) {
+      const int t = threadIdx.x - 64;
+      const int U = a.BN * BM / 4;  // float4 units of the tile
+      const int u0 = (int)((int64_t)rank * U / S), u1 = (int)((int64_t)(rank + 1) * U / S);
+      for (int u = u0 + t; u < u1; u += kGroups * kDecomp) {
+        const uint32_t la = sA + (uint32_t)u * 16;
+        float4 v = ld_cluster_f4(la, 0);
+        for (int p = 1; p < S; ++p) {  // fixed rank order: partials over consecutive K ranges
+          const float4 w = ld_cluster_f4(la, (uint32_t)p);
+          v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+        }
+        const int n = u >> 5, row = (u & 31) * 4;
+        const int64_t ng = n0 + n;
+        if (ng < a.N) {
+          raw_t* yp = (raw_t*)a.Y + ng * a.ldy + m0 + row;
+          const float f[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (row + e < mt) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
+        }
+      }
+    }
+    cluster_sync_all();  // peers' shared memory stays alive until every slice is read
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -277,38 +326,73 @@ __global__ void spmm_cc_kernel(const uint8_t* __restrict__ W, const void* __rest
   }
 }
 
-template <int DT, int IS>
+// Split-K factor for a row-tile count and chunk count: enough clusters to cover the SMs once, never
+// more chunks than exist. Depends only on (M, K), never on N.
+int split_k(int64_t tiles, int64_t NC) {
+  int64_t S = bsk::dev_props().sms / tiles;
+  if (S > kMaxCluster) S = kMaxCluster;
+  if (S > NC) S = NC;
+  return S < 1 ? 1 : (int)S;
+}
+
+template <int DT>
 cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
                       int64_t ldy, cudaStream_t s) {
+  if (((uintptr_t)X & 15) != 0 || (ldx % 8) != 0) return cudaErrorNotSupported;  // TMA: 16-byte rows
   TcArgs a;
   a.W = (const uint8_t*)packed;
-  a.X = X;
   a.Y = Y;
-  a.M = g.M; a.K = g.K; a.NB = g.NB; a.N = N; a.ldx = ldx; a.ldy = ldy;
-  a.B = g.B; a.k = g.k; a.CB = g.V; a.NC = (int)g.NBf; a.is = g.is; a.tile_stride = g.offB;
+  a.M = g.M; a.NB = g.NB; a.N = N; a.ldy = ldy;
+  a.B = g.B; a.k = g.k; a.CB = g.V; a.NC = (int)g.NBf; a.tile_stride = g.offB;
+  a.blob_max = (int)(bsk::align_up((int64_t)BM * g.V * g.k * 2, 16) + bsk::align_up((int64_t)BM * g.V * g.k, 16));
+  a.S = split_k(g.P, g.NBf);
+  auto kern = spmm_tc_kernel<DT>;
+  static int static_smem = -1;
+  if (static_smem < 0) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             bsk::dev_props().smem_optin - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) return e;
+    static_smem = (int)fa.sharedSizeBytes;
+  }
+  // NA dense A tiles + NSB stages of (X tile, blob): BN as large as 4 stages allow (<= 256), then as
+  // many stages as fit (deep rings keep enough bytes in flight when blobs are small)
+  const int64_t avail = bsk::dev_props().smem_optin - static_smem - 1024;  // 1024: alignment slack
+  const int64_t ring = avail - (int64_t)NA * BM * 128;
+  int64_t bn_max = ((ring / 4 - a.blob_max) / 128) / 16 * 16;
+  if (bn_max > 256) bn_max = 256;
+  if (bn_max < 16) return cudaErrorNotSupported;
   int64_t BN = (N + 15) / 16 * 16;
-  if (BN > 256) BN = 256;
+  if (BN > bn_max) BN = bn_max;
   a.BN = (int)BN;
-  a.blob_max = (int)(bsk::align_up((int64_t)BM * g.V * g.k * 2, 16) + bsk::align_up((int64_t)BM * g.V * g.k * g.is, 16));
-  a.xvec = (((uintptr_t)X & 15) == 0) && (ldx % 8 == 0);
-  const uint32_t fmt = DT == BS_BF16 ? 1u : 0u;
-  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  a.idesc = idesc_f16(DT == BS_BF16, BM, (int)BN, false);
   int cols = 32;
   while (cols < BN) cols <<= 1;
   a.tmem_cols = cols;
-  const int64_t smem = 1024 + 2LL * BM * 128 + 2LL * BN * 128 + (int64_t)NSB * a.blob_max;
-  auto kern = spmm_tc_kernel<DT, IS>;
-  static int configured = 0;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         bsk::dev_props().smem_optin - 1024);
-    if (e != cudaSuccess) return e;
-    configured = 1;
-  }
-  if (smem > bsk::dev_props().smem_optin - 1024) return cudaErrorNotSupported;
-  dim3 grid((unsigned)g.P, (unsigned)((N + BN - 1) / BN));
-  kern<<<grid, kThreads, (size_t)smem, s>>>(a);
-  return cudaGetLastError();
+  int64_t nsb = ring / (BN * 128 + a.blob_max);
+  if (nsb > kMaxStages) nsb = kMaxStages;
+  nsb &= ~1LL;  // even: each decompress group keeps to one stage parity
+  if (nsb < 4) return cudaErrorNotSupported;
+  a.NSB = (int)nsb;
+  const int64_t smem = 1024 + (int64_t)NA * BM * 128 + nsb * (BN * 128 + a.blob_max);
+  if (a.S > 1 && BN * BM * 4 > smem - 1024) return cudaErrorNotSupported;  // partial tile must fit
+  CUtensorMap tX;
+  if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, KC, (int)BN)) return cudaErrorNotSupported;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(g.P * a.S), (unsigned)((N + BN - 1) / BN));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)a.S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tX, a);
 }
 
 template <int DT, int IS>
@@ -338,10 +422,8 @@ cudaError_t bsk_launch_spmm(const bsk::Geom& g, const void* packed, const void* 
   }
   const bool tc = g.es == 2 && (64 % g.B) == 0;
   if (tc) {
-    cudaError_t e = g.dt == BS_BF16 ? (g.is == 1 ? launch_tc<BS_BF16, 1>(g, packed, X, N, ldx, Y, ldy, s)
-                                                 : launch_tc<BS_BF16, 2>(g, packed, X, N, ldx, Y, ldy, s))
-                                    : (g.is == 1 ? launch_tc<BS_F16, 1>(g, packed, X, N, ldx, Y, ldy, s)
-                                                 : launch_tc<BS_F16, 2>(g, packed, X, N, ldx, Y, ldy, s));
+    cudaError_t e = g.dt == BS_BF16 ? launch_tc<BS_BF16>(g, packed, X, N, ldx, Y, ldy, s)
+                                    : launch_tc<BS_F16>(g, packed, X, N, ldx, Y, ldy, s);
     if (e != cudaErrorNotSupported) return e;
   }
   switch (g.dt) {

@@ -12,10 +12,10 @@
 //     fp32 accumulator in tensor memory; tcgen05.commit releases the stage.
 //   - Epilogue: tcgen05.ld → Y [N][M].
 // No decompression: the tensor core consumes the packed bytes directly.
-#include <cuda.h>
 
 #include "bs_common.cuh"
 #include "bs_device.cuh"
+#include "bs_tc.cuh"
 
 namespace {
 
@@ -34,35 +34,7 @@ struct Sp24Args {
   int mstride;          // TMEM columns between the metadata of consecutive K = 32 steps
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done)
-                 : "r"(bar), "r"(parity)
-                 : "memory");
-  }
-}
-__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
-         ((uint64_t)2 << 61);
-}
+using namespace bsk_tc;
 
 template <int DT>
 __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_constant__ CUtensorMap tA,
@@ -220,37 +192,6 @@ __global__ void sp24_cc_kernel(const uint8_t* __restrict__ vals, const uint8_t* 
   }
 }
 
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
-                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn encode_fn() {
-  static EncodeFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = (EncodeFn)p;
-  }
-  return fn;
-}
-
-// 2-D tensor map of a row-major [rows][cols] 16-bit matrix with row stride `ld` elements; box
-// (bc columns, br rows), 128-byte swizzle, zero fill out of bounds.
-bool make_map(CUtensorMap* m, int dt, const void* base, int64_t cols, int64_t rows, int64_t ld, int bc, int br) {
-  EncodeFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
-  cuuint32_t es[2] = {1, 1};
-  const CUtensorMapDataType t = dt == BS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  return fn(m, t, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
-}
-
 template <int DT>
 cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
                         int64_t ldy, cudaStream_t s) {
@@ -258,17 +199,15 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   if (BN > 64) BN = N >= 192 ? 128 : 64;  // more CTAs along N for big batches
   CUtensorMap tA, tX;
   const uint8_t* base = (const uint8_t*)packed;
-  if (!make_map(&tA, DT, base + g.offA, g.K / 2, g.M, g.K / 2, 64, BM)) return cudaErrorNotSupported;
-  if (!make_map(&tX, DT, X, g.K, N, ldx, 64, BN)) return cudaErrorNotSupported;
+  if (!bsk_make_map_2d(&tA, DT, base + g.offA, g.K / 2, g.M, g.K / 2, 64, BM)) return cudaErrorNotSupported;
+  if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, 64, BN)) return cudaErrorNotSupported;
   Sp24Args a;
   a.meta = base + g.offB;
   a.Y = Y;
   a.M = g.M; a.K = g.K; a.N = N; a.ldy = ldy;
   a.BN = BN;
   a.NC = (int)(g.K / KCH);
-  const uint32_t fmt = DT == BS_BF16 ? 1u : 0u;
-  // sparse flag (bit 2), f32 accumulate, K-major A and B, N = BN, M = 128
-  a.idesc = (1u << 2) | (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  a.idesc = idesc_f16(DT == BS_BF16, BM, BN, true);
   a.mstride = 4;  // the metadata address of each K = 32 step must be 4-column aligned (stride 1 faults)
   int p2 = 32;
   while (p2 < BN) p2 <<= 1;
@@ -305,6 +244,35 @@ cudaError_t launch_cc24(const bsk::Geom& g, const void* packed, const void* X, i
 }
 
 }  // namespace
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeFn)p;
+  }
+  return fn;
+}
+
+bool bsk_make_map_2d(CUtensorMap* m, int dt, const void* base, int64_t cols, int64_t rows, int64_t ld, int bc, int br) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
+  cuuint32_t es[2] = {1, 1};
+  const CUtensorMapDataType t = dt == BS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  return fn(m, t, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
 
 // Y = W·X for W in SP24 layout. The tensor path needs f16/bf16, K % 128 == 0, 16-byte aligned X rows and
 // N >= 2 (batch 1 is memory-bound: the CUDA-core kernel serves it).

@@ -13,8 +13,11 @@ cudaError_t bsk_spmv_dispatch_f32(const bsk::Geom& g, const SpmvArgs& a, cudaStr
 
 // nv = 1: SpMV (y = W·x). nv = 8: one pass over W for up to 8 batch columns (16-bit dtypes): column
 // n of X at x + n·ldx, column n of Y at y + n·ldy, n < ncols.
+// chunk_nv: the slot width that fixes the K-chunking (the panels summed per partial). Batch passes of
+// every width use chunk_nv = 8, so a column's fp32 summation order does not depend on the pass width
+// (NV = 2, 4, 8 accumulate each column in the same order), i.e. on N.
 static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const void* x, int64_t ldx, void* y,
-                                  int64_t ldy, int ncols, int nv, cudaStream_t s) {
+                                  int64_t ldy, int ncols, int nv, int chunk_nv, cudaStream_t s) {
   SpmvArgs a;
   const uint8_t* base = (const uint8_t*)packed;
   a.A = base + g.offA;
@@ -37,10 +40,10 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
   a.xvec = aligned && (g.es == 2 ? g.B % 8 == 0 : g.B % 4 == 0);
   // chunking of the K dimension by whole panels (depends only on K, B, dtype: deterministic)
   const int64_t group_bytes = (int64_t)g.B * 32 * g.es * nv;  // 32 blocks of x slots
-  const int64_t panel_bytes = group_bytes * g.V;
+  const int64_t chunk_group = (int64_t)g.B * 32 * g.es * chunk_nv;
   const int64_t tail_groups = (g.NB + 31) / 32 - g.NBf * g.V;
   if (g.NBf > 0 && g.k > 0) {
-    int64_t PC = kXBudget / panel_bytes;
+    int64_t PC = kXBudget / (chunk_group * g.V);
     if (PC < 1) PC = 1;
     if (PC > g.NBf) PC = g.NBf;
     int64_t nchunks = (g.NBf + PC - 1) / PC;
@@ -52,8 +55,8 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
     const int64_t last_np = g.NBf - (nchunks - 1) * PC;
     a.PC = (int)PC;
     a.nchunks = (int)nchunks;
-    a.tail_in_last = (last_np * g.V + tail_groups) * group_bytes <= kXBudget;
-    int64_t xb = PC * panel_bytes;
+    a.tail_in_last = (last_np * g.V + tail_groups) * chunk_group <= kXBudget;
+    int64_t xb = PC * g.V * group_bytes;
     const int64_t need_last = (last_np * g.V + (a.tail_in_last ? tail_groups : 0)) * group_bytes;
     if (need_last > xb) xb = need_last;
     if (!a.tail_in_last && tail_groups * group_bytes > xb) xb = tail_groups * group_bytes;
@@ -74,16 +77,19 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
 }
 
 cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, cudaStream_t s) {
-  return launch_spmv_nv(g, packed, x, 0, y, 0, 1, 1, s);
+  return launch_spmv_nv(g, packed, x, 0, y, 0, 1, 1, 1, s);
 }
 
-// Batched product on the SPMV layout (16-bit): passes of 8 batch columns, each one stream of W.
+// Batched product on the SPMV layout (16-bit): passes of up to 8 batch columns, each one stream of W;
+// a pass of w columns uses x slots of NV = 2, 4 or 8 columns (the smallest >= w).
 cudaError_t bsk_launch_spmv_batch(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,
                                   void* Y, int64_t ldy, cudaStream_t s) {
   if (g.es != 2) return cudaErrorNotSupported;
   for (int64_t n0 = 0; n0 < N; n0 += 8) {
     const int nc = (int)((N - n0) < 8 ? (N - n0) : 8);
-    cudaError_t e = launch_spmv_nv(g, packed, (const uint16_t*)X + n0 * ldx, ldx, (uint16_t*)Y + n0 * ldy, ldy, nc, 8, s);
+    const int nv = nc <= 2 ? 2 : nc <= 4 ? 4 : 8;
+    cudaError_t e =
+        launch_spmv_nv(g, packed, (const uint16_t*)X + n0 * ldx, ldx, (uint16_t*)Y + n0 * ldy, ldy, nc, nv, 8, s);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

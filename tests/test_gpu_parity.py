@@ -169,6 +169,40 @@ def test_spmm_column_independence(bs):
         assert torch.equal(bs.spmm(A, X[n0:n1].contiguous()), Y64[n0:n1])
 
 
+def test_spmm_spmv_layout_pass_widths(bs):
+    """SPMV-layout SpMM: passes of 1..8 columns (x slots NV = 2, 4, 8) share one K-chunking, so column
+    n is bit-identical for every N (K spans several x chunks plus a tail), and matches the oracle."""
+    M, K, B, k = 150, 16384 + 32 * 40, 32, 3
+    W = synth.matrix(M, K, "f16", seed=64)
+    X = synth.vector(K, "f16", seed=65, n=13)
+    vals, idx, ov, oi = _prune_parity(bs, W, "f16", B, k)
+    A = bs.pack(vals, idx, K, B, layout="spmv")
+    Xd = X.cuda()
+    Y13 = bs.spmm(A, Xd)
+    for n0, n1 in ((0, 1), (3, 5), (5, 9), (9, 12), (12, 13)):
+        assert torch.equal(bs.spmm(A, Xd[n0:n1].contiguous()), Y13[n0:n1]), (n0, n1)
+    Yr, bound = oracle.spmm(ov, oi, oracle.F16, M, K, B, k, synth.to_numpy(X))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y13), oracle.F16), Yr, bound, oracle.TAU[oracle.F16])
+    assert ok, worst
+
+
+@pytest.mark.parametrize("M", [77, 700, 4096 + 33, 9800])
+def test_spmm_tc_split_k(bs, M):
+    """K6 split-K over a cluster: the row-tile count sets S (1 tile -> 8, 6 -> 8, 33 -> 4, 77 -> 1 on
+    148 SMs); every S matches the oracle, and columns stay independent of N."""
+    K, B, k, N = 2048 + 32, 32, 4, 24
+    W = synth.matrix(M, K, "bf16", seed=66)
+    X = synth.vector(K, "bf16", seed=67, n=N)
+    vals, idx, ov, oi = _prune_parity(bs, W, "bf16", B, k)
+    A = bs.pack(vals, idx, K, B, layout="spmm")
+    Xd = X.cuda()
+    Y = bs.spmm(A, Xd)
+    Yr, bound = oracle.spmm(ov, oi, oracle.BF16, M, K, B, k, synth.to_numpy(X))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y), oracle.BF16), Yr, bound, oracle.TAU[oracle.BF16])
+    assert ok, worst
+    assert torch.equal(bs.spmm(A, Xd[7:8].contiguous()), Y[7:8])
+
+
 def test_spmv_host_e2e(bs):
     M, K, B, k = 512, 4096, 32, 3
     W = synth.matrix(M, K, "f16", seed=50)

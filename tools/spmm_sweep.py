@@ -19,7 +19,8 @@ from bench import dense_from_canonical, graph_time_us  # noqa: E402
 
 SHAPES = {"fc6": (4096, 25088, [0.9], [8, 32]), "fc7": (4096, 4096, [0.9], [8, 32]),
           "ctc_ih": (4096, 2048, [0.875], [1, 2, 4, 8, 16, 32, 64, 128, 256]),
-          "ctc_hh": (4096, 1024, [0.875], [8, 64, 256]), "bench": (16384, 8192, [0.5, 0.9], [8])}
+          "ctc_hh": (4096, 1024, [0.875], [8, 64, 256]), "bench": (16384, 8192, [0.5, 0.9], [8]),
+          "sq16k": (16384, 16384, [0.5, 0.9], [1, 8, 32, 128, 256, 1024])}
 
 
 def main(names):
@@ -28,11 +29,12 @@ def main(names):
     for name in names:
         M, K, sps, Ns = SHAPES[name]
         W = synth.matrix(M, K, "f16", seed=3, device=dev)
-        for s in sps:
-            k = bs.k_from_sparsity(32, s)
-            v, i, _ = bs.prune(W, 32, k=k)
-            A = bs.pack(v, i, K, 32, layout=LAYOUT)
-            Wd = dense_from_canonical(v, i, M, K, 32)
+        B = 4 if LAYOUT == "sp24" else 32
+        for s in ([0.5] if LAYOUT == "sp24" else sps):
+            k = bs.k_from_sparsity(B, s)
+            v, i, _ = bs.prune(W, B, k=k)
+            A = bs.pack(v, i, K, B, layout=LAYOUT)
+            Wd = dense_from_canonical(v, i, M, K, B)
             C = max(1, -(-3 * l2 // A.nbytes))
             mats = [A] + [bs.BSMatrix(A.M, A.K, A.block, A.k, A.dtype, A.layout, A.packed.clone()) for _ in range(C - 1)]
             Cd = max(1, -(-3 * l2 // (Wd.numel() * 2)))
