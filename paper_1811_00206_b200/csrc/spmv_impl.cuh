@@ -11,15 +11,16 @@
 //     as soon as the warp has consumed it, and mbarriers with transaction counts signal arrival. So
 //     the bytes in flight do not depend on register pressure or on the compute phase
 //     (tools/membench.cu: >= 6.9 TB/s at 64 KB in flight per SM).
-//   - x is staged per CTA in a block-interleaved order of 32-bit slots: element (b, o) of a chunk
-//     goes to word (gl·B + o)·32 + (b & 31), with gl = (b>>5) - first group of the chunk. 16-bit
-//     values sit zero-extended in the low half. Lane l only ever touches bank l, whatever the
-//     indices are, so every gather is conflict-free by construction. The slot address is one
-//     IMAD of the index byte (extracted by one PRMT): 4 instructions per nonzero including the
-//     FHFMA. Staging is lane-per-block too, so its stores are conflict-free; all of a lane's loads
-//     are issued before its stores.
-//   - K is processed in chunks of whole panels when x does not fit in shared memory (65536 columns
-//     of 16-bit x take 256 KB as slots). Each (row, chunk) partial is reduced by the warp and added
+//   - x is staged per CTA in a block-interleaved order of slots (halfwords for f16/bf16, words for
+//     f32; NV·2 bytes holding NV batch columns for the batched variant): element (b, o) of a chunk
+//     goes to slot (gl·B + o)·32 + (b & 31), with gl = (b>>5) - first group of the chunk. Lane l
+//     only ever touches its own bank (16-bit: lanes 2m, 2m+1 share a word, which is a broadcast,
+//     not a conflict), whatever the indices are, so every gather is conflict-free by construction.
+//     The slot address is one IMAD of the index byte (extracted by one PRMT): about 4 instructions
+//     per nonzero including the FHFMA. Staging is lane-per-block too, so its stores are
+//     conflict-free; all of a lane's loads are issued before its stores.
+//   - K is processed in chunks of whole panels when x does not fit in 128 KB of shared memory (16-bit
+//     x fits up to 65536 columns; f32 x and the batched variant chunk). Each (row, chunk) partial is reduced by the warp and added
 //     in chunk order. The tail blocks (T < 32·V per row) follow through the same ring.
 //   - f16/bf16 products are one FHFMA (exact 16x16 product, fp32 accumulate). Each lane keeps V
 //     independent accumulators. They are summed in a fixed order and reduced with a warp butterfly.
