@@ -469,6 +469,63 @@ def layer_rows(a, bs, hbm_peak, l2):
                            "o_time = measured empty-kernel graph node (P:264-266, SURVEY A18)"}
 
 
+def spmm_rows(a, bs, hbm_peak, l2):
+    """SpMM legs of BASELINE configs[2] (fc6/fc7 at batch 32) and configs[3] (CTC batch sweep 1-256 with the
+    balanced B = 32 layer and the 2:4 sparse-MMA path), CUDA-graph timed with rotating copies, next to cuBLAS
+    dense GEMM on the same W_bs. Paths: K4 = CUDA-core batched SpMV (SPMV layout), K6 = decompress + tcgen05.mma
+    (SPMM layout), K5 = tcgen05.mma.sp (SP24 layout)."""
+    rows = []
+    dev = torch.device("cuda")
+    shapes = [("configs[2] VGG fc6 4096x25088", 4096, 25088, [0.9], [32]),
+              ("configs[2] VGG fc7 4096x4096", 4096, 4096, [0.5, 0.9], [32]),
+              ("configs[3] CTC W_ih 4096x2048", 4096, 2048, [0.875], [1, 2, 4, 8, 16, 32, 64, 128, 256]),
+              ("configs[3] CTC W_hh 4096x1024", 4096, 1024, [0.875], [8, 64, 256])]
+
+    def timed(mats, X, Y):
+        C = len(mats)
+        return graph_time_us(lambda j: bs.spmm(mats[j % C], X, out=Y), 20 * C if C < 10 else 2 * C)
+
+    def dense_time(Wbs, X):
+        Cd = max(1, -(-3 * l2 // (Wbs.numel() * Wbs.element_size())))
+        dens = [Wbs] + [Wbs.clone() for _ in range(Cd - 1)]
+        return graph_time_us(lambda j: torch.matmul(X, dens[j % Cd].t()), 4 * Cd)
+
+    for name, M, K, sps, Ns in shapes:
+        W = synth.matrix(M, K, a.dtype, seed=synth.seed_for(3, M + K), device=dev)
+        variants = []
+        for s in sps:
+            ks = bs.k_from_sparsity(a.block, s)
+            v, i, _ = bs.prune(W, a.block, k=ks)
+            variants.append((f"B={a.block} s={s}", a.block, ks, v, i, {"K4": "spmv", "K6": "spmm"}))
+        if "CTC W_ih" in name:  # the 2:4 shape (B = 4, 50%) of the same layer
+            v, i, _ = bs.prune(W, 4, k=2)
+            variants.append(("2:4 (B=4 s=0.5)", 4, 2, v, i, {"K5": "sp24"}))
+        for label, B, ks, v, i, paths in variants:
+            Wbs = dense_from_canonical(v, i, M, K, B)
+            packed = {kn: rotating(bs, bs.pack(v, i, K, B, layout=lay), l2) for kn, lay in paths.items()}
+            for N in Ns:
+                X = synth.vector(K, a.dtype, seed=synth.seed_for(3, N), n=N, device=dev)
+                Y = torch.empty((N, M), dtype=W.dtype, device=dev)
+                td = dense_time(Wbs, X)
+                row = {"layer": name, "variant": label, "N": N, "cublas_dense_us": round(td, 2)}
+                best = None
+                for kn, mats in packed.items():
+                    t = timed(mats, X, Y)
+                    pk = mats[0].nbytes + N * (K + M) * W.element_size()
+                    row[f"{kn}_us"] = round(t, 2)
+                    row[f"{kn}_packed_GBps"] = round(pk / t / 1e3, 1)
+                    if best is None or t < best[1]:
+                        best = (kn, t)
+                row["best"] = best[0]
+                row["speedup_vs_cublas"] = round(td / best[1], 2)
+                row["TFLOPs_nnz"] = round(2.0 * M * (K // B) * ks * N / best[1] / 1e6, 2)
+                rows.append(row)
+            del packed, Wbs
+        del W
+    return {"spmm": rows, "spmm_note": "graph-timed, rotating copies (> 3x L2); TFLOPs_nnz counts 2 flops per stored "
+                                       "nonzero per batch column; packed_GBps = (packed W + X + Y) / time"}
+
+
 def extras(a, bs, W, A, vals, idx, x, k, es, hbm_peak, stream):
     """N=1 context: the 65536^2 sparsity sweep against cuBLAS dense GEMV and cuSPARSE CSR (int32) on the same
     W_bs, the paper's layer shapes, and the oracle CPU baseline."""
@@ -507,6 +564,7 @@ def extras(a, bs, W, A, vals, idx, x, k, es, hbm_peak, stream):
     res["baselines"] = {"cublas_dense_us": round(t_dense, 2), "cublas_path": f"torch.{dense_name} on dense W_bs (f16)",
                         "cusparse_path": "torch.mv on int32 CSR of W_bs (cusparseSpMV)"}
     res.update(layer_rows(a, bs, hbm_peak, l2))
+    res.update(spmm_rows(a, bs, hbm_peak, l2))
     res["paper_context"] = ("paper: 1.4-3.1x over cuBLAS/cuSPARSE/block-sparse on an unnamed ~2018 GPU (P:8, P:48); "
                             "context only, not a target")
     # oracle on host cores

@@ -52,22 +52,6 @@ struct TcArgs {
   int tmem_cols;
 };
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ float4 ld_cluster_f4(uint32_t local_addr, uint32_t rank) {
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(rank));
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
-  return v;
-}
-
 template <int DT>
 __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_constant__ CUtensorMap tX, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -331,7 +315,7 @@ __global__ void spmm_cc_kernel(const uint8_t* __restrict__ W, const void* __rest
 int split_k(int64_t tiles, int64_t NC) {
   int64_t S = bsk::dev_props().sms / tiles;
   if (S > kMaxCluster) S = kMaxCluster;
-  if (S > NC) S = NC;
+  if (S > NC / 6) S = NC / 6;  // at least 6 chunks per CTA: fixed costs stay amortised
   return S < 1 ? 1 : (int)S;
 }
 

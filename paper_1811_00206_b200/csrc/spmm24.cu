@@ -3,7 +3,9 @@
 //
 // The SP24 layout (docs/layout.md) is already the operand format of a 2:4 sparse MMA: the kept values
 // form the compressed A (M × K/2, row-major) and the block nibbles idx0 | idx1 << 2 form the metadata
-// (M × K/8 bytes). Per CTA: a 128-row tile of W and BN batch columns; K in chunks of 128 columns.
+// (M × K/8 bytes). Per CTA: a 128-row tile of W, BN <= 128 batch columns and a contiguous range of the
+// 128-column K chunks (split-K over a cluster of S CTAs, S from M and K only; the S fp32 partial tiles
+// are summed in rank order through distributed shared memory, as in K6).
 //   - One producer lane issues TMA tensor copies (cp.async.bulk.tensor.2d, 128-byte swizzle): the
 //     compressed A chunk (128 rows × 64 values) and the X chunk (BN rows × 2 atoms of 64 columns).
 //   - 128 threads (thread = row) copy their 16 metadata bytes of the chunk into tensor memory with
@@ -21,14 +23,16 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int KCH = 128;  // original columns per chunk (64 compressed values: one 128-byte swizzle atom)
-constexpr int NST = 4;    // pipeline stages
+constexpr int kMaxStages = 4;  // pipeline stages (runtime NST: 2..4, fewer for BN = 256)
 constexpr int kThreads = 192;
 
 struct Sp24Args {
   const uint8_t* meta;  // M × K/8 bytes
   void* Y;
   int64_t M, K, N, ldy;
-  int BN, NC;           // batch columns per CTA (multiple of 16), chunks
+  int BN, NC;           // batch columns per CTA (multiple of 16), chunks per row tile
+  int S;                // split-K cluster size
+  int NST;              // pipeline stages
   uint32_t idesc;
   int tmem_cols, meta_col;
   int mstride;          // TMEM columns between the metadata of consecutive K = 32 steps
@@ -40,18 +44,23 @@ template <int DT>
 __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_constant__ CUtensorMap tA,
                                                              const __grid_constant__ CUtensorMap tX, Sp24Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bars[3 * NST + 1];
+  __shared__ __align__(8) uint64_t bars[3 * kMaxStages + 1];
+  using raw_t = uint16_t;
   __shared__ uint32_t tmem_holder;
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t ASZ = BM * 128;                 // compressed A chunk: 128 rows × 128 B
   const uint32_t BSZ = 2u * (uint32_t)a.BN * 128;  // X chunk: 2 atoms of BN rows × 128 B
+  const int NST = a.NST;
   const uint32_t sA = smem_u32(smem), sB = sA + NST * ASZ;
-  const uint32_t full = smem_u32(&bars[0]), empty = smem_u32(&bars[NST]), meta_ok = smem_u32(&bars[2 * NST]);
-  const uint32_t acc_full = smem_u32(&bars[3 * NST]);
+  const uint32_t full = smem_u32(&bars[0]), empty = smem_u32(&bars[kMaxStages]);
+  const uint32_t meta_ok = smem_u32(&bars[2 * kMaxStages]), acc_full = smem_u32(&bars[3 * kMaxStages]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int S = a.S;
+  const int rank = S > 1 ? (int)cluster_rank() : 0;
+  const int64_t m0 = (int64_t)(blockIdx.x / S) * BM;
   const int64_t mt = (a.M - m0) < BM ? (a.M - m0) : BM;
   const int64_t n0 = (int64_t)blockIdx.y * a.BN;
+  const int c0 = (int)((int64_t)rank * a.NC / S), nloc = (int)((int64_t)(rank + 1) * a.NC / S) - c0;  // >= 1
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -76,20 +85,23 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      for (int c = 0; c < a.NC; ++c) {
-        const int s = c % NST;
-        if (c >= NST) mbar_wait(empty + 8 * s, (uint32_t)(((c / NST) - 1) & 1));
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nloc; ++i) {
+        const int c = c0 + i;
+        if (i >= NST) mbar_wait(empty + 8 * s, ph ^ 1u);
         mbar_expect_tx(full + 8 * s, ASZ + BSZ);
         tma_2d(sA + s * ASZ, &tA, c * (KCH / 2), (int)m0, full + 8 * s);
         tma_2d(sB + s * BSZ, &tX, c * KCH, (int)n0, full + 8 * s);
         tma_2d(sB + s * BSZ + (uint32_t)a.BN * 128, &tX, c * KCH + 64, (int)n0, full + 8 * s);
+        if (++s == NST) { s = 0; ph ^= 1u; }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- sparse MMA issuer
-      for (int c = 0; c < a.NC; ++c) {
-        const int s = c % NST;
-        const uint32_t par = (uint32_t)((c / NST) & 1);
+      int s = 0;
+      uint32_t par = 0;
+      for (int i = 0; i < nloc; ++i) {
         mbar_wait(full + 8 * s, par);
         mbar_wait(meta_ok + 8 * s, par);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -99,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
           // A: 16 compressed values (32 B) per K = 32 step; B: 32 columns (64 B) per step, atom j / 2
           const uint64_t db = sw128_desc(sB + s * BSZ + (uint32_t)(j >> 1) * (uint32_t)a.BN * 128) + (uint64_t)((j & 1) * 4);
           const uint32_t te = tmem + (uint32_t)a.meta_col + (uint32_t)((s * 4 + j) * a.mstride);
-          const uint32_t acc = (c > 0 || j > 0) ? 1u : 0u;
+          const uint32_t acc = (i > 0 || j > 0) ? 1u : 0u;
           asm volatile(
               "{ .reg .pred p; setp.ne.b32 p, %5, 0;\n\t"
               "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, p; }" ::"r"(tmem),
@@ -107,22 +119,28 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty + 8 * s)
                      : "memory");
+        if (++s == NST) { s = 0; par ^= 1u; }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(acc_full)
                    : "memory");
     }
   } else {
-    // ---- metadata → tensor memory (thread = row u); then the epilogue
-    const int u = threadIdx.x - 64;
+    // ---- metadata → tensor memory (thread = row); then the epilogue. A row's 16 metadata bytes of a
+    // chunk are loaded two chunks ahead, so the global latency overlaps the MMAs.
     const int q = warp & 3;  // TMEM lane quarter of this warp: rows 32q .. 32q + 31
     const int64_t row = 32 * q + lane;
-    const uint8_t* mrow = a.meta + (m0 + row) * (a.K / 8);
-    (void)u;
-    for (int c = 0; c < a.NC; ++c) {
-      const int s = c % NST;
-      if (c >= NST) mbar_wait(empty + 8 * s, (uint32_t)(((c / NST) - 1) & 1));
-      uint4 m = make_uint4(0u, 0u, 0u, 0u);
-      if (row < mt) m = __ldg((const uint4*)(mrow + c * 16));
+    const uint8_t* mrow = a.meta + (m0 + row) * (a.K / 8) + (int64_t)c0 * 16;
+    auto ldm = [&](int i) {
+      return (row < mt && i < nloc) ? __ldg((const uint4*)(mrow + (int64_t)i * 16)) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    uint4 m_cur = ldm(0), m_nxt = ldm(1);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nloc; ++i) {
+      if (i >= NST) mbar_wait(empty + 8 * s, ph ^ 1u);
+      const uint4 m = m_cur;
+      m_cur = m_nxt;
+      m_nxt = ldm(i + 2);
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)a.meta_col + (uint32_t)(s * 4 * a.mstride);
       const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
@@ -140,17 +158,21 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(meta_ok + 8 * s);
+      if (++s == NST) { s = 0; ph ^= 1u; }
     }
     mbar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    using raw_t = uint16_t;
+    float* red = (float*)smem;  // split-K partial tile [BN][128] (the rings are idle now)
     for (int nb = 0; nb < a.BN; nb += 8) {
       uint32_t r[8];
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                    : "r"(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)nb));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < mt) {
+      if (S > 1) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) red[(nb + e) * BM + row] = __uint_as_float(r[e]);
+      } else if (row < mt) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int64_t ng = n0 + nb + e;
@@ -158,6 +180,32 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
         }
       }
     }
+  }
+  if (S > 1) {  // fixed-order sum of the S partial tiles through distributed shared memory
+    cluster_sync_all();
+    if (warp >= 2) {
+      const int t = threadIdx.x - 64;
+      const int U = a.BN * BM / 4;
+      const int u0 = (int)((int64_t)rank * U / S), u1 = (int)((int64_t)(rank + 1) * U / S);
+      for (int u = u0 + t; u < u1; u += 128) {
+        const uint32_t la = sA + (uint32_t)u * 16;
+        float4 v = ld_cluster_f4(la, 0);
+        for (int p = 1; p < S; ++p) {
+          const float4 w = ld_cluster_f4(la, (uint32_t)p);
+          v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+        }
+        const int n = u >> 5, r4 = (u & 31) * 4;
+        const int64_t ng = n0 + n;
+        if (ng < a.N) {
+          raw_t* yp = (raw_t*)a.Y + ng * a.ldy + m0 + r4;
+          const float f[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (r4 + e < mt) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
+        }
+      }
+    }
+    cluster_sync_all();
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -196,7 +244,7 @@ template <int DT>
 cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
                         int64_t ldy, cudaStream_t s) {
   int BN = (int)((N + 15) / 16 * 16);
-  if (BN > 64) BN = N >= 192 ? 128 : 64;  // more CTAs along N for big batches
+  if (BN > 128) BN = 128;  // keeps a 4-stage ring (BN = 256 would leave 2 stages, measured slower)
   CUtensorMap tA, tX;
   const uint8_t* base = (const uint8_t*)packed;
   if (!bsk_make_map_2d(&tA, DT, base + g.offA, g.K / 2, g.M, g.K / 2, 64, BM)) return cudaErrorNotSupported;
@@ -218,7 +266,18 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   a.meta_col = p2;
   a.tmem_cols = cols;
   if (a.tmem_cols > 512) return cudaErrorNotSupported;
-  const int64_t smem = 1024 + (int64_t)NST * (BM * 128 + 2LL * BN * 128);
+  const int64_t stage = BM * 128 + 2LL * BN * 128;
+  int64_t nst = (bsk::dev_props().smem_optin - 2048) / stage;
+  if (nst > kMaxStages) nst = kMaxStages;
+  if (nst < 2) return cudaErrorNotSupported;
+  a.NST = (int)nst;
+  const int64_t smem = 1024 + nst * stage;
+  const int64_t tiles = (g.M + BM - 1) / BM;
+  int64_t S = bsk::dev_props().sms / tiles;  // split-K: from M and K only (never N)
+  if (S > 8) S = 8;
+  if (S > a.NC / 6) S = a.NC / 6;  // at least 6 chunks per CTA: fixed costs stay amortised
+  if (S < 1) S = 1;
+  a.S = (int)S;
   auto kern = spmm24_kernel<DT>;
   static int configured = 0;
   if (!configured) {
@@ -228,9 +287,19 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
     configured = 1;
   }
   if (smem > bsk::dev_props().smem_optin - 1024) return cudaErrorNotSupported;
-  dim3 grid((unsigned)((g.M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
-  kern<<<grid, kThreads, (size_t)smem, s>>>(tA, tX, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(tiles * S), (unsigned)((N + BN - 1) / BN));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tA, tX, a);
 }
 
 template <int DT>

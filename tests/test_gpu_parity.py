@@ -188,8 +188,8 @@ def test_spmm_spmv_layout_pass_widths(bs):
 
 @pytest.mark.parametrize("M", [77, 700, 4096 + 33, 9800])
 def test_spmm_tc_split_k(bs, M):
-    """K6 split-K over a cluster: the row-tile count sets S (1 tile -> 8, 6 -> 8, 33 -> 4, 77 -> 1 on
-    148 SMs); every S matches the oracle, and columns stay independent of N."""
+    """K6 split-K over a cluster: S = min(8, SMs / tiles, chunks / 6) (1 tile -> 5, 6 -> 5, 33 -> 4,
+    77 -> 1 on 148 SMs with 33 chunks); every S matches the oracle, and columns stay independent of N."""
     K, B, k, N = 2048 + 32, 32, 4, 24
     W = synth.matrix(M, K, "bf16", seed=66)
     X = synth.vector(K, "bf16", seed=67, n=N)
@@ -309,6 +309,23 @@ def test_sp24_spmm(bs, N, dname):
     Yr, bound = oracle.spmm(ov, oi, DT[dname], M, K, 4, 2, synth.to_numpy(X))
     ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y), DT[dname]), Yr, bound, 1e-2)
     assert ok, f"sp24 N={N}: worst {worst}"
+
+
+@pytest.mark.parametrize("M", [130, 4096, 9600])
+def test_sp24_split_k(bs, M):
+    """K5 split-K clusters (33 chunks): S = 5 (2 tiles), 4 (32 tiles), 1 (75 tiles); oracle parity and
+    N-independence."""
+    K, N = 4096 + 128, 40
+    W = synth.matrix(M, K, "f16", seed=68)
+    X = synth.vector(K, "f16", seed=69, n=N)
+    vals, idx, ov, oi = _prune_parity(bs, W, "f16", 4, 2)
+    A = bs.pack(vals, idx, K, 4, layout="sp24")
+    Xd = X.cuda()
+    Y = bs.spmm(A, Xd)
+    Yr, bound = oracle.spmm(ov, oi, oracle.F16, M, K, 4, 2, synth.to_numpy(X))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y), oracle.F16), Yr, bound, 1e-2)
+    assert ok, worst
+    assert torch.equal(bs.spmm(A, Xd[3:5].contiguous()), Y[3:5])
 
 
 def test_sp24_spmv_and_integer_exact(bs):
