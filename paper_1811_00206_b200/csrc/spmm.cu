@@ -2,18 +2,24 @@
 //
 // K6, tensor cores (f16/bf16, SPMM layout, B | 64). Per CTA: one 128-row tile of W, up to 256 batch
 // columns, and a contiguous range of the 64-column K chunks (split-K over a thread-block cluster).
-//   - Warp 0, one lane: per chunk, a bulk copy of the packed (tile, chunk) blob (docs/layout.md SPMM)
-//     and a TMA tensor copy of the BN × 64 X tile (128-byte swizzle, zero fill past N and K) into an
-//     NSB-stage ring (mbarrier complete_tx), 4..16 stages deep.
-//   - Warps 2..17: two groups of 8 warps, alternating chunks, rebuild the dense 128 × 64 A tile in one
-//     of NA = 4 buffers: a linear zero fill, a named barrier, then an entry-parallel scatter: thread
-//     t takes blob entries t, t+256, ... (consecutive lanes read consecutive values and indices:
-//     conflict-free; four entries' loads in flight before their stores) and stores each value
-//     at (row, (entry's block)·B + index) of the K-major SWIZZLE_128B tile. The balanced rows give every
-//     chunk the same entry count per row, so (row, block) follow from the entry number by a
-//     running quotient. fence.proxy.async publishes the stores to the tensor core.
-//   - Warp 1, one lane: 4 × tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = BN, K = 16) per chunk into
-//     the fp32 accumulator in tensor memory; tcgen05.commit frees the blob/X stage and the A buffer.
+//   - Warps 0..3, one lane each, chunks in turn: a bulk copy of the packed (tile, chunk) blob
+//     (docs/layout.md SPMM) and a TMA tensor copy of the BN × 64 X tile (128-byte swizzle, zero fill
+//     past N and K) into a ring of NSB = 4, 8, 12 or 16 stages (mbarrier complete_tx).
+//   - Warps 6..21: four groups of 4 warps, chunks in turn, rebuild the dense 128 × 64 A tile in one of
+//     NA = 4 or 8 buffers. A thread owns (row, block) units (at least 8 columns): it zero-fills the
+//     unit's 16-byte pieces of the K-major SWIZZLE_128B tile, then stores each kept value at
+//     (row, block·B + index). The balanced rows give every unit the same k entries per block,
+//     contiguous in the blob. The same thread zero-fills and scatters, so no barrier is needed;
+//     fence.proxy.async publishes the stores to the tensor core.
+//   - Warps 4 and 5, one lane each, alternating chunks: 4 × tcgen05.mma.cta_group::1.kind::f16
+//     (M = 128, N = BN, K = 16) per chunk into two fp32 accumulators in tensor memory (summed
+//     acc0 + acc1 in the epilogue). tcgen05.commit frees the blob/X stage and the A buffer. Measured
+//     with clock64, one issuing thread spends ~650 cycles per chunk (MMA issues ~80 cycles each,
+//     commits ~90, waits ~80 even when ready), which alone bounded the kernel at N <= 32; a second
+//     issuer gave 1.5x, a third and fourth nothing more.
+//   - Every stage and A buffer belongs to one producer, one group and one MMA warp (NSB, NA multiples
+//     of 4), which use it strictly in turn: mbarrier parity waits alias when a waiter runs two phases
+//     ahead (odd ring depths faulted on stale blob indices).
 //   - Epilogue: tcgen05.ld (32x32b) → Y [N][M]. With split-K (cluster of S CTAs along K), each CTA
 //     parks its fp32 partial tile in shared memory, and after a cluster barrier CTA j sums slice j of
 //     the tile over the S partials in rank order through distributed shared memory (ld.shared::cluster).
@@ -33,11 +39,15 @@ using namespace bsk_tc;
 
 constexpr int BM = 128;          // rows per tile (MMA M)
 constexpr int KC = 64;           // columns per chunk (one SWIZZLE_128B atom of 16-bit values)
-constexpr int NA = 4;            // dense A tile buffers
-constexpr int kMaxStages = 16;   // blob + X tile ring stages (runtime NSB: even, 4..16)
-constexpr int kDecomp = 256;     // threads per decompress group (8 warps)
-constexpr int kGroups = 2;       // decompress groups, alternating chunks
-constexpr int kThreads = 64 + kGroups * kDecomp;
+constexpr int kMaxNA = 8;        // dense A tile buffers (runtime NA: 4 or 8)
+constexpr int kMaxStages = 16;   // blob + X tile ring stages (runtime NSB: 4, 8, 12 or 16)
+constexpr int kDecomp = 128;     // threads per decompress group (4 warps)
+constexpr int kGroups = 4;       // decompress groups, chunks in turn (4 chunks rebuilt concurrently)
+constexpr int kProducers = 4;    // producer warps: one bulk copy takes ~0.3 us to issue (measured)
+constexpr int kMmaWarp = kProducers;  // first MMA warp
+constexpr int kMmaWarps = 2;          // MMA issuers (a tcgen05.mma issue costs ~80 cycles: one thread cannot keep up with N <= 32)
+constexpr int kFirstDecomp = 32 * (kProducers + kMmaWarps);
+constexpr int kThreads = kFirstDecomp + kGroups * kDecomp;
 constexpr int kMaxCluster = 8;   // split-K factor (portable cluster size)
 
 struct TcArgs {
@@ -46,30 +56,30 @@ struct TcArgs {
   int64_t M, NB, N, ldy;
   int B, k, CB, NC;   // block width, kept per block, blocks per chunk, chunks per row tile
   int64_t tile_stride;
-  int BN, S, NSB;     // batch columns per CTA (multiple of 16), split-K cluster size, ring stages
+  int BN, S, NSB, NA; // batch columns per CTA (multiple of 16), split-K cluster size, ring stages, A buffers
   int blob_max;       // bytes of a full blob (128 rows, CB blocks)
   uint32_t idesc;
-  int tmem_cols;
+  int tmem_cols, acc_cols;  // allocated columns; columns per accumulator (one per MMA warp)
 };
 
 template <int DT>
 __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_constant__ CUtensorMap tX, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bars[2 * kMaxStages + 2 * NA + 1];
+  __shared__ __align__(8) uint64_t bars[2 * kMaxStages + 2 * kMaxNA + 1];
   __shared__ uint32_t tmem_holder;
-  __shared__ uint8_t ctab[64];  // entry number within a row's chunk run -> block offset (entry / k)·B
   using raw_t = uint16_t;
   constexpr int ES = 2;
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const int NSB = a.NSB;
+  const int NSB = a.NSB, NA = a.NA;
   const uint32_t sA = smem_u32(smem);                          // NA × 16 KB dense A tiles
   const uint32_t XSZ = (uint32_t)a.BN * 128;                   // X tile: BN rows × 128 B
   const uint32_t sX = sA + NA * BM * 128;                      // NSB × XSZ
   const uint32_t sR = sX + (uint32_t)NSB * XSZ;                // NSB × blob_max
   const uint32_t full = smem_u32(&bars[0]), empty = smem_u32(&bars[kMaxStages]);
-  const uint32_t a_full = smem_u32(&bars[2 * kMaxStages]), a_empty = smem_u32(&bars[2 * kMaxStages + NA]);
-  const uint32_t acc_full = smem_u32(&bars[2 * kMaxStages + 2 * NA]);
+  const uint32_t a_full = smem_u32(&bars[2 * kMaxStages]), a_empty = smem_u32(&bars[2 * kMaxStages + kMaxNA]);
+  const uint32_t acc_full = smem_u32(&bars[2 * kMaxStages + 2 * kMaxNA]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lg_na = NA == 8 ? 3 : 2;
   const int S = a.S;
   const int rank = S > 1 ? (int)cluster_rank() : 0;
   const int64_t tile = blockIdx.x / S;
@@ -94,14 +104,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
       mbar_init(a_full + 8 * s, kDecomp);  // one decompress group
       mbar_init(a_empty + 8 * s, 1);
     }
-    mbar_init(acc_full, 1);
+    mbar_init(acc_full, kMmaWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x >= 64 && threadIdx.x < 128) {
-    const int q = threadIdx.x - 64;
-    ctab[q] = (uint8_t)(q < a.CB * k ? (q / k) * a.B : 0);
-  }
-  if (warp == 1) {  // tensor-memory accumulator: 128 lanes × tmem_cols fp32 columns
+  if (warp == kMmaWarp) {  // tensor-memory accumulator: 128 lanes × tmem_cols fp32 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_holder)),
                  "r"(a.tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -111,12 +117,12 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_d = tmem_holder;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---- producer
-      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tX) : "memory");
-      int s = 0;
+  if (warp < kProducers) {
+    if (lane == 0) {  // ---- producers: warp w issues chunks i = w, w + 4, ...
+      if (warp == 0) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tX) : "memory");
+      int s = warp % NSB;
       uint32_t ph = 0;
-      for (int i = 0; i < nloc; ++i) {
+      for (int i = warp; i < nloc; i += kProducers) {
         const int c = c0 + i;
         if (i >= NSB) mbar_wait(empty + 8 * s, ph ^ 1u);
         const int64_t cb = (a.NB - (int64_t)a.CB * c) < a.CB ? (a.NB - (int64_t)a.CB * c) : a.CB;
@@ -124,90 +130,95 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
         mbar_expect_tx(full + 8 * s, bytes + XSZ);
         bulk_g2s(sR + (uint32_t)s * (uint32_t)a.blob_max, tile_base + (int64_t)c * blobCB, bytes, full + 8 * s);
         tma_2d(sX + (uint32_t)s * XSZ, &tX, c * KC, (int)n0, full + 8 * s);
-        if (++s == NSB) { s = 0; ph ^= 1u; }
+        s += kProducers;
+        if (s >= NSB) { s -= NSB; ph ^= 1u; }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
-      int s = 0;
+  } else if (warp < kFirstDecomp / 32) {
+    if (lane == 0) {  // ---- MMA issuers: warp j issues chunks i = j, j + kMmaWarps, ... into accumulator j
+      const int j = warp - kMmaWarp;
+      const uint32_t acc_j = tmem_d + (uint32_t)(j * a.acc_cols);
+      int s = j % NSB;
       uint32_t ph = 0;
-      for (int i = 0; i < nloc; ++i) {
+      for (int i = j; i < nloc; i += kMmaWarps) {
         const int ab = i & (NA - 1);
         mbar_wait(full + 8 * s, ph);
-        mbar_wait(a_full + 8 * ab, (uint32_t)(i / NA) & 1u);
+        mbar_wait(a_full + 8 * ab, (uint32_t)(i >> lg_na) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint64_t da = sw128_desc(sA + (uint32_t)ab * BM * 128), db = sw128_desc(sX + (uint32_t)s * XSZ);
 #pragma unroll
         for (int kk = 0; kk < KC / 16; ++kk) {
-          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          const uint32_t acc = (i >= kMmaWarps || kk > 0) ? 1u : 0u;
           asm volatile(
               "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem_d),
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(acc_j),
               "l"(da + 2 * kk), "l"(db + 2 * kk), "r"(a.idesc), "r"(acc));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty + 8 * s)
                      : "memory");
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(a_empty + 8 * ab)
                      : "memory");
-        if (++s == NSB) { s = 0; ph ^= 1u; }
+        s += kMmaWarps;
+        if (s >= NSB) { s -= NSB; ph ^= 1u; }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(acc_full)
                    : "memory");
     }
   } else {
-    // ---- decompress: group grp (8 warps) rebuilds chunks i = grp, grp + 2, ...; thread t = 0..255.
-    // Entry e of a chunk sits in row e / rk at run position e % rk (rk = entries per row); thread t
-    // walks e = t, t + 256, ... keeping (row, position) by a running quotient. Full chunks and the
-    // last (shorter) chunk of the row tile each get their constants once.
-    const int grp = (threadIdx.x - 64) / kDecomp, t = (threadIdx.x - 64) % kDecomp;
-    struct CG {
-      int rk, dq, dr, r0, e0, n_e, ioff;
-    };
-    auto mk = [&](int rk) {
-      CG g;
-      g.rk = rk; g.dq = kDecomp / rk; g.dr = kDecomp % rk; g.r0 = t / rk; g.e0 = t % rk;
-      g.n_e = (int)mt * rk; g.ioff = (int)bsk::align_up((int64_t)g.n_e * ES, 16);
-      return g;
-    };
-    const CG gF = mk(a.CB * k), gL = mk((int)(a.NB - (int64_t)a.CB * (a.NC - 1)) * k);
+    // ---- decompress: group grp (4 warps) rebuilds chunks i = grp, grp + 4, ...; thread t = 0..127.
+    // Work unit = (row r, U = max(B, 8) columns): its U / 8 16-byte pieces of the K-major SWIZZLE_128B
+    // tile and its entries (blocks u·BPU .. u·BPU + BPU - 1, contiguous in the blob). The owner zero-fills
+    // its pieces and then scatters its entries, so program order alone orders the two (no barrier).
+    // Entries are read 8 at a time (16-byte value load, 8-byte index load) when k % 8 == 0.
+    const int grp = (threadIdx.x - kFirstDecomp) / kDecomp, t = (threadIdx.x - kFirstDecomp) % kDecomp;
+    const int U = a.B >= 8 ? a.B : 8, BPU = U / a.B, PPU = U / 8;
+    const int lg_upr = 31 - __clz(KC / U);  // units per row: 1, 2, 4 or 8 (U divides 64)
+    const int nunits = BM << lg_upr;
+    const bool vec8 = (k & 7) == 0;
     const int ilast = a.NC - 1 - c0;  // local index of the row tile's last chunk (may be >= nloc)
-    uint8_t* const ring = smem + (sR - sA);
-    int s = grp;  // ring stage of chunk i (NSB is even, so group grp keeps stages of its parity)
+    const int cbF = a.CB, cbL = (int)(a.NB - (int64_t)a.CB * (a.NC - 1));
+    int s = grp;  // ring stage of chunk i
     uint32_t ph = 0;
     for (int i = grp; i < nloc; i += kGroups) {
       const int ab = i & (NA - 1);
-      const uint32_t aph = (uint32_t)(i / NA) & 1u;
+      const uint32_t aph = (uint32_t)(i >> lg_na) & 1u;
       const uint32_t aT = sA + (uint32_t)ab * BM * 128;
-      uint8_t* const aTp = smem + ab * BM * 128;
+      const int cb = i == ilast ? cbL : cbF;
+      const int n_e = (int)mt * cb * k;
       if (i >= NA) mbar_wait(a_empty + 8 * ab, aph ^ 1u);  // MMA done with this A tile
-#pragma unroll
-      for (int q = 0; q < 4; ++q) bsk::sts_v4(aT + q * 4096 + t * 16, 0u, 0u, 0u, 0u);
-      const CG& G = i == ilast ? gL : gF;
-      const int rk = G.rk, dq = G.dq, dr = G.dr, n_e = G.n_e;
-      int r = G.r0, rem = G.e0;
       mbar_wait(full + 8 * s, ph);
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kDecomp) : "memory");  // zero fill before any scatter
-      const uint8_t* blob = ring + s * a.blob_max;
-      const uint16_t* bv = (const uint16_t*)blob;
-      const uint8_t* bi = blob + G.ioff;
-      for (int e0 = t; e0 < n_e; e0 += 4 * kDecomp) {
-        uint16_t w[4];
-        uint8_t o[4];
+      // 32-bit shared addresses (a generic pointer here would compile to LD.E with 64-bit math)
+      const uint32_t bv = sR + (uint32_t)s * (uint32_t)a.blob_max;
+      const uint32_t bi = bv + (((uint32_t)n_e * ES + 15u) & ~15u);
+      for (int unit = t; unit < nunits; unit += kDecomp) {
+        const int r = unit >> lg_upr, u = unit & ((1 << lg_upr) - 1);
+        const uint32_t rowb = aT + (uint32_t)r * 128;
+        for (int p = 0; p < PPU; ++p)
+          bsk::sts_v4(rowb + ((((uint32_t)(u * PPU + p)) ^ (uint32_t)(r & 7)) << 4), 0u, 0u, 0u, 0u);
+        if (r >= mt) continue;
+        const int j0 = u * BPU, j1 = (j0 + BPU) < cb ? (j0 + BPU) : cb;
+        for (int j = j0; j < j1; ++j) {
+          const int e0 = (r * cb + j) * k;
+          const uint32_t cbase = (uint32_t)(j * a.B);
+          auto put = [&](uint32_t w, uint32_t o) {
+            const uint32_t col = cbase + o;
+            bsk::sts_u16(rowb + ((((col >> 3) ^ (uint32_t)r) & 7) << 4) + (col & 7) * 2, (uint16_t)w);
+          };
+          if (vec8) {
+            for (int e = e0; e < e0 + k; e += 8) {
+              uint32_t ww[4], ii[2];
+              bsk::lds_v4(bv + 2u * (uint32_t)e, ww[0], ww[1], ww[2], ww[3]);
+              asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(ii[0]), "=r"(ii[1]) : "r"(bi + (uint32_t)e));
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {  // loads first: four entries in flight
-          const int e = e0 + u * kDecomp;
-          w[u] = e < n_e ? bv[e] : (uint16_t)0;
-          o[u] = e < n_e ? bi[e] : (uint8_t)0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (e0 + u * kDecomp < n_e) {
-            const uint32_t col = (uint32_t)ctab[rem] + o[u];
-            *(uint16_t*)(aTp + sw128_off((uint32_t)r, col)) = w[u];
+              for (int q = 0; q < 8; ++q) put((ww[q >> 1] >> (16 * (q & 1))) & 0xFFFFu, (ii[q >> 2] >> (8 * (q & 3))) & 0xFFu);
+            }
+          } else {
+            for (int e = e0; e < e0 + k; ++e) {
+              uint16_t o8;
+              asm volatile("ld.shared.u8 %0, [%1];" : "=h"(o8) : "r"(bi + (uint32_t)e));
+              put(bsk::lds_u16(bv + 2u * (uint32_t)e), o8);
+            }
           }
-          rem += dr;
-          r += dq;
-          if (rem >= rk) { rem -= rk; ++r; }
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core
@@ -219,21 +230,32 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
     // column part (w - 2) / 4 of NP parts.
     mbar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const int q = warp & 3, part = (warp - 2) >> 2;
+    const int q = warp & 3, part = (warp - kFirstDecomp / 32) >> 2;
     const int NP = a.BN % 32 == 0 ? 4 : 2;  // parts of BN / NP columns, a multiple of 8
     const int m = 32 * q + lane;
-    float* red = (float*)smem;  // split-K partial tile [BN][128] (the rings are idle now)
+    // split-K partial tile [BN][128] fp32 at sA (the rings are idle now)
     if (part < NP) {
       const int pw = a.BN / NP;
       for (int nb = part * pw; nb < (part + 1) * pw; nb += 8) {
+        // accumulator j holds chunks i = j mod kMmaWarps; summed ((acc0 + acc1) + acc2) + ..., a fixed order
         uint32_t rr[8];
+        const uint32_t ta = tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)nb;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]), "=r"(rr[7])
-                     : "r"(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)nb));
+                     : "r"(ta));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int jacc = 1; jacc < kMmaWarps && jacc < nloc; ++jacc) {
+          uint32_t r1[8];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(r1[0]), "=r"(r1[1]), "=r"(r1[2]), "=r"(r1[3]), "=r"(r1[4]), "=r"(r1[5]), "=r"(r1[6]), "=r"(r1[7])
+                       : "r"(ta + (uint32_t)(jacc * a.acc_cols)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int e = 0; e < 8; ++e) rr[e] = __float_as_uint(__uint_as_float(rr[e]) + __uint_as_float(r1[e]));
+        }
         if (S > 1) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) red[(nb + e) * BM + m] = __uint_as_float(rr[e]);
+          for (int e = 0; e < 8; ++e) bsk::sts_u32(sA + (uint32_t)(((nb + e) * BM + m) * 4), rr[e]);
         } else if (m < mt) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
@@ -246,8 +268,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
   }
   if (S > 1) {
     cluster_sync_all();  // every partial tile is parked
-    if (warp >= 2) {
-      const int t = threadIdx.x - 64;
+    if (warp >= kFirstDecomp / 32) {
+      const int t = threadIdx.x - kFirstDecomp;
       const int U = a.BN * BM / 4;  // float4 units of the tile
       const int u0 = (int)((int64_t)rank * U / S), u1 = (int)((int64_t)(rank + 1) * U / S);
       for (int u = u0 + t; u < u1; u += kGroups * kDecomp) {
@@ -272,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(a.tmem_cols));
   }
@@ -341,12 +363,11 @@ cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int
     if (e != cudaSuccess) return e;
     static_smem = (int)fa.sharedSizeBytes;
   }
-  // NA dense A tiles + NSB stages of (X tile, blob): BN as large as 4 stages allow (<= 256), then as
-  // many stages as fit (deep rings keep enough bytes in flight when blobs are small)
+  // NA dense A tiles + NSB stages of (X tile, blob): BN as large as 4 stages allow with NA = 4 (<= 256);
+  // NA = 8 when 8 stages still fit (more chunks in flight hide the MMA completion latency), else 4.
   const int64_t avail = bsk::dev_props().smem_optin - static_smem - 1024;  // 1024: alignment slack
-  const int64_t ring = avail - (int64_t)NA * BM * 128;
-  int64_t bn_max = ((ring / 4 - a.blob_max) / 128) / 16 * 16;
-  if (bn_max > 256) bn_max = 256;
+  int64_t bn_max = (((avail - 4LL * BM * 128) / 4 - a.blob_max) / 128) / 16 * 16;
+  if (bn_max > 512 / kMmaWarps) bn_max = 512 / kMmaWarps;  // kMmaWarps accumulators in 512 TMEM columns
   if (bn_max < 16) return cudaErrorNotSupported;
   int64_t BN = (N + 15) / 16 * 16;
   if (BN > bn_max) BN = bn_max;
@@ -354,13 +375,20 @@ cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int
   a.idesc = idesc_f16(DT == BS_BF16, BM, (int)BN, false);
   int cols = 32;
   while (cols < BN) cols <<= 1;
-  a.tmem_cols = cols;
+  a.acc_cols = cols;
+  a.tmem_cols = cols * kMmaWarps;  // <= 512 (BN <= 256)
+  a.NA = (avail - 8LL * BM * 128) / (BN * 128 + a.blob_max) >= 8 ? 8 : 4;
+  const int64_t ring = avail - (int64_t)a.NA * BM * 128;
   int64_t nsb = ring / (BN * 128 + a.blob_max);
   if (nsb > kMaxStages) nsb = kMaxStages;
-  nsb &= ~1LL;  // even: each decompress group keeps to one stage parity
+  // A multiple of 4 (= producers = decompress groups, a multiple of the MMA warps): then every stage
+  // belongs to one producer, one group and one MMA warp, which use it strictly in turn, so no waiter
+  // is ever two phases ahead of a barrier (mbarrier parity waits alias beyond one phase; odd depths
+  // faulted on stale blob indices).
+  nsb &= ~3LL;
   if (nsb < 4) return cudaErrorNotSupported;
   a.NSB = (int)nsb;
-  const int64_t smem = 1024 + (int64_t)NA * BM * 128 + nsb * (BN * 128 + a.blob_max);
+  const int64_t smem = 1024 + (int64_t)a.NA * BM * 128 + nsb * (BN * 128 + a.blob_max);
   if (a.S > 1 && BN * BM * 4 > smem - 1024) return cudaErrorNotSupported;  // partial tile must fit
   CUtensorMap tX;
   if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, KC, (int)BN)) return cudaErrorNotSupported;

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
     }
     mbar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    float* red = (float*)smem;  // split-K partial tile [BN][128] (the rings are idle now)
+    // split-K partial tile [BN][128] fp32 at sA (the rings are idle now)
     for (int nb = 0; nb < a.BN; nb += 8) {
       uint32_t r[8];
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (S > 1) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) red[(nb + e) * BM + row] = __uint_as_float(r[e]);
+        for (int e = 0; e < 8; ++e) bsk::sts_u32(sA + (uint32_t)(((nb + e) * BM + row) * 4), r[e]);
       } else if (row < mt) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
