@@ -240,6 +240,52 @@ __global__ void sp24_cc_kernel(const uint8_t* __restrict__ vals, const uint8_t* 
   }
 }
 
+// Batch-1 2:4 SpMV, 16-bit values (HBM-bound): a warp per row; lane l takes groups of 4 blocks
+// (16 columns) g = l, l + 32, ...: one 16-byte load of the group's 8 kept values, one 2-byte load of its
+// 4 metadata nibbles, two 16-byte loads of x (L1/L2-resident), then 8 FHFMAs on the selected halves.
+// Two groups are loaded before either is used. Requires K % 16 == 0 and a 16-byte aligned x.
+template <int DT>
+__global__ void __launch_bounds__(256) sp24_spmv16_kernel(const uint16_t* __restrict__ vals,
+                                                          const uint8_t* __restrict__ meta,
+                                                          const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
+                                                          int64_t M, int64_t K) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t NG = K / 16;  // groups of 4 blocks per row
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < M; r += nwarps) {
+    const uint4* vr = (const uint4*)(vals + r * (K / 2));
+    const uint16_t* mr = (const uint16_t*)(meta + r * (K / 8));
+    const uint4* xv = (const uint4*)x;
+    float acc0 = 0.f, acc1 = 0.f;
+    auto group = [&](float& acc, uint4 w, uint32_t nib, uint4 xa, uint4 xb) {
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+      const uint32_t xx[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // block q: x halves in words 2q, 2q + 1
+        const uint32_t n4 = (nib >> (4 * q)) & 0xFu;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t o = h == 0 ? (n4 & 3u) : (n4 >> 2);
+          const uint32_t xw = (o & 2u) ? xx[2 * q + 1] : xx[2 * q];
+          bsk::fma_acc<DT>(acc, (ww[q] >> (16 * h)) & 0xFFFFu, (xw >> (16 * (o & 1u))) & 0xFFFFu);
+        }
+      }
+    };
+    int64_t g = lane;
+    for (; g + 32 < NG; g += 64) {
+      const uint4 w0 = __ldcs(vr + g), w1 = __ldcs(vr + g + 32);
+      const uint32_t n0 = __ldcs(mr + g), n1 = __ldcs(mr + g + 32);
+      const uint4 x0a = __ldg(xv + 2 * g), x0b = __ldg(xv + 2 * g + 1);
+      const uint4 x1a = __ldg(xv + 2 * (g + 32)), x1b = __ldg(xv + 2 * (g + 32) + 1);
+      group(acc0, w0, n0, x0a, x0b);
+      group(acc1, w1, n1, x1a, x1b);
+    }
+    if (g < NG) group(acc0, __ldcs(vr + g), __ldcs(mr + g), __ldg(xv + 2 * g), __ldg(xv + 2 * g + 1));
+    const float tot = bsk::warp_sum_f(acc0 + acc1);
+    if (lane == 0) y[r] = (uint16_t)bsk::from_float<DT>(tot);
+  }
+}
+
 template <int DT>
 cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
                         int64_t ldy, cudaStream_t s) {
@@ -352,6 +398,15 @@ cudaError_t bsk_launch_sp24(const bsk::Geom& g, const void* packed, const void* 
     cudaError_t e = g.dt == BS_BF16 ? launch_tc24<BS_BF16>(g, packed, X, N, ldx, Y, ldy, s)
                                     : launch_tc24<BS_F16>(g, packed, X, N, ldx, Y, ldy, s);
     if (e != cudaErrorNotSupported) return e;
+  }
+  if (N == 1 && g.es == 2 && g.K % 16 == 0 && ((uintptr_t)X & 15) == 0) {  // batch 1: HBM-bound SpMV
+    const uint8_t* base = (const uint8_t*)packed;
+    int64_t blocks = (g.M + 7) / 8;
+    if (blocks > (int64_t)bsk::dev_props().sms * 8) blocks = (int64_t)bsk::dev_props().sms * 8;
+    auto kern = g.dt == BS_BF16 ? sp24_spmv16_kernel<BS_BF16> : sp24_spmv16_kernel<BS_F16>;
+    kern<<<(unsigned)blocks, 256, 0, s>>>((const uint16_t*)(base + g.offA), base + g.offB, (const uint16_t*)X,
+                                          (uint16_t*)Y, g.M, g.K);
+    return cudaGetLastError();
   }
   switch (g.dt) {
     case BS_F32: return launch_cc24<BS_F32>(g, packed, X, N, ldx, Y, ldy, s);
