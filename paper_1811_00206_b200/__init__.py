@@ -42,7 +42,7 @@ class _Matrix(ctypes.Structure):
 
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1811_00206_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1811_00206_b200/build.py` "
                           "(there is no CPU fallback)")
     L = ctypes.CDLL(LIB_PATH)
     vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int

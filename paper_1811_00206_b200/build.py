@@ -1,6 +1,6 @@
 """Build libbs.so (the C-ABI CUDA library) in-tree with nvcc for sm_100a.
 
-    python -m paper_1811_00206_b200.build [--force]
+    python paper_1811_00206_b200/build.py [--force]
 
 Each kernel translation unit compiles in parallel to an object file under build/, then links into
 paper_1811_00206_b200/libbs.so with a static CUDA runtime. The .so ships to the GPU box with the

@@ -18,8 +18,8 @@ def _declared_symbols():
 
 @pytest.fixture(scope="module")
 def bs():
-    from paper_1811_00206_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__._build_module().build()
     import paper_1811_00206_b200 as bs
     return bs
 

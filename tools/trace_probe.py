@@ -13,7 +13,8 @@ LIB = os.path.join(ROOT, "tools", "bin", "libbs_trace.so")
 
 
 def build():
-    from paper_1811_00206_b200 import build as b
+    import __graft_entry__
+    b = __graft_entry__._build_module()
     objs = []
     os.makedirs(os.path.join(ROOT, "build", "trace"), exist_ok=True)
     for src in b.SOURCES:
