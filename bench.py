@@ -449,7 +449,12 @@ def layer_rows(a, bs, hbm_peak, l2):
             A = bs.pack(v, i, K, a.block)
             mats = rotating(bs, A, l2)
             C = len(mats)
-            t_ours = graph_time_us(lambda j: bs.spmv(mats[j % C], x, out=y), 20 * C if C < 10 else 2 * C)
+            n_in = 20 * C if C < 10 else 2 * C
+            # three launch modes of the same kernel (include/bs.h): plain, PDL (bs_spmv's default) and
+            # PDL with static weights (W streams before the previous layer has finished: inference)
+            t_modes = {m: graph_time_us(lambda j, f=f: bs.spmv(mats[j % C], x, out=y, flags=f), n_in)
+                       for m, f in (("plain", 0), ("pdl", bs.SPMV_PDL), ("pdl_w_static", bs.SPMV_PDL | bs.SPMV_W_STATIC))}
+            t_ours = t_modes["pdl_w_static"]
             if t_dense is None:
                 Wbs = dense_from_canonical(v, i, M, K, a.block)
                 dens = [Wbs] + [Wbs.clone() for _ in range(max(1, -(-3 * l2 // Wbs.numel() // Wbs.element_size())) - 1)]
@@ -458,14 +463,18 @@ def layer_rows(a, bs, hbm_peak, l2):
                               graph_time_us(lambda j: torch.matmul(dens[j % Cd], x.view(-1, 1)), 4 * Cd))
                 del dens, Wbs
             pk = A.nbytes + K * W.element_size() + M * W.element_size()
-            rows.append({"layer": name, "sparsity": s, "k": ks, "us": round(t_ours, 2), "cublas_dense_us": round(t_dense, 2),
+            rows.append({"layer": name, "sparsity": s, "k": ks, "us": round(t_ours, 2),
+                         "us_plain": round(t_modes["plain"], 2), "us_pdl": round(t_modes["pdl"], 2),
+                         "cublas_dense_us": round(t_dense, 2),
                          "speedup_vs_cublas": round(t_dense / t_ours, 2), "packed_GBps": round(pk / t_ours / 1e3, 1),
                          "packed_frac": round(pk / t_ours / 1e3 / hbm_peak, 4),
                          "paper_ideal_us": round(oracle.ideal_time(t_dense, o_time, 1 - ks / a.block), 2)})
             del mats, A, v, i
         del W
     return {"layers": rows, "o_time_us": round(o_time, 2),
-            "layers_note": "latency regime; ideal line i_time = (d_time - o_time)(1 - s) + o_time with d_time = cuBLAS and "
+            "layers_note": "latency regime; us = bs_spmv_ex(PDL | W_STATIC) back to back (static weights: each layer's W "
+                           "streams while the previous kernel finishes; x and y wait for it), us_pdl = bs_spmv (PDL, every "
+                           "global access waits), us_plain = flags 0; ideal line i_time = (d_time - o_time)(1 - s) + o_time with d_time = cuBLAS and "
                            "o_time = measured empty-kernel graph node (P:264-266, SURVEY A18)"}
 
 

@@ -114,6 +114,23 @@ int bs_unpack(const void* packed, int64_t M, int64_t K, int block, int k, int dt
  * layout. */
 int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream);
 
+/* Launch flags of bs_spmv_ex.
+ * BS_SPMV_PDL: launch as a programmatic dependent of the kernel before it on `stream` (PDL). The
+ *   kernel's prologue (shared-memory set-up) overlaps the previous kernel's tail; every global read
+ *   and write still waits for the previous kernel to complete (griddepcontrol.wait), so the call is
+ *   stream-ordered exactly like a plain launch. bs_spmv uses this flag.
+ * BS_SPMV_W_STATIC (with BS_SPMV_PDL): the caller promises that no kernel still running on `stream`
+ *   writes A->packed (weights are static, the inference case). The packed W then starts streaming
+ *   into shared memory before the wait; x and y still wait. The paper's batch-1 time is dominated by
+ *   fixed per-layer costs ("communication inside GPU"; o_time), which this hides. */
+#define BS_SPMV_PDL 1u
+#define BS_SPMV_W_STATIC 2u
+
+/* bs_spmv_ex: bs_spmv with launch flags (above). flags = BS_SPMV_PDL is bs_spmv; flags = 0 is a
+ * plain launch. Errors: as bs_spmv; BS_ERR_ARG for unknown flag bits. Results are bit-identical for
+ * every flag combination. */
+int bs_spmv_ex(const bs_matrix* A, const void* x, void* y, unsigned flags, void* stream);
+
 /* bs_spmv_host: the same product with HOST x and y. The call enqueues H2D(x) -> bs_spmv -> D2H(y) on
  * `stream`, using caller-owned device scratch x_dev (K elements) and y_dev (M elements). x_host and
  * y_host should be pinned for the copies to be asynchronous. The call does not synchronise: y_host

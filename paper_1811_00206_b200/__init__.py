@@ -26,7 +26,8 @@ DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 LAYOUTS = {"spmv": 1, "spmm": 2, "sp24": 3}
 
 EXPORTS = ("bs_k_from_sparsity", "bs_packed_bytes", "bs_status_str", "bs_version", "bs_prune", "bs_prune_k",
-           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_host", "bs_spmm")
+           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_host", "bs_spmm")
+SPMV_PDL, SPMV_W_STATIC = 1, 2  # bs_spmv_ex flags (include/bs.h)
 
 
 class BSError(RuntimeError):
@@ -59,9 +60,10 @@ def _load() -> ctypes.CDLL:
     L.bs_pack.argtypes = [vp, vp, i64, i64, ci, ci, ci, ci, vp, vp]
     L.bs_unpack.argtypes = [vp, i64, i64, ci, ci, ci, ci, vp, vp, vp]
     L.bs_spmv.argtypes = [ctypes.POINTER(_Matrix), vp, vp, vp]
+    L.bs_spmv_ex.argtypes = [ctypes.POINTER(_Matrix), vp, vp, ctypes.c_uint, vp]
     L.bs_spmv_host.argtypes = [ctypes.POINTER(_Matrix), vp, vp, vp, vp, vp]
     L.bs_spmm.argtypes = [ctypes.POINTER(_Matrix), vp, i64, i64, vp, i64, vp]
-    for f in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_host", "bs_spmm"):
+    for f in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_host", "bs_spmm"):
         getattr(L, f).restype = ci
     return L
 
@@ -193,8 +195,9 @@ def unpack(A: BSMatrix):
     return vals, idx
 
 
-def spmv(A: BSMatrix, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """y = W_bs·x (Eq. 1 with B = 0). x: [K] of A.dtype; returns y: [M]."""
+def spmv(A: BSMatrix, x: torch.Tensor, out: torch.Tensor | None = None, flags: int | None = None) -> torch.Tensor:
+    """y = W_bs·x (Eq. 1 with B = 0). x: [K] of A.dtype; returns y: [M].
+    flags: None -> bs_spmv (PDL launch); otherwise bs_spmv_ex with SPMV_PDL / SPMV_W_STATIC bits."""
     _need_cuda(x)
     if x.dtype != A.dtype or x.numel() != A.K:
         raise ValueError("x must have A.K elements of A.dtype")
@@ -202,7 +205,10 @@ def spmv(A: BSMatrix, x: torch.Tensor, out: torch.Tensor | None = None) -> torch
     y = out if out is not None else torch.empty(A.M, dtype=A.dtype, device=x.device)
     m = A.cstruct()
     with torch.cuda.device(x.device):
-        st = _lib.bs_spmv(ctypes.byref(m), x.data_ptr(), y.data_ptr(), _stream(x.device))
+        if flags is None:
+            st = _lib.bs_spmv(ctypes.byref(m), x.data_ptr(), y.data_ptr(), _stream(x.device))
+        else:
+            st = _lib.bs_spmv_ex(ctypes.byref(m), x.data_ptr(), y.data_ptr(), flags, _stream(x.device))
     _check(st, "bs_spmv")
     return y
 

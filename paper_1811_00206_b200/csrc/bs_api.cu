@@ -136,15 +136,20 @@ int bs_unpack(const void* packed, int64_t M, int64_t K, int block, int k, int dt
   return from_cuda(bsk_launch_unpack(packed, g, vals, idx, (cudaStream_t)stream));
 }
 
-int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream) {
+int bs_spmv_ex(const bs_matrix* A, const void* x, void* y, unsigned flags, void* stream) {
   bsk::Geom g;
   int st = matrix_geom(A, &g);
   if (st) return st;
   if (!x || !y) return BS_ERR_ARG;
+  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC)) return BS_ERR_ARG;
   if (g.layout == BS_LAYOUT_SP24)  // 2:4: CUDA-core path with 2-bit metadata
     return from_cuda(bsk_launch_sp24(g, A->packed, x, 1, g.K, y, g.M, (cudaStream_t)stream));
   if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;  // SPMM tiles feed bs_spmm
-  return from_cuda(bsk_launch_spmv(g, A->packed, x, y, (cudaStream_t)stream));
+  return from_cuda(bsk_launch_spmv(g, A->packed, x, y, flags, (cudaStream_t)stream));
+}
+
+int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream) {
+  return bs_spmv_ex(A, x, y, BS_SPMV_PDL, stream);
 }
 
 int bs_spmv_host(const bs_matrix* A, const void* x_host, void* y_host, void* x_dev, void* y_dev, void* stream) {
@@ -177,7 +182,7 @@ int bs_spmm(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, void* Y, 
   const size_t es = (size_t)g.es;
   for (int64_t n = 0; n < N; ++n) {
     e = bsk_launch_spmv(g, A->packed, (const char*)X + (size_t)(n * ldx) * es, (char*)Y + (size_t)(n * ldy) * es,
-                        (cudaStream_t)stream);
+                        BS_SPMV_PDL, (cudaStream_t)stream);
     if (e != cudaSuccess) return from_cuda(e);
   }
   return BS_OK;

@@ -17,8 +17,10 @@ cudaError_t bsk_spmv_dispatch_f32(const bsk::Geom& g, const SpmvArgs& a, cudaStr
 // every width use chunk_nv = 8, so a column's fp32 summation order does not depend on the pass width
 // (NV = 2, 4, 8 accumulate each column in the same order), i.e. on N.
 static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const void* x, int64_t ldx, void* y,
-                                  int64_t ldy, int ncols, int nv, int chunk_nv, cudaStream_t s) {
+                                  int64_t ldy, int ncols, int nv, int chunk_nv, unsigned flags, cudaStream_t s) {
   SpmvArgs a;
+  a.pdl = (flags & BS_SPMV_PDL) != 0;
+  a.w_early = a.pdl && (flags & BS_SPMV_W_STATIC) != 0;
   const uint8_t* base = (const uint8_t*)packed;
   a.A = base + g.offA;
   a.Bt = base + g.offB;
@@ -76,8 +78,9 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
   }
 }
 
-cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, cudaStream_t s) {
-  return launch_spmv_nv(g, packed, x, 0, y, 0, 1, 1, 1, s);
+cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, unsigned flags,
+                            cudaStream_t s) {
+  return launch_spmv_nv(g, packed, x, 0, y, 0, 1, 1, 1, flags, s);
 }
 
 // Batched product on the SPMV layout (16-bit): passes of up to 8 batch columns, each one stream of W;
@@ -89,7 +92,7 @@ cudaError_t bsk_launch_spmv_batch(const bsk::Geom& g, const void* packed, const 
     const int nc = (int)((N - n0) < 8 ? (N - n0) : 8);
     const int nv = nc <= 2 ? 2 : nc <= 4 ? 4 : 8;
     cudaError_t e =
-        launch_spmv_nv(g, packed, (const uint16_t*)X + n0 * ldx, ldx, (uint16_t*)Y + n0 * ldy, ldy, nc, nv, 8, s);
+        launch_spmv_nv(g, packed, (const uint16_t*)X + n0 * ldx, ldx, (uint16_t*)Y + n0 * ldy, ldy, nc, nv, 8, BS_SPMV_PDL, s);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

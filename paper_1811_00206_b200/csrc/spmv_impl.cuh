@@ -77,7 +77,15 @@ struct SpmvArgs {
   int xvec;          // x is 16-byte aligned and B allows 16-byte staging loads
   int64_t ldx, ldy;  // batch-column strides of X and Y (NV > 1)
   int ncols;         // valid batch columns in this pass (NV > 1)
+  int w_early;       // PDL: W may be streamed before griddepcontrol.wait (BS_SPMV_W_STATIC)
+  int pdl;           // host: launch with programmatic stream serialization (BS_SPMV_PDL)
 };
+
+// Programmatic dependent launch (PDL). launch_dependents lets the next kernel on the stream be
+// scheduled while this one runs; wait blocks until the previous kernel has completed and its writes
+// are visible. Both are no-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(bar), "r"(count));
@@ -125,24 +133,24 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 // 2m and 2m+1 share a word. Work items are (group, 16-byte piece of a block); each lane issues up to
 // 8 piece loads before storing them. `after_loads()` runs once, right after the first batch of
 // loads is in flight, so that the caller can queue the W bulk copies behind them.
-template <int ES, typename F>
+template <int ES, int BT, typename F>
 __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint32_t sx, int64_t g0, int64_t g1, F after_loads) {
   constexpr int PE = 16 / ES;        // elements per 16-byte piece
   constexpr uint32_t ROWB = 32 * ES;  // bytes per slot row (one offset o of 32 blocks)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int B = a.B;
+  const int B = BT > 0 ? BT : a.B;
   bool hooked = false;
   if (a.xvec) {  // 16-byte aligned x and B % PE == 0
-    const int ppb = B / PE;  // pieces per block
-    const int64_t items = (g1 - g0) * ppb;
-    for (int64_t j0 = warp; j0 < items || !hooked; j0 += 8LL * nw) {
+    const uint32_t ppb = (uint32_t)(B / PE);  // pieces per block (x slots fit in shared memory: 32-bit)
+    const uint32_t items = (uint32_t)(g1 - g0) * ppb;
+    for (uint32_t j0 = warp; j0 < items || !hooked; j0 += 8u * nw) {
       uint4 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int64_t j = j0 + (int64_t)u * nw;
+        const uint32_t j = j0 + (uint32_t)u * nw;
         if (j < items) {
-          const int64_t gl = j / ppb;
-          const int q = (int)(j - gl * ppb);
+          const uint32_t gl = j / ppb;
+          const uint32_t q = j - gl * ppb;
           const int64_t b = (g0 + gl) * 32 + lane;
           if (b < a.NB) v[u] = __ldg((const uint4*)((const uint8_t*)a.x + (b * B + q * PE) * ES));
         }
@@ -153,13 +161,13 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint32_t sx, int64_t 
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int64_t j = j0 + (int64_t)u * nw;
+        const uint32_t j = j0 + (uint32_t)u * nw;
         if (j < items) {
-          const int64_t gl = j / ppb;
-          const int q = (int)(j - gl * ppb);
+          const uint32_t gl = j / ppb;
+          const uint32_t q = j - gl * ppb;
           const int64_t b = (g0 + gl) * 32 + lane;
           if (b < a.NB) {
-            const uint32_t col = sx + (uint32_t)(gl * B + q * PE) * ROWB + lane * ES;
+            const uint32_t col = sx + (gl * B + q * PE) * ROWB + lane * ES;
             const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
             for (int e = 0; e < PE; ++e) {
@@ -188,19 +196,19 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint32_t sx, int64_t 
 // gathers the column's batch vector. Slot (gl·B + o)·32 + l of NV halves; rows n >= ncols are zero.
 // Lane l copies block 32·g + l: per 8-column piece it loads NV 16-byte row pieces, transposes them in
 // registers and writes 8 slots.
-template <int NV, typename F>
+template <int NV, int BT, typename F>
 __device__ __forceinline__ void stage_xn(const SpmvArgs& a, uint32_t sx, int64_t g0, int64_t g1, F after_loads) {
   constexpr uint32_t SLB = 2 * NV, ROWB = 32 * SLB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int B = a.B;
+  const int B = BT > 0 ? BT : a.B;
   bool hooked = false;
   if (a.xvec) {  // rows 16-byte aligned, B % 8 == 0
-    const int ppb = B / 8;
-    const int64_t items = (g1 - g0) * ppb;
-    for (int64_t j = warp; j < items || !hooked; j += nw) {
+    const uint32_t ppb = (uint32_t)(B / 8);
+    const uint32_t items = (uint32_t)(g1 - g0) * ppb;
+    for (uint32_t j = warp; j < items || !hooked; j += nw) {
       uint4 v[NV];
-      const int64_t gl = j < items ? j / ppb : 0;
-      const int q = j < items ? (int)(j - gl * ppb) : 0;
+      const uint32_t gl = j < items ? j / ppb : 0;
+      const uint32_t q = j < items ? j - gl * ppb : 0;
       const int64_t b = (g0 + gl) * 32 + lane;
       const bool ok = j < items && b < a.NB;
 #pragma unroll
@@ -213,7 +221,7 @@ __device__ __forceinline__ void stage_xn(const SpmvArgs& a, uint32_t sx, int64_t
         hooked = true;
       }
       if (ok) {
-        const uint32_t col = sx + (uint32_t)(gl * B + q * 8) * ROWB + lane * SLB;
+        const uint32_t col = sx + (gl * B + q * 8) * ROWB + lane * SLB;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           uint32_t h[NV];
@@ -401,6 +409,11 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
       armed = true;
     }
   };
+  pdl_launch_dependents();
+  // Everything above touched only shared memory. With w_early (static weights) the W ring fills while
+  // the previous kernel finishes; x (its output) and y (which it may still read) wait for it.
+  if (a.w_early) arm_once();
+  pdl_wait();
 
   float acc[NA];
 #pragma unroll
@@ -441,14 +454,23 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
 
   BS_MARK(1);
   // ---- consumer
-  int64_t consumed = 0;
+  // ring position of the next stage to consume: slot cst, mbarrier phase cph (no divisions)
+  uint32_t cst = 0, cph = 0;
+  bool first_stage = true;
+  auto advance = [&]() {
+    if (++cst == (uint32_t)NS) {
+      cst = 0;
+      cph ^= 1u;
+    }
+  };
   for (int c = 0; c < a.nchunks; ++c) {
     const int64_t g0 = (int64_t)c * a.PC * V;
     const bool last = c == a.nchunks - 1;
-    const int64_t g1 = last && a.tail_in_last ? (a.NB + 31) / 32 : g0 + (seg_len(c) / (a.k > 0 ? a.k : 1)) * V;
+    const int64_t npc = (a.NBf - (int64_t)c * a.PC) < a.PC ? (a.NBf - (int64_t)c * a.PC) : a.PC;
+    const int64_t g1 = last && a.tail_in_last ? (a.NB + 31) / 32 : g0 + npc * V;
     if (c > 0) __syncthreads();  // all warps are done with the previous chunk's x
-    if constexpr (NV == 1) stage_x<ES>(a, sx, g0, g1, arm_once);
-    else stage_xn<NV>(a, sx, g0, g1, arm_once);
+    if constexpr (NV == 1) stage_x<ES, BT>(a, sx, g0, g1, arm_once);
+    else stage_xn<NV, BT>(a, sx, g0, g1, arm_once);
     if (c == 0) BS_MARK(6);
     __syncthreads();
     if (c == 0) BS_MARK(2);
@@ -460,9 +482,10 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
       uint32_t pb = sx + lane * SLB;  // slot base of the current panel within the chunk
       int t = 0;
       for (int64_t s0 = 0; s0 < L; s0 += Q) {
-        const uint32_t st = (uint32_t)(consumed % NS);
-        mbar_wait(bar0 + st * 8, (uint32_t)((consumed / NS) & 1));
-        if (consumed == 0) BS_MARK(3);
+        const uint32_t st = cst;
+        mbar_wait(bar0 + st * 8, cph);
+        if (first_stage) BS_MARK(3);
+        first_stage = false;
         const uint32_t sbase = ring + st * SB;
         const int nq = (L - s0) < Q ? (int)(L - s0) : Q;
         auto step = [&](int q) {
@@ -498,7 +521,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
             if (q < nq) step(q);
         }
         __syncwarp();  // every lane is done with stage st
-        ++consumed;
+        advance();
         if (lane == 0 && more()) issue(st);
       }
       const int64_t r = wr0 + i;
@@ -520,8 +543,8 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
       tbase = sx + (uint32_t)(gt0 - (int64_t)(a.nchunks - 1) * a.PC * V) * GSW;
     } else {
       __syncthreads();
-      if constexpr (NV == 1) stage_x<ES>(a, sx, gt0, gt1, arm_once);
-      else stage_xn<NV>(a, sx, gt0, gt1, arm_once);
+      if constexpr (NV == 1) stage_x<ES, BT>(a, sx, gt0, gt1, arm_once);
+      else stage_xn<NV, BT>(a, sx, gt0, gt1, arm_once);
       __syncthreads();
       tbase = sx;
     }
@@ -549,8 +572,8 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
     if (ring_tail) {  // tails arrive through the ring, R rows per stage
       for (int64_t t0 = 0; t0 < nrows; t0 += a.tail_rows) {
         const int64_t R = (nrows - t0) < a.tail_rows ? (nrows - t0) : a.tail_rows;
-        const uint32_t st = (uint32_t)(consumed % NS);
-        mbar_wait(bar0 + st * 8, (uint32_t)((consumed / NS) & 1));
+        const uint32_t st = cst;
+        mbar_wait(bar0 + st * 8, cph);
         uint32_t dv, bv, di, bi;
         tail_geom(t0, R, dv, bv, di, bi);
         for (int64_t rr = 0; rr < R; ++rr) {
@@ -561,7 +584,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
           finish_row(wr0 + t0 + rr);
         }
         __syncwarp();
-        ++consumed;
+        advance();
         if (lane == 0 && more()) issue(st);
       }
     } else {  // direct loads (a row's tail does not fit a ring stage)
@@ -619,8 +642,18 @@ cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   if (NS < 1) return cudaErrorInvalidConfiguration;
   a.NS = NS;
   const int64_t smem_all = a.xbytes + (int64_t)(NT / 32) * NS * SB + scratch;
-  kern<<<(unsigned)grid, NT, (size_t)smem_all, s>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = (size_t)smem_all;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  if (!a.pdl) a.w_early = 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <int DT, int V, int IS, int BT, bool MULTI, int NV>

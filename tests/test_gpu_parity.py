@@ -142,6 +142,45 @@ def test_row_sharding_bit_identical(bs):
         assert torch.equal(torch.cat(parts), y1)
 
 
+def test_spmv_launch_modes_and_dependencies(bs):
+    """bs_spmv_ex flags (plain / PDL / PDL + static weights) give bit-identical y, and the PDL waits hold:
+    a chain of layers where each x is the previous kernel's y, with ping-pong y buffers (a WAR hazard if
+    y were written before the wait), and a pack immediately followed by a PDL SpMV that reads its output."""
+    K, B, k = 4096, 32, 3
+    dev = torch.device("cuda")
+    mats = []
+    for j in range(6):
+        W = synth.matrix(K, K, "f16", seed=synth.seed_for(9, j), device=dev)
+        v, i, _ = bs.prune(W, B, k=k)
+        mats.append(bs.pack(v, i, K, B))
+    x0 = synth.vector(K, "f16", seed=synth.seed_for(9, 99), device=dev)
+    modes = (0, bs.SPMV_PDL, bs.SPMV_PDL | bs.SPMV_W_STATIC)
+    outs = []
+    for f in modes:
+        ping, pong = torch.empty(K, dtype=torch.float16, device=dev), torch.empty(K, dtype=torch.float16, device=dev)
+        cur = x0.clone()
+        for rep in range(3):
+            for j, A in enumerate(mats):
+                dst = ping if (rep * len(mats) + j) % 2 == 0 else pong
+                bs.spmv(A, cur, out=dst, flags=f)
+                cur = dst
+                cur.mul_(1.0 / 16)  # a torch kernel between layers (writes x of the next SpMV)
+        torch.cuda.synchronize()
+        outs.append(cur.clone())
+    assert torch.isfinite(outs[0].float()).all()
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    # pack -> PDL SpMV (the SpMV's W reads must wait for the pack kernel)
+    W = synth.matrix(700, K, "f16", seed=synth.seed_for(9, 50), device=dev)
+    v, i, _ = bs.prune(W, B, k=k)
+    ref = bs.spmv(bs.pack(v, i, K, B), x0, flags=0)
+    for _ in range(3):
+        A = bs.pack(v, i, K, B)
+        assert torch.equal(bs.spmv(A, x0), ref)
+    with pytest.raises(bs.BSError):
+        bs.spmv(mats[0], x0, flags=4)
+
+
 @pytest.mark.parametrize("N", [1, 2, 3, 8, 13, 32, 64])
 @pytest.mark.parametrize("dname", ["f16", "bf16", "f32"])
 def test_spmm_small(bs, N, dname):

@@ -9,7 +9,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 PKG = os.path.join(ROOT, "paper_1811_00206_b200")
-LIB = os.path.join(ROOT, "tools", "bin", "libbs_trace.so")
+LIB = os.path.join(ROOT, "probe_bin", "libbs_trace.so")
 
 
 def build():
