@@ -176,6 +176,7 @@ static int64_t blob_bytes(int64_t mt, int64_t cb, int k, int es, int is) {
 typedef struct {
   int64_t V, P, NBf, T;
   int es, is;                 /* value bytes, index bytes */
+  int64_t ri;                 /* SPMV: bytes of a step's index run (160 for 5-bit runs, else P*is) */
   int64_t offA, offB, offC, total;  /* SP24: offA = values, offB = metadata */
 } orc_geom;
 
@@ -208,8 +209,10 @@ static int geom(int64_t M, int64_t K, int B, int k, int dt, int layout, orc_geom
     g->P = 32 * V;
     g->NBf = NB / g->P;
     g->T = NB - g->NBf * g->P;
+    /* docs/layout.md: 5-bit index runs when B = 32 and V = 8 (two planes: 32 u32 words + 32 bytes) */
+    g->ri = (B == 32 && V == 8) ? 160 : g->P * g->is;
     g->offA = 0;
-    g->offB = align256(M * g->NBf * k * g->P * (g->es + g->is));
+    g->offB = align256(M * g->NBf * k * (g->P * g->es + g->ri));
     g->offC = g->offB + align256(M * k * g->T * g->es);
     g->total = g->offC + align256(M * k * g->T * g->is);
     return 0;
@@ -276,7 +279,8 @@ int orc_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int B,
     }
     return 0;
   }
-  int64_t step_bytes = g.P * (g.es + g.is);
+  int64_t step_bytes = g.P * g.es + g.ri;
+  int five = g.ri != g.P * g.is; /* 5-bit index runs */
   for (int64_t r = 0; r < M; ++r) {
     /* region A: step (r, p, t) = P values then P indices; entry (l, v) at position l*V + v,
      * holding canonical (r, b = p*P + v*32 + l, t) */
@@ -289,7 +293,15 @@ int orc_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int B,
             int64_t src = (r * NB + b) * k + t;
             int64_t pos = l * g.V + v;
             memcpy(step + pos * g.es, in + src * g.es, g.es);
-            put_index(step + g.P * g.es + pos * g.is, g.is, idx[src]);
+            if (!five) put_index(step + g.P * g.es + pos * g.is, g.is, idx[src]);
+          }
+        if (five) /* F_l = sum_v idx(l, v) << 5v: u32 plane (bits 0..31), then byte plane (32..39) */
+          for (int l = 0; l < 32; ++l) {
+            uint64_t F = 0;
+            for (int64_t v = 0; v < 8; ++v) F |= (uint64_t)idx[(r * NB + p * g.P + v * 32 + l) * k + t] << (5 * v);
+            unsigned char* run = step + g.P * g.es;
+            for (int j = 0; j < 4; ++j) run[4 * l + j] = (unsigned char)(F >> (8 * j));
+            run[128 + l] = (unsigned char)(F >> 32);
           }
       }
     /* regions B (values) and C (indices): entry (r, t, v, l) at element r*k*T + t*T + v*32 + l

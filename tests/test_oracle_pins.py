@@ -238,12 +238,18 @@ def test_bf16_decoder_sample():
 # ------------------------------------------------------------------ pack (docs/layout.md)
 
 def test_packed_bytes_closed_form():
-    """fc6 4096x25088, f16, B=32, k=3: every region is 256-aligned, so bytes = 3·nnz exactly."""
+    """fc6 4096x25088, f16, B=32, k=3: NB = 784 = 3 panels of 256 blocks + a 16-block tail. Panel entries
+    cost 2 + 5/8 bytes (5-bit index runs, docs/layout.md), tail entries 2 + 1; every region is 256-aligned.
+    That is the algorithmic 2.625 B per nonzero of SURVEY §8(d) on the panels."""
     nnz = 4096 * 784 * 3
-    assert oracle.packed_bytes(4096, 25088, 32, 3, oracle.F16, oracle.SPMV) == 3 * nnz == 28901376
-    assert oracle.packed_bytes(4096, 25088, 32, 3, oracle.F32, oracle.SPMV) == 5 * nnz
-    # 65536², 90%: 402,653,184 nnz -> 1,207,959,552 bytes (f16 + u8)
-    assert oracle.packed_bytes(65536, 65536, 32, 3, oracle.F16, oracle.SPMV) == 3 * 65536 * 2048 * 3
+    panel, tail = 4096 * 768 * 3, 4096 * 16 * 3
+    assert panel + tail == nnz
+    assert oracle.packed_bytes(4096, 25088, 32, 3, oracle.F16, oracle.SPMV) == panel * 21 // 8 + 3 * tail == 25362432
+    assert oracle.packed_bytes(4096, 25088, 32, 3, oracle.F32, oracle.SPMV) == 5 * nnz  # f32: V = 4, u8 indices
+    # 65536², 90%: 402,653,184 nnz, all in panels -> 2.625 B each = 1,056,964,608 bytes
+    assert oracle.packed_bytes(65536, 65536, 32, 3, oracle.F16, oracle.SPMV) == 65536 * 2048 * 3 * 21 // 8 == 1056964608
+    # fc7 (NB = 128 -> V = 4): u8 indices, 3 B per nonzero
+    assert oracle.packed_bytes(4096, 4096, 32, 3, oracle.F16, oracle.SPMV) == 3 * 4096 * 128 * 3
     # B > 256 -> u16 indices: 4 B per nnz at f16
     assert oracle.packed_bytes(64, 1024, 512, 8, oracle.F16, oracle.SPMV) == 4 * 64 * 2 * 8
     # SP24: K/2 values + K/8 metadata bytes per row
@@ -281,6 +287,29 @@ def test_pack_spmv_steps_closed_form():
         np.testing.assert_array_equal(step[512:], np.full(128, t, dtype=np.uint8))
 
 
+def test_pack_spmv_five_bit_runs_closed_form():
+    """B=32, f16, K=8192: NB=256 -> V=8, one panel, k=1. Block b keeps offset (7b+3) mod 32 with value b.
+    The step is 256 values (lane-major transpose), then lane l's 40-bit field sum_v idx(v*32+l) << 5v as
+    32 u32 words and 32 bytes (docs/layout.md), 672 bytes in all, padded to 768."""
+    K, B, NB = 8192, 32, 256
+    blk = np.arange(NB)
+    vals = blk.astype(np.float16).reshape(1, NB, 1)
+    offs = (7 * blk + 3) % 32
+    idx = offs.astype(np.uint16).reshape(1, NB, 1)
+    buf = oracle.pack(vals, idx, 1, K, B, 1, oracle.F16, oracle.SPMV)
+    assert buf.size == 768
+    np.testing.assert_array_equal(buf[:512].view(np.float16), blk.reshape(8, 32).T.reshape(-1).astype(np.float16))
+    words = buf[512:640].view("<u4")
+    tops = buf[640:672]
+    for lane in range(32):
+        F = 0
+        for v in range(8):
+            F |= int(offs[v * 32 + lane]) << (5 * v)
+        assert int(words[lane]) == F & 0xFFFFFFFF
+        assert int(tops[lane]) == F >> 32
+    assert not buf[672:].any()
+
+
 def test_pack_spmm_blob_closed_form():
     """SPMM layout: M=130 rows -> tiles of 128 and 2; K=96, B=32 -> CB=2 blocks per chunk -> chunks of 2 and 1 blocks.
     Each blob lists (row, block, entry) values row-major, 16-byte padded, then the indices."""
@@ -308,7 +337,8 @@ def test_pack_spmm_blob_closed_form():
 
 @pytest.mark.parametrize("layout", [oracle.SPMV, oracle.SPMM])
 @pytest.mark.parametrize("M,K,B,k,dt,dname", [(5, 3008, 32, 3, oracle.F16, "f16"), (3, 1024, 16, 8, oracle.F32, "f32"),
-                                               (2, 2048, 512, 9, oracle.BF16, "bf16"), (4, 64, 4, 2, oracle.F16, "f16")])
+                                               (2, 2048, 512, 9, oracle.BF16, "bf16"), (4, 64, 4, 2, oracle.F16, "f16"),
+                                               (3, 8192 + 1024, 32, 3, oracle.BF16, "bf16")])
 def test_pack_is_a_permutation(layout, M, K, B, k, dt, dname):
     """The packed value+index pairs are exactly the canonical multiset (no entry lost or duplicated)."""
     W = synth.to_numpy(synth.matrix(M, K, dname, seed=21))
@@ -343,15 +373,23 @@ def test_pack_is_a_permutation(layout, M, K, B, k, dt, dname):
     nB = n - nA
     T = NB - (NB // P) * P
     a = lambda x: (x + 255) // 256 * 256
-    A = buf[:nA * (es + isz)].reshape(-1, P * (es + isz))           # steps: P values then P indices
-    offB = a(nA * (es + isz))
+    five = B == 32 and V == 8
+    ri = 160 if five else P * isz                                    # index run bytes per step
+    nsteps = nA // P
+    A = buf[:nsteps * (P * es + ri)].reshape(-1, P * es + ri)         # steps: P values then the index run
+    offB = a(nsteps * (P * es + ri))
     offC = offB + a(nB * es)
     assert buf.size == offC + a(nB * isz)
     vraw = np.concatenate([A[:, :P * es].reshape(-1), buf[offB:offB + nB * es]])   # tail values (region B)
-    iraw = np.concatenate([A[:, P * es:].reshape(-1), buf[offC:offC + nB * isz]])  # tail indices (region C)
     assert T * M * k == nB
     pv = vraw.view(np.uint32 if es == 4 else np.uint16).astype(np.uint64)
-    pi = iraw.view(np.uint8 if isz == 1 else np.uint16).astype(np.uint64)
+    if five:  # 40-bit lane fields: u32 plane + byte plane; index v of lane l is bits 5v..5v+4
+        F = A[:, P * es:P * es + 128].copy().view("<u4").astype(np.uint64) | (A[:, P * es + 128:].astype(np.uint64) << 32)
+        ia = np.stack([(F >> (5 * v)) & 31 for v in range(8)], axis=-1).reshape(-1)  # (step, lane, v) = position l*V + v
+        pi = np.concatenate([ia, buf[offC:offC + nB].astype(np.uint64)])
+    else:
+        iraw = np.concatenate([A[:, P * es:].reshape(-1), buf[offC:offC + nB * isz]])  # tail indices (region C)
+        pi = iraw.view(np.uint8 if isz == 1 else np.uint16).astype(np.uint64)
     cv = vals.reshape(-1).view(np.uint32 if es == 4 else np.uint16).astype(np.uint64)
     ci = idx.reshape(-1).astype(np.uint64)
     np.testing.assert_array_equal(np.sort(pv << 16 | pi), np.sort(cv << 16 | ci))
