@@ -163,8 +163,8 @@ def run_reference(a, rank, world):
     for _ in range(a.steps):
         oracle.spmv_rowslice(v, i, dt, a.K, a.block, k, x)
     dt_s = (time.perf_counter() - t0) / a.steps
-    nnz = rows * (a.K // a.block) * k
-    bytes_step = nnz * (es + 1) + a.K * es + rows * es
+    # the same bytes our arm's value counts (packed W of these rows + x + y), so the two lines compare
+    bytes_step = oracle.packed_bytes(a.M, a.K, a.block, k, dt, oracle.SPMV) * rows / a.M + a.K * es + rows * es
     val = bytes_step / dt_s / 1e9
     sample = f"{rows} of {a.M} rows per step (rows 0..{rows - 1}), sparse-form fp64 SpMV, single thread"
     print(json.dumps({
@@ -190,8 +190,7 @@ def cpu_baseline(a, vals_rows: np.ndarray, idx_rows: np.ndarray, x: np.ndarray, 
         reps += 1
         t_total = time.perf_counter() - t0
     per = t_total / reps
-    nnz = rows * (a.K // a.block) * k
-    b = nnz * (es + 1) + a.K * es + rows * es
+    b = oracle.packed_bytes(a.M, a.K, a.block, k, dt, oracle.SPMV) * rows / a.M + a.K * es + rows * es
     return {"value": round(b / per / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"{rows} sampled rows of the {a.M}x{a.K} layer, fp64 sparse-form SpMV, {reps} reps "
                       f"({t_total:.1f} s), os.cpu_count()={os.cpu_count()}"}
@@ -330,7 +329,7 @@ def main():
         "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
         "config": {"workload": f"configs[4] {M}x{K} balanced-sparse layer, B={B}, s={a.sparsity} (k={k}, achieved "
                                f"{1 - k / B:.5f}), batch 1 SpMV, row-sharded x{world}" + (" + NCCL all_gather(y)" if world > 1 else ""),
-                   "M": M, "K": K, "block": B, "k": k, "batch": 1, "index_bytes": 1 if B <= 256 else 2,
+                   "M": M, "K": K, "block": B, "k": k, "batch": 1, "index_bits": 5 if (B == 32 and es == 2 and K // B >= 256) else (8 if B <= 256 else 16),
                    "packed_bytes_total": full_packed, "packed_bytes_per_rank": A.nbytes,
                    "l2": f"inputs larger than L2: {C} rotating cop{'y' if C == 1 else 'ies'} of a {A.nbytes / 1e6:.0f} MB "
                          f"packed slice vs {l2 / 1e6:.0f} MB L2",

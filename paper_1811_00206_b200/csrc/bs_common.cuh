@@ -27,6 +27,7 @@ struct Geom {
   int64_t P;    // 32*V blocks per panel
   int64_t NBf;  // full panels per row
   int64_t T;    // tail blocks per row
+  int64_t ri;   // SPMV: bytes of a step's index run (160 = 5-bit runs for B = 32, V = 8; else P·is)
   int64_t offA, offB, offC, total;  // SPMV/SPMM: panel steps, tail values, tail indices. SP24: values, metadata.
 };
 
@@ -45,6 +46,7 @@ inline bool make_geom(int64_t M, int64_t K, int B, int k, int dt, int layout, Ge
     g->P = (M + 127) / 128;
     g->NBf = (g->NB + CB - 1) / CB;
     g->T = 0;
+    g->ri = 0;
     const int64_t mt_last = M - 128 * (g->P - 1), cb_last = g->NB - CB * (g->NBf - 1);
     auto blob = [&](int64_t mt, int64_t cb) {
       return align_up(mt * cb * k * g->es, 16) + align_up(mt * cb * k * g->is, 16);
@@ -65,16 +67,19 @@ inline bool make_geom(int64_t M, int64_t K, int B, int k, int dt, int layout, Ge
     g->P = 32LL * V;
     g->NBf = g->NB / g->P;
     g->T = g->NB - g->NBf * g->P;
-    // region A: M·NBf·k steps of P·(es + is) bytes; B / C: tail values / indices (M·k·T each)
+    // docs/layout.md: 5-bit index runs (a u32 plane and a byte plane of 40-bit lane fields) when
+    // B = 32 and V = 8; otherwise P indices of `is` bytes
+    g->ri = (B == 32 && V == 8) ? 160 : g->P * g->is;
+    // region A: M·NBf·k steps of P·es + ri bytes; B / C: tail values / indices (M·k·T each)
     g->offA = 0;
-    g->offB = align_up(M * g->NBf * k * g->P * (g->es + g->is), kAlign);
+    g->offB = align_up(M * g->NBf * k * (g->P * g->es + g->ri), kAlign);
     g->offC = g->offB + align_up(M * k * g->T * g->es, kAlign);
     g->total = g->offC + align_up(M * k * g->T * g->is, kAlign);
     return true;
   }
   if (layout == BS_LAYOUT_SP24) {
     if (B != 4 || k != 2 || K % 8 != 0) return false;
-    g->V = 0; g->P = 0; g->NBf = 0; g->T = 0;
+    g->V = 0; g->P = 0; g->NBf = 0; g->T = 0; g->ri = 0;
     g->offA = 0;
     g->offB = align_up(M * (K / 2) * g->es, kAlign);
     g->offC = 0;

@@ -10,6 +10,7 @@ namespace {
 struct PackArgs {
   int64_t M, NB, NBf, T, P;
   int V, k, es, is;
+  int64_t ri;  // index run bytes per step (160: 5-bit runs, written by pack_idx5_kernel)
   int64_t offA, offB, offC;
 };
 
@@ -18,7 +19,8 @@ __global__ void pack_kernel(const VT* __restrict__ vals, const uint16_t* __restr
                             uint8_t* __restrict__ base, int64_t nA, int64_t nB, bool unpack,
                             VT* __restrict__ out_vals, uint16_t* __restrict__ out_idx) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t step_bytes = a.P * (a.es + a.is);
+  const int64_t step_bytes = a.P * a.es + a.ri;
+  const bool five = a.ri != a.P * a.is;
   const int64_t kT = (int64_t)a.k * a.T;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nA + nB; e += stride) {
     int64_t src;
@@ -46,6 +48,19 @@ __global__ void pack_kernel(const VT* __restrict__ vals, const uint16_t* __restr
       vdst = base + a.offB + f * a.es;
       idst = base + a.offC + f * a.is;
     }
+    if (five && e < nA) {  // 5-bit runs: indices are packed per lane by pack_idx5_kernel
+      const int64_t pos = e % a.P;
+      const int l = (int)(pos / a.V), v = (int)(pos % a.V);
+      if (!unpack) {
+        *(VT*)vdst = vals[src];
+      } else {
+        const uint8_t* run = vdst - pos * a.es + a.P * a.es;
+        const uint64_t F = (uint64_t)(*(const uint32_t*)(run + 4 * l)) | ((uint64_t)run[128 + l] << 32);
+        out_vals[src] = *(const VT*)vdst;
+        out_idx[src] = (uint16_t)((F >> (5 * v)) & 31u);
+      }
+      continue;
+    }
     if (!unpack) {
       *(VT*)vdst = vals[src];
       const uint16_t o = idx[src];
@@ -59,6 +74,29 @@ __global__ void pack_kernel(const VT* __restrict__ vals, const uint16_t* __restr
 }
 
 // SP24 metadata: byte (r, c) holds blocks b = 2c, 2c+1 of row r as nibbles idx0 | idx1 << 2.
+// 5-bit index runs (docs/layout.md): one thread per (step, lane) builds the 40-bit field
+// F_l = sum_v idx(l, v) << 5v of its 8 indices and writes word l of the u32 plane and byte l of the byte plane.
+__global__ void pack_idx5_kernel(const uint16_t* __restrict__ idx, PackArgs a, uint8_t* __restrict__ base, int64_t nsl) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t step_bytes = a.P * a.es + a.ri;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nsl; e += stride) {
+    const int64_t s = e >> 5;
+    const int l = (int)(e & 31);
+    const int t = (int)(s % a.k);
+    const int64_t rp = s / a.k;
+    const int64_t p = rp % a.NBf, r = rp / a.NBf;
+    uint64_t F = 0;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int64_t b = p * a.P + (int64_t)v * 32 + l;
+      F |= (uint64_t)(idx[(r * a.NB + b) * a.k + t] & 31u) << (5 * v);
+    }
+    uint8_t* run = base + a.offA + s * step_bytes + a.P * a.es;
+    *(uint32_t*)(run + 4 * l) = (uint32_t)F;
+    run[128 + l] = (uint8_t)(F >> 32);
+  }
+}
+
 __global__ void sp24_meta_kernel(const uint16_t* __restrict__ idx, int64_t nbytes, uint8_t* __restrict__ meta,
                                  bool unpack, uint16_t* __restrict__ out_idx) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -153,10 +191,11 @@ cudaError_t run(const bsk::Geom& g, const void* vals, const uint16_t* idx, void*
   }
   PackArgs a;
   a.M = g.M; a.NB = g.NB; a.NBf = g.NBf; a.T = g.T; a.P = g.P; a.V = g.V; a.k = g.k; a.es = g.es; a.is = g.is;
+  a.ri = g.ri;
   a.offA = g.offA; a.offB = g.offB; a.offC = g.offC;
   const int64_t nA = g.M * g.NBf * g.P * g.k, nB = g.M * g.T * g.k;
   if (!unpack) {
-    if ((err = zero_gap(base, nA * (g.es + g.is), g.offB, s))) return err;
+    if ((err = zero_gap(base, (nA / (g.P > 0 ? g.P : 1)) * (g.P * g.es + g.ri), g.offB, s))) return err;
     if ((err = zero_gap(base, g.offB + nB * g.es, g.offC, s))) return err;
     if ((err = zero_gap(base, g.offC + nB * g.is, g.total, s))) return err;
   }
@@ -169,6 +208,13 @@ cudaError_t run(const bsk::Geom& g, const void* vals, const uint16_t* idx, void*
   } else {
     pack_kernel<uint16_t><<<(unsigned)blocks, 256, 0, s>>>((const uint16_t*)vals, idx, a, base, nA, nB, unpack,
                                                           (uint16_t*)out_vals, out_idx);
+  }
+  if (!unpack && nA > 0 && g.ri != g.P * g.is) {
+    if ((err = cudaGetLastError())) return err;
+    const int64_t nsl = nA / g.P * 32;  // (step, lane) pairs
+    int64_t b5 = (nsl + 255) / 256;
+    if (b5 > (int64_t)sms * 32) b5 = (int64_t)sms * 32;
+    pack_idx5_kernel<<<(unsigned)b5, 256, 0, s>>>(idx, a, base, nsl);
   }
   return cudaGetLastError();
 }

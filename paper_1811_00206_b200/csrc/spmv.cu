@@ -44,6 +44,9 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
   const int64_t group_bytes = (int64_t)g.B * 32 * g.es * nv;  // 32 blocks of x slots
   const int64_t chunk_group = (int64_t)g.B * 32 * g.es * chunk_nv;
   const int64_t tail_groups = (g.NB + 31) / 32 - g.NBf * g.V;
+  // 16-bit SpMV with V >= 2 stores x in group pairs (spmv_impl.cuh stage_x PAIR): round staged groups up to even
+  const bool pair = g.es == 2 && nv == 1 && g.V >= 2;
+  auto ev = [&](int64_t n) { return pair ? (n + 1) / 2 * 2 : n; };
   if (g.NBf > 0 && g.k > 0) {
     int64_t PC = kXBudget / (chunk_group * g.V);
     if (PC < 1) PC = 1;
@@ -59,15 +62,15 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
     a.nchunks = (int)nchunks;
     a.tail_in_last = (last_np * g.V + tail_groups) * chunk_group <= kXBudget;
     int64_t xb = PC * g.V * group_bytes;
-    const int64_t need_last = (last_np * g.V + (a.tail_in_last ? tail_groups : 0)) * group_bytes;
+    const int64_t need_last = ev(last_np * g.V + (a.tail_in_last ? tail_groups : 0)) * group_bytes;
     if (need_last > xb) xb = need_last;
-    if (!a.tail_in_last && tail_groups * group_bytes > xb) xb = tail_groups * group_bytes;
+    if (!a.tail_in_last && ev(tail_groups) * group_bytes > xb) xb = ev(tail_groups) * group_bytes;
     a.xbytes = (int)xb;
   } else {  // no full panels (or k == 0): the tail groups only
     a.PC = 1;
     a.nchunks = 0;
     a.tail_in_last = 0;
-    a.xbytes = g.k > 0 ? (int)(tail_groups * group_bytes) : 0;
+    a.xbytes = g.k > 0 ? (int)(ev(tail_groups) * group_bytes) : 0;
   }
   if (a.xbytes > bsk::dev_props().smem_optin - 16 * 1024) return cudaErrorInvalidConfiguration;
   if ((uint64_t)g.M * (uint64_t)(bsk::dev_props().sms + 1) >= (1ULL << 32)) return cudaErrorInvalidConfiguration;

@@ -133,10 +133,14 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 // 2m and 2m+1 share a word. Work items are (group, 16-byte piece of a block); each lane issues up to
 // 8 piece loads before storing them. `after_loads()` runs once, right after the first batch of
 // loads is in flight, so that the caller can queue the W bulk copies behind them.
-template <int ES, int BT, typename F>
+// PAIR (16-bit x, V >= 2): groups 2j and 2j+1 share slot words. Element (b, o), b = 32·g + l, goes to
+// byte ((g>>1)·B + o)·128 + 4·l + 2·(g&1): lane l's slots are all in bank l, for any offsets (with
+// halfword slots per group, lanes 2m and 2m+1 would share a bank with different offsets: 2-way
+// conflicts). The consumer's group index is compile-time, so the address is still one IMAD.
+template <int ES, int BT, bool PAIR, typename F>
 __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint32_t sx, int64_t g0, int64_t g1, F after_loads) {
   constexpr int PE = 16 / ES;        // elements per 16-byte piece
-  constexpr uint32_t ROWB = 32 * ES;  // bytes per slot row (one offset o of 32 blocks)
+  constexpr uint32_t ROWB = PAIR ? 128 : 32 * ES;  // bytes per slot row (one offset o of 32 blocks, or of 64 when paired)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int B = BT > 0 ? BT : a.B;
   bool hooked = false;
@@ -167,7 +171,8 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint32_t sx, int64_t 
           const uint32_t q = j - gl * ppb;
           const int64_t b = (g0 + gl) * 32 + lane;
           if (b < a.NB) {
-            const uint32_t col = sx + (gl * B + q * PE) * ROWB + lane * ES;
+            const uint32_t col = PAIR ? sx + ((gl >> 1) * B + q * PE) * ROWB + lane * 4 + (gl & 1) * 2
+                                      : sx + (gl * B + q * PE) * ROWB + lane * ES;
             const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
             for (int e = 0; e < PE; ++e) {
@@ -183,7 +188,9 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint32_t sx, int64_t 
     for (int64_t g = g0 + warp; g < g1; g += nw) {
       const int64_t b = g * 32 + lane;
       if (b >= a.NB) continue;
-      const uint32_t col = sx + (uint32_t)(g - g0) * (uint32_t)B * ROWB + lane * ES;
+      const uint32_t gl = (uint32_t)(g - g0);
+      const uint32_t col = PAIR ? sx + (gl >> 1) * (uint32_t)B * ROWB + lane * 4 + (gl & 1) * 2
+                                : sx + gl * (uint32_t)B * ROWB + lane * ES;
       for (int o = 0; o < B; ++o) {
         if (ES == 2) bsk::sts_u16(col + o * ROWB, __ldg((const uint16_t*)a.x + b * B + o));
         else bsk::sts_u32(col + o * ROWB, __ldg((const uint32_t*)a.x + b * B + o));
@@ -311,11 +318,19 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   using raw_t = typename bsk::DTraits<DT>::raw_t;
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int P = 32 * V;
-  constexpr uint32_t STEPB = P * (ES + IS);  // bytes per step (values then indices)
+  // IS: index bytes (1 or 2), or 5 = 5-bit index runs (B = 32, V = 8; docs/layout.md): per step a
+  // plane of 32 u32 words and a plane of 32 bytes, lane l's 40-bit field sum_v idx(l, v) << 5v
+  static_assert(IS != 5 || (V == 8 && BT == 32), "5-bit runs need V = 8 and B = 32");
+  constexpr int ISt = IS == 5 ? 1 : IS;                // tail index bytes (regions B/C)
+  constexpr uint32_t RI = IS == 5 ? 160u : P * IS;     // index run bytes per step
+  constexpr uint32_t STEPB = P * ES + RI;              // bytes per step (values then indices)
   constexpr uint32_t SB = Q * STEPB;         // bytes per ring stage
   const int B = BT > 0 ? BT : a.B;
   constexpr uint32_t SLB = ES * NV;       // bytes per x slot (NV batch columns of one x column)
   constexpr uint32_t ROWB = 32 * SLB;     // bytes per slot row of x (one offset o of 32 blocks)
+  constexpr bool PAIR = ES == 2 && NV == 1 && V >= 2;  // paired groups (stage_x): lane l stays in bank l
+  constexpr uint32_t XROW = PAIR ? 128u : ROWB;         // slot-row stride seen by the gathers
+  constexpr uint32_t LSLB = PAIR ? 4u : SLB;            // lane stride of the slots
   constexpr int NA = NV == 1 ? V : NV;    // accumulators: V chains (SpMV) or one per batch column
   const uint32_t GSW = (uint32_t)B * ROWB;  // bytes per group of 32 blocks
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = NT / 32;
@@ -336,11 +351,11 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   // A tail stage holds R rows: the value run (from the 16-byte-aligned address at or below it, offset
   // dv), then, at the next 16-byte boundary, the index run (offset di).
   auto tail_geom = [&](int64_t t0, int64_t R, uint32_t& dv, uint32_t& bv, uint32_t& di, uint32_t& bi) {
-    const int64_t ov = (wr0 + t0) * kT * ES, oi = (wr0 + t0) * kT * IS;
+    const int64_t ov = (wr0 + t0) * kT * ES, oi = (wr0 + t0) * kT * ISt;
     dv = (uint32_t)(ov & 15);
     di = (uint32_t)(oi & 15);
     bv = (uint32_t)((dv + R * kT * ES + 15) & ~15LL);
-    bi = (uint32_t)((di + R * kT * IS + 15) & ~15LL);
+    bi = (uint32_t)((di + R * kT * ISt + 15) & ~15LL);
   };
 
   // ---- producer cursor (lane 0). Phase 1: (chunk pc, row pr, step ps) of the next panel stage.
@@ -383,7 +398,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
       tail_geom(tr, R, dv, bv, di, bi);
       mbar_expect_tx(bar, bv + bi);
       bulk_g2s(ring + st * SB, a.Bt + (wr0 + tr) * kT * ES - dv, bv, bar, pol);
-      bulk_g2s(ring + st * SB + bv, a.Ct + (wr0 + tr) * kT * IS - di, bi, bar, pol);
+      bulk_g2s(ring + st * SB + bv, a.Ct + (wr0 + tr) * kT * ISt - di, bi, bar, pol);
       tr += R;
     }
   };
@@ -421,7 +436,9 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   // gather x slot(s) of offset o for owned block v and accumulate w·x
   auto gather_fma = [&](uint32_t base, uint32_t o, int v, uint32_t w) {
     if constexpr (NV == 1) {
-      bsk::fma_acc<DT>(acc[v], w, lds_x<DT>(base + o * ROWB + v * GSW));
+      const uint32_t ad = PAIR ? base + o * XROW + (uint32_t)(v >> 1) * 2u * GSW + (uint32_t)(v & 1) * 2u
+                               : base + o * ROWB + v * GSW;
+      bsk::fma_acc<DT>(acc[v], w, lds_x<DT>(ad));
     } else {
       uint32_t xw[4];
       const uint32_t ad = base + o * ROWB + v * GSW;
@@ -469,7 +486,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
     const int64_t npc = (a.NBf - (int64_t)c * a.PC) < a.PC ? (a.NBf - (int64_t)c * a.PC) : a.PC;
     const int64_t g1 = last && a.tail_in_last ? (a.NB + 31) / 32 : g0 + npc * V;
     if (c > 0) __syncthreads();  // all warps are done with the previous chunk's x
-    if constexpr (NV == 1) stage_x<ES, BT>(a, sx, g0, g1, arm_once);
+    if constexpr (NV == 1) stage_x<ES, BT, PAIR>(a, sx, g0, g1, arm_once);
     else stage_xn<NV, BT>(a, sx, g0, g1, arm_once);
     if (c == 0) BS_MARK(6);
     __syncthreads();
@@ -479,7 +496,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
     const uint32_t pstep = V * GSW;
     const int k = a.k;
     for (int64_t i = 0; i < nrows; ++i) {
-      uint32_t pb = sx + lane * SLB;  // slot base of the current panel within the chunk
+      uint32_t pb = sx + lane * LSLB;  // slot base of the current panel within the chunk
       int t = 0;
       for (int64_t s0 = 0; s0 < L; s0 += Q) {
         const uint32_t st = cst;
@@ -489,21 +506,27 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
         const uint32_t sbase = ring + st * SB;
         const int nq = (L - s0) < Q ? (int)(L - s0) : Q;
         auto step = [&](int q) {
-          uint32_t wv[(V * ES + 3) / 4], iv[(V * IS + 3) / 4];
+          uint32_t wv[(V * ES + 3) / 4], iv[(V * ISt + 3) / 4 > 2 ? (V * ISt + 3) / 4 : 2];
           const uint32_t av = sbase + q * STEPB + lane * (V * ES);
-          const uint32_t ai = sbase + q * STEPB + P * ES + lane * (V * IS);
+          const uint32_t ai = sbase + q * STEPB + P * ES + lane * (IS == 5 ? 4 : V * IS);
           if constexpr (V * ES == 16) bsk::lds_v4(av, wv[0], wv[1], wv[2], wv[3]);
           else if constexpr (V * ES == 8) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(wv[0]), "=r"(wv[1]) : "r"(av));
           else if constexpr (V * ES == 4) wv[0] = bsk::lds_u32(av);
           else wv[0] = bsk::lds_u16(av);
-          if constexpr (V * IS == 16) bsk::lds_v4(ai, iv[0], iv[1], iv[2], iv[3]);
+          if constexpr (IS == 5) {
+            iv[0] = bsk::lds_u32(ai);
+            iv[1] = lds_u8(sbase + q * STEPB + P * ES + 128 + lane);
+          } else if constexpr (V * IS == 16) bsk::lds_v4(ai, iv[0], iv[1], iv[2], iv[3]);
           else if constexpr (V * IS == 8) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(iv[0]), "=r"(iv[1]) : "r"(ai));
           else if constexpr (V * IS == 4) iv[0] = bsk::lds_u32(ai);
           else if constexpr (V * IS == 2) iv[0] = bsk::lds_u16(ai);
           else iv[0] = lds_u8(ai);
 #pragma unroll
           for (int v = 0; v < V; ++v) {
-            const uint32_t o = IS == 1 ? byte_of(iv[v >> 2], v & 3) : (iv[v >> 1] >> (16 * (v & 1))) & 0xffffu;
+            uint32_t o;
+            if constexpr (IS == 5) o = (v < 7 ? __funnelshift_r(iv[0], iv[1], 5 * v) : iv[1] >> 3) & 31u;
+            else if constexpr (IS == 1) o = byte_of(iv[v >> 2], v & 3);
+            else o = (iv[v >> 1] >> (16 * (v & 1))) & 0xffffu;
             const uint32_t w = ES == 2 ? (wv[v >> 1] >> (16 * (v & 1))) & 0xffffu : wv[v];
             gather_fma(pb, o, v, w);
           }
@@ -543,7 +566,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
       tbase = sx + (uint32_t)(gt0 - (int64_t)(a.nchunks - 1) * a.PC * V) * GSW;
     } else {
       __syncthreads();
-      if constexpr (NV == 1) stage_x<ES, BT>(a, sx, gt0, gt1, arm_once);
+      if constexpr (NV == 1) stage_x<ES, BT, PAIR>(a, sx, gt0, gt1, arm_once);
       else stage_xn<NV, BT>(a, sx, gt0, gt1, arm_once);
       __syncthreads();
       tbase = sx;
@@ -564,7 +587,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
           if (v < Vt && bl < a.T) {
             const uint32_t w = ldv(e0 + bl);
             const uint32_t o = ldi(e0 + bl);
-            gather_fma(tbase + lane * SLB, o, v, w);
+            gather_fma(tbase + lane * LSLB, o, v, w);
           }
         }
       }
@@ -578,9 +601,9 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
         tail_geom(t0, R, dv, bv, di, bi);
         for (int64_t rr = 0; rr < R; ++rr) {
           const uint32_t rv = ring + st * SB + dv + (uint32_t)(rr * kT * ES);
-          const uint32_t ri = ring + st * SB + bv + di + (uint32_t)(rr * kT * IS);
+          const uint32_t ri = ring + st * SB + bv + di + (uint32_t)(rr * kT * ISt);
           tail_row([&](uint32_t e) { return ES == 2 ? bsk::lds_u16(rv + e * 2) : bsk::lds_u32(rv + e * 4); },
-                   [&](uint32_t e) { return IS == 1 ? lds_u8(ri + e) : bsk::lds_u16(ri + e * 2); });
+                   [&](uint32_t e) { return ISt == 1 ? lds_u8(ri + e) : bsk::lds_u16(ri + e * 2); });
           finish_row(wr0 + t0 + rr);
         }
         __syncwarp();
@@ -590,9 +613,9 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
     } else {  // direct loads (a row's tail does not fit a ring stage)
       for (int64_t i = 0; i < nrows; ++i) {
         const uint8_t* rv = a.Bt + (wr0 + i) * kT * ES;
-        const uint8_t* ri = a.Ct + (wr0 + i) * kT * IS;
+        const uint8_t* ri = a.Ct + (wr0 + i) * kT * ISt;
         tail_row([&](uint32_t e) { return ES == 2 ? (uint32_t)__ldg((const uint16_t*)rv + e) : __ldg((const uint32_t*)rv + e); },
-                 [&](uint32_t e) { return IS == 1 ? (uint32_t)__ldg(ri + e) : (uint32_t)__ldg((const uint16_t*)ri + e); });
+                 [&](uint32_t e) { return ISt == 1 ? (uint32_t)__ldg(ri + e) : (uint32_t)__ldg((const uint16_t*)ri + e); });
         finish_row(wr0 + i);
       }
     }
@@ -613,7 +636,7 @@ template <int DT, int V, int IS, int BT, bool MULTI, int NT, int QM, int NV>
 cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int Q = StageSteps<V, ES>::value * QM;
-  constexpr int SB = Q * 32 * V * (ES + IS);
+  constexpr int SB = Q * (32 * V * ES + (IS == 5 ? 160 : 32 * V * IS));
   static int static_smem = -1;  // per instantiation: static smem (the mbarriers)
   auto kern = spmv_kernel<DT, V, IS, Q, BT, MULTI, NT, NV>;
   const auto& dp = bsk::dev_props();
@@ -628,7 +651,7 @@ cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   SpmvArgs a = a0;
   a.tail_rows = 0;
   if (a.T > 0 && a.k > 0) {  // whole rows of tail per ring stage (32 bytes of alignment slack)
-    const int64_t per = (int64_t)a.k * a.T * (ES + IS);
+    const int64_t per = (int64_t)a.k * a.T * (ES + (IS == 5 ? 1 : IS));
     const int64_t R = (SB - 64) / per;
     a.tail_rows = R >= 1 ? (int)(R < 64 ? R : 64) : 0;
   }
@@ -664,9 +687,14 @@ cudaError_t launch_nt(const SpmvArgs& a, cudaStream_t s) {
 template <int DT, int V, int IS, int NV>
 cudaError_t launch_t(const SpmvArgs& a, cudaStream_t s) {
   const bool multi = a.nchunks > 1 || a.T > 0;
-  if (a.B == 32 && IS == 1)
+  if constexpr (IS == 5) {  // B = 32, V = 8 only
     return multi ? launch_nt<DT, V, IS, 32, true, NV>(a, s) : launch_nt<DT, V, IS, 32, false, NV>(a, s);
-  return multi ? launch_nt<DT, V, IS, 0, true, NV>(a, s) : launch_nt<DT, V, IS, 0, false, NV>(a, s);
+  } else {
+    // B = 32 with V = 8 (16-bit) always uses 5-bit runs, so the B = 32 specialisation is for V < 8
+    if constexpr (IS == 1 && V < 8)
+      if (a.B == 32) return multi ? launch_nt<DT, V, IS, 32, true, NV>(a, s) : launch_nt<DT, V, IS, 32, false, NV>(a, s);
+    return multi ? launch_nt<DT, V, IS, 0, true, NV>(a, s) : launch_nt<DT, V, IS, 0, false, NV>(a, s);
+  }
 }
 
 template <int DT, int IS, int NV>
@@ -683,6 +711,8 @@ cudaError_t dispatch_v(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
 
 template <int DT, int NV>
 cudaError_t dispatch_is(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
+  if constexpr (DT != BS_F32)
+    if (g.ri != g.P * g.is) return launch_t<DT, 8, 5, NV>(a, s);  // 5-bit index runs
   return g.is == 1 ? dispatch_v<DT, 1, NV>(g, a, s) : dispatch_v<DT, 2, NV>(g, a, s);
 }
 
