@@ -35,7 +35,7 @@
 
 #if defined(BS_TRACE) && defined(BS_TRACE_TU)
 // Debug timeline (tools/trace_probe.py): %globaltimer at phase boundaries, per (CTA, warp).
-__device__ unsigned long long g_bs_trace[1024 * 16 * 8];
+__device__ unsigned long long g_bs_trace[1024 * 16 * 16];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -44,7 +44,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define BS_MARK(i)                                                                                       \
   do {                                                                                                   \
     if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < 16)                                              \
-      g_bs_trace[(blockIdx.x * 16 + (threadIdx.x >> 5)) * 8 + (i)] = gtime();                            \
+      g_bs_trace[(blockIdx.x * 16 + (threadIdx.x >> 5)) * 16 + (i)] = gtime();                           \
   } while (0)
 extern "C" int bs_trace_read(void* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, g_bs_trace, (size_t)n * 8);
@@ -625,6 +625,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
     __syncwarp();
     for (int64_t i = lane; i < nrows * NV; i += 32) store_y(wr0 + i / NV, (int)(i % NV), part[(wr0 + i / NV) * NV + i % NV]);
   }
+  BS_MARK(8);
 }
 
 template <int V, int ES>
@@ -679,6 +680,8 @@ cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+// One 16-warp CTA per SM. (8-warp CTAs in half an SM, so that the next PDL kernel's CTA could be
+// resident and prefetch its W, measured 1.1-1.4x slower on every latency-regime layer: DESIGN.md §4.)
 template <int DT, int V, int IS, int BT, bool MULTI, int NV>
 cudaError_t launch_nt(const SpmvArgs& a, cudaStream_t s) {
   return launch_cfg<DT, V, IS, BT, MULTI, 512, 1, NV>(a, s);

@@ -1,4 +1,4 @@
-"""Tuning sweep for the SpMV kernel knobs (BS_SPMV_CFG, BS_SPMV_ROWS) on the GPU.
+"""Timing sweep of bs_spmv_ex on the paper's layer shapes (FLAGS = launch flags) on the GPU.
 
     python tools/spmv_sweep.py            # parent: runs each knob combination in a subprocess
 Prints one JSON line per (knobs, shape, sparsity): microseconds and packed GB/s (CUDA events, rotating
@@ -13,6 +13,9 @@ sys.path.insert(0, ROOT)
 
 SHAPES = [("big", 65536, 65536), ("fc6", 4096, 25088), ("fc7", 4096, 4096), ("ptb", 6000, 3008), ("ctc_ih", 4096, 2048), ("ctc_hh", 4096, 1024)]
 SPARS = [0.5, 0.9, 0.97]
+
+
+FLAGS = int(os.environ.get("FLAGS", "3"))  # bs_spmv_ex flags: 1 = PDL, 3 = PDL | W_STATIC
 
 
 def child():
@@ -43,7 +46,7 @@ def child():
             with torch.cuda.stream(s_):
                 with torch.cuda.graph(g, stream=s_):
                     for j in range(min(iters, 200)):
-                        bs.spmv(mats[j % C], x, out=y)
+                        bs.spmv(mats[j % C], x, out=y, flags=FLAGS)
             reps = max(1, iters // 200)
             g.replay()
             torch.cuda.synchronize()
@@ -55,9 +58,9 @@ def child():
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / (reps * min(iters, 200)) * 1e3
             pk = A.nbytes + K * 2 + M * 2
-            print(json.dumps({"cfg": os.environ.get("BS_SPMV_CFG", "auto"), "rows": os.environ.get("BS_SPMV_ROWS", "strided"),
+            print(json.dumps({
                               "shape": name, "s": s, "us": round(us, 2), "GBps": round(pk / us / 1e3, 1),
-                              "copies": C}), flush=True)
+                              "copies": C, "flags": FLAGS}), flush=True)
             del mats, A
 
 
@@ -65,7 +68,6 @@ if __name__ == "__main__":
     if "--child" in sys.argv:
         child()
         sys.exit(0)
-    combos = [c.split("/") for c in os.environ.get("COMBOS", "auto/contig").split(",")]
-    for cfg, rows in combos:
-        env = dict(os.environ, BS_SPMV_CFG=cfg, BS_SPMV_ROWS=rows)
+    for _ in (0,):
+        env = dict(os.environ)
         subprocess.run([sys.executable, __file__, "--child"], env=env, check=False)

@@ -47,17 +47,19 @@ if __name__ == "__main__":
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    bs.spmv(mats[-1], x, out=y)
+    fl = int(os.environ.get("FLAGS", "1"))
+    bs.spmv(mats[-2], x, out=y, flags=fl)  # the traced kernel follows another one, as in a layer chain
+    bs.spmv(mats[-1], x, out=y, flags=fl)
     e1.record()
     torch.cuda.synchronize()
-    n = 148 * 16 * 8
+    n = 148 * 16 * 16
     buf = (ctypes.c_ulonglong * n)()
     bs._lib.bs_trace_read(ctypes.byref(buf), n)
-    t = np.frombuffer(buf, dtype=np.uint64).reshape(148, 16, 8).astype(np.int64)
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(148, 16, 16).astype(np.int64)
     t0 = t[:, :, 0][t[:, :, 0] > 0].min()
     rel = np.where(t > 0, t - t0, -1)
     print(f"{name} s={s} event_us={e0.elapsed_time(e1)*1e3:.2f}")
-    for ph, lab in [(0, "entry"), (5, "mbar init"), (7, "1st copy"), (1, "issued"), (6, "staged(warp)"), (2, "x staged"), (3, "first stage"), (4, "panels done")]:
+    for ph, lab in [(0, "entry"), (5, "mbar init"), (7, "1st copy"), (1, "issued"), (6, "staged(warp)"), (2, "x staged"), (3, "first stage"), (4, "panels done"), (8, "end")]:
         col = rel[:, :, ph]
         col = col[col >= 0]
         if col.size:
