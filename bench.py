@@ -477,6 +477,43 @@ def layer_rows(a, bs, hbm_peak, l2):
                            "o_time = measured empty-kernel graph node (P:264-266, SURVEY A18)"}
 
 
+def epilogue_rows(a, bs, l2):
+    """The fused layer epilogue (bs_spmv_fused, Eq. 1 with its +B and an activation) on
+    the paper's layers: one kernel vs the same SpMV followed by torch bias-add and activation kernels, and vs
+    cuBLAS dense addmv + activation on the same W_bs. CUDA-graph timed, rotating copies (> 3x L2)."""
+    rows = []
+    dev = torch.device("cuda")
+    acts = {"relu": torch.relu, "sigmoid": torch.sigmoid, "tanh": torch.tanh}
+    for name, M, K, s, act in (("configs[2] VGG fc6 4096x25088", 4096, 25088, 0.9, "relu"),
+                               ("configs[2] VGG fc7 4096x4096", 4096, 4096, 0.9, "relu"),
+                               ("configs[1] PTB LSTM gates 6000x3008", 6000, 3008, 0.9, "sigmoid")):
+        W = synth.matrix(M, K, a.dtype, seed=synth.seed_for(5, M + K), device=dev)
+        x = synth.vector(K, a.dtype, seed=synth.seed_for(5, 1), device=dev)
+        b = synth.vector(M, a.dtype, seed=synth.seed_for(5, 2), device=dev)
+        y = torch.empty(M, dtype=W.dtype, device=dev)
+        ks = bs.k_from_sparsity(a.block, s)
+        v, i, _ = bs.prune(W, a.block, k=ks)
+        A = bs.pack(v, i, K, a.block)
+        mats = rotating(bs, A, l2)
+        C = len(mats)
+        n_in = 20 * C if C < 10 else 2 * C
+        fl = bs.SPMV_PDL | bs.SPMV_W_STATIC
+        t_fused = graph_time_us(lambda j: bs.spmv(mats[j % C], x, out=y, flags=fl, bias=b, act=act), n_in)
+        f = acts[act]
+        t_unfused = graph_time_us(lambda j: f(bs.spmv(mats[j % C], x, out=y, flags=fl).add_(b)), n_in)
+        Wbs = dense_from_canonical(v, i, M, K, a.block)
+        dens = [Wbs] + [Wbs.clone() for _ in range(max(1, -(-3 * l2 // (Wbs.numel() * Wbs.element_size()))) - 1)]
+        Cd = len(dens)
+        t_dense = graph_time_us(lambda j: f(torch.addmv(b, dens[j % Cd], x)), 4 * Cd)
+        rows.append({"layer": name, "sparsity": s, "k": ks, "act": act, "fused_us": round(t_fused, 2),
+                     "unfused_us": round(t_unfused, 2), "cublas_addmv_act_us": round(t_dense, 2),
+                     "speedup_vs_unfused": round(t_unfused / t_fused, 2), "speedup_vs_cublas": round(t_dense / t_fused, 2)})
+        del dens, Wbs, mats, A, v, i, W
+    return {"epilogue": rows,
+            "epilogue_note": "y = act(W_bs x + b): fused = bs_spmv_fused (one kernel, bias staged in shared memory); "
+                             "unfused = bs_spmv + torch add_ + act; cublas = torch.addmv on the dense W_bs + act"}
+
+
 def spmm_rows(a, bs, hbm_peak, l2):
     """SpMM legs of BASELINE configs[2] (fc6/fc7 at batch 32) and configs[3] (CTC batch sweep 1-256 with the
     balanced B = 32 layer and the 2:4 sparse-MMA path), CUDA-graph timed with rotating copies, next to cuBLAS
@@ -572,6 +609,7 @@ def extras(a, bs, W, A, vals, idx, x, k, es, hbm_peak, stream):
     res["baselines"] = {"cublas_dense_us": round(t_dense, 2), "cublas_path": f"torch.{dense_name} on dense W_bs (f16)",
                         "cusparse_path": "torch.mv on int32 CSR of W_bs (cusparseSpMV)"}
     res.update(layer_rows(a, bs, hbm_peak, l2))
+    res.update(epilogue_rows(a, bs, l2))
     res.update(spmm_rows(a, bs, hbm_peak, l2))
     res["paper_context"] = ("paper: 1.4-3.1x over cuBLAS/cuSPARSE/block-sparse on an unnamed ~2018 GPU (P:8, P:48); "
                             "context only, not a target")

@@ -131,6 +131,20 @@ int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream);
  * every flag combination. */
 int bs_spmv_ex(const bs_matrix* A, const void* x, void* y, unsigned flags, void* stream);
 
+/* Activations of the fused layer epilogue. */
+typedef enum { BS_ACT_NONE = 0, BS_ACT_RELU = 1, BS_ACT_SIGMOID = 2, BS_ACT_TANH = 3 } bs_act;
+
+/* bs_spmv_fused: the whole layer of Eq. 1, Y = W·X + B, at batch 1 with an activation:
+ *   y[r] = act( (W_bs · x)[r] + bias[r] )
+ * computed in fp32 (the product exactly as bs_spmv, then + bias, then act: max(v, 0), 1/(1+e^-v) or
+ * tanh v) and rounded once to A->dt. The epilogue is fused into the SpMV kernel: the CTA's bias rows
+ * are staged in shared memory beside x, so no extra kernel or HBM pass runs.
+ *   bias  device, M elements of A->dt, or NULL (no bias);  act  a bs_act value;  flags  as bs_spmv_ex.
+ * With bias = NULL and act = BS_ACT_NONE the result is bit-identical to bs_spmv_ex.
+ * Errors: as bs_spmv_ex; BS_ERR_ARG for an unknown act; BS_ERR_UNSUPPORTED for layout SP24. */
+int bs_spmv_fused(const bs_matrix* A, const void* x, const void* bias, int act, void* y, unsigned flags,
+                  void* stream);
+
 /* bs_spmv_host: the same product with HOST x and y. The call enqueues H2D(x) -> bs_spmv -> D2H(y) on
  * `stream`, using caller-owned device scratch x_dev (K elements) and y_dev (M elements). x_host and
  * y_host should be pinned for the copies to be asynchronous. The call does not synchronise: y_host

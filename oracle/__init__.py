@@ -68,6 +68,11 @@ def lib() -> ctypes.CDLL:
         L.orc_spmm_rows.restype = ctypes.c_int
         L.orc_ideal_time.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double]
         L.orc_ideal_time.restype = ctypes.c_double
+        L.orc_act.argtypes = [ctypes.c_double, ctypes.c_int]
+        L.orc_act.restype = ctypes.c_double
+        L.orc_spmv_act.argtypes = [_vp, _vp, ctypes.c_int, _c_i64, _c_i64, ctypes.c_int, ctypes.c_int, _vp, _vp,
+                                   ctypes.c_int, _vp, _vp]
+        L.orc_spmv_act.restype = ctypes.c_int
         L.orc_elem.argtypes = [_vp, ctypes.c_int, _c_i64]
         L.orc_elem.restype = ctypes.c_double
         _lib = L
@@ -153,6 +158,31 @@ def spmv(vals, idx, dt, M, K, block, k, x, rows=None):
     bound = np.zeros(n, dtype=np.float64)
     if lib().orc_spmv_rows(_ptr(vals), _ptr(idx), dt, M, K, block, k, _ptr(x), rp, n, _ptr(y), _ptr(bound)) != 0:
         raise ValueError("orc_spmv_rows rejected the arguments")
+    return y, bound
+
+
+ACT = {"none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}
+
+
+def act(v: float, name: str) -> float:
+    """The epilogue activation in fp64, from its definition (orc_act)."""
+    return lib().orc_act(float(v), ACT[name])
+
+
+def spmv_act(vals, idx, dt, M, K, block, k, x, bias, act_name):
+    """fp64 y = act(W_bs·x + bias) (Eq. 1 with its +B, and an activation) and the tolerance scale
+    sum|w||x| + |bias|. bias may be None."""
+    vals = _check(vals, dt)
+    x = _check(x, dt)
+    idx = np.ascontiguousarray(idx, dtype=np.uint16)
+    bp = None
+    if bias is not None:
+        bias = _check(bias, dt)
+        bp = _ptr(bias)
+    y = np.zeros(M, dtype=np.float64)
+    bound = np.zeros(M, dtype=np.float64)
+    if lib().orc_spmv_act(_ptr(vals), _ptr(idx), dt, M, K, block, k, _ptr(x), bp, ACT[act_name], _ptr(y), _ptr(bound)) != 0:
+        raise ValueError("orc_spmv_act rejected the arguments")
     return y, bound
 
 

@@ -17,7 +17,8 @@
  *     NaN ranks above +Inf with all NaNs equal (A17).
  *   - k = lround((1 - s) * B).
  *   - The FC layer Y = W·X + B with B = 0 (Eq. 1), summed in fp64:
- *     y_r = sum_c W_bs[r][c] * x_c.
+ *     y_r = sum_c W_bs[r][c] * x_c. With its bias (Eq. 1's +B) and an activation for the fused layer
+ *     epilogue: y_r = act(sum + b_r), act = ReLU, logistic sigmoid or tanh.
  *   - The SPMV/SPMM/SP24 byte layouts, written from docs/layout.md (not from kernel code).
  *
  * Half-precision decoding is written out from the IEEE 754 binary16 and bfloat16 definitions.
@@ -390,6 +391,38 @@ int orc_spmm_rows(const void* vals, const uint16_t* idx, int dt, int64_t M, int6
     if (orc_spmv_rows(vals, idx, dt, M, K, B, k, xn, rows, nrows, Y + n * nrows,
                       bound ? bound + n * nrows : NULL))
       return -1;
+  }
+  return 0;
+}
+
+/* The activations of the layer epilogue, from their definitions: ReLU max(v, 0), the logistic
+ * sigmoid 1 / (1 + e^-v), and tanh v = (e^v - e^-v) / (e^v + e^-v) (written out, not libm's tanh). */
+double orc_act(double v, int act) {
+  switch (act) {
+    case 0: return v;
+    case 1: return v > 0.0 ? v : 0.0;
+    case 2: return 1.0 / (1.0 + exp(-v));
+    case 3: {
+      if (v > 20.0) return 1.0;  /* |tanh v - 1| < 1e-17 beyond 20: avoids inf/inf */
+      if (v < -20.0) return -1.0;
+      double e = exp(v), f = exp(-v);
+      return (e - f) / (e + f);
+    }
+    default: return NAN;
+  }
+}
+
+/* The whole layer of Eq. 1 at batch 1 with an activation: y[r] = act(sum + bias[r]), fp64.
+ * bias: M elements of dt, or NULL. bound[r] = sum |w||x| + |bias[r]| (the tolerance scale of O-7
+ * extended by the bias term; act is 1-Lipschitz for all three activations). */
+int orc_spmv_act(const void* vals, const uint16_t* idx, int dt, int64_t M, int64_t K, int B, int k,
+                 const void* x, const void* bias, int act, double* y, double* bound) {
+  if (act < 0 || act > 3) return -1;
+  if (orc_spmv_rows(vals, idx, dt, M, K, B, k, x, NULL, M, y, bound)) return -1;
+  for (int64_t r = 0; r < M; ++r) {
+    double b = bias ? orc_elem(bias, dt, r) : 0.0;
+    y[r] = orc_act(y[r] + b, act);
+    if (bound) bound[r] += fabs(b);
   }
   return 0;
 }

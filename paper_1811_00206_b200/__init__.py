@@ -26,7 +26,8 @@ DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 LAYOUTS = {"spmv": 1, "spmm": 2, "sp24": 3}
 
 EXPORTS = ("bs_k_from_sparsity", "bs_packed_bytes", "bs_status_str", "bs_version", "bs_prune", "bs_prune_k",
-           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_host", "bs_spmm")
+           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm")
+ACTS = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}  # bs_act (include/bs.h)
 SPMV_PDL, SPMV_W_STATIC = 1, 2  # bs_spmv_ex flags (include/bs.h)
 
 
@@ -61,9 +62,10 @@ def _load() -> ctypes.CDLL:
     L.bs_unpack.argtypes = [vp, i64, i64, ci, ci, ci, ci, vp, vp, vp]
     L.bs_spmv.argtypes = [ctypes.POINTER(_Matrix), vp, vp, vp]
     L.bs_spmv_ex.argtypes = [ctypes.POINTER(_Matrix), vp, vp, ctypes.c_uint, vp]
+    L.bs_spmv_fused.argtypes = [ctypes.POINTER(_Matrix), vp, vp, ci, vp, ctypes.c_uint, vp]
     L.bs_spmv_host.argtypes = [ctypes.POINTER(_Matrix), vp, vp, vp, vp, vp]
     L.bs_spmm.argtypes = [ctypes.POINTER(_Matrix), vp, i64, i64, vp, i64, vp]
-    for f in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_host", "bs_spmm"):
+    for f in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm"):
         getattr(L, f).restype = ci
     return L
 
@@ -195,9 +197,12 @@ def unpack(A: BSMatrix):
     return vals, idx
 
 
-def spmv(A: BSMatrix, x: torch.Tensor, out: torch.Tensor | None = None, flags: int | None = None) -> torch.Tensor:
+def spmv(A: BSMatrix, x: torch.Tensor, out: torch.Tensor | None = None, flags: int | None = None,
+         bias: torch.Tensor | None = None, act: str | None = None) -> torch.Tensor:
     """y = W_bs·x (Eq. 1 with B = 0). x: [K] of A.dtype; returns y: [M].
-    flags: None -> bs_spmv (PDL launch); otherwise bs_spmv_ex with SPMV_PDL / SPMV_W_STATIC bits."""
+    flags: None -> bs_spmv (PDL launch); otherwise bs_spmv_ex with SPMV_PDL / SPMV_W_STATIC bits.
+    bias ([M] of A.dtype) and act ("relu" | "sigmoid" | "tanh") select the fused layer epilogue
+    y = act(W_bs·x + bias) (bs_spmv_fused, Eq. 1 with its +B)."""
     _need_cuda(x)
     if x.dtype != A.dtype or x.numel() != A.K:
         raise ValueError("x must have A.K elements of A.dtype")
@@ -205,12 +210,28 @@ def spmv(A: BSMatrix, x: torch.Tensor, out: torch.Tensor | None = None, flags: i
     y = out if out is not None else torch.empty(A.M, dtype=A.dtype, device=x.device)
     m = A.cstruct()
     with torch.cuda.device(x.device):
-        if flags is None:
+        if bias is not None or act is not None:
+            if act not in ACTS:
+                raise ValueError(f"act must be one of {sorted(k for k in ACTS if k)}")
+            if bias is not None:
+                _need_cuda(bias)
+                if bias.dtype != A.dtype or bias.numel() != A.M:
+                    raise ValueError("bias must have A.M elements of A.dtype")
+                bias = bias.contiguous()
+            st = _lib.bs_spmv_fused(ctypes.byref(m), x.data_ptr(), bias.data_ptr() if bias is not None else None,
+                                    ACTS[act], y.data_ptr(), bs_flags_default() if flags is None else flags,
+                                    _stream(x.device))
+        elif flags is None:
             st = _lib.bs_spmv(ctypes.byref(m), x.data_ptr(), y.data_ptr(), _stream(x.device))
         else:
             st = _lib.bs_spmv_ex(ctypes.byref(m), x.data_ptr(), y.data_ptr(), flags, _stream(x.device))
     _check(st, "bs_spmv")
     return y
+
+
+def bs_flags_default() -> int:
+    """The launch flags bs_spmv uses (PDL)."""
+    return SPMV_PDL
 
 
 def spmv_host(A: BSMatrix, x_host: torch.Tensor, y_host: torch.Tensor, x_dev: torch.Tensor, y_dev: torch.Tensor):

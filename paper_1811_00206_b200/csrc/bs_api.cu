@@ -148,6 +148,19 @@ int bs_spmv_ex(const bs_matrix* A, const void* x, void* y, unsigned flags, void*
   return from_cuda(bsk_launch_spmv(g, A->packed, x, y, flags, (cudaStream_t)stream));
 }
 
+int bs_spmv_fused(const bs_matrix* A, const void* x, const void* bias, int act, void* y, unsigned flags,
+                  void* stream) {
+  if (!bias && act == BS_ACT_NONE) return bs_spmv_ex(A, x, y, flags, stream);
+  bsk::Geom g;
+  int st = matrix_geom(A, &g);
+  if (st) return st;
+  if (!x || !y) return BS_ERR_ARG;
+  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC)) return BS_ERR_ARG;
+  if (act < BS_ACT_NONE || act > BS_ACT_TANH) return BS_ERR_ARG;
+  if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;
+  return from_cuda(bsk_launch_spmv(g, A->packed, x, y, flags, (cudaStream_t)stream, bias, act));
+}
+
 int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream) {
   return bs_spmv_ex(A, x, y, BS_SPMV_PDL, stream);
 }

@@ -107,7 +107,7 @@ cudaError_t bsk_launch_pack(const void* vals, const uint16_t* idx, const bsk::Ge
 cudaError_t bsk_launch_unpack(const void* packed, const bsk::Geom& g, void* vals, uint16_t* idx,
                               cudaStream_t s);
 cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, unsigned flags,
-                            cudaStream_t s);
+                            cudaStream_t s, const void* bias = nullptr, int act = 0);
 cudaError_t bsk_launch_spmv_batch(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,
                                   void* Y, int64_t ldy, cudaStream_t s);
 cudaError_t bsk_launch_sp24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,

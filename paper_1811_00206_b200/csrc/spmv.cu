@@ -17,8 +17,12 @@ cudaError_t bsk_spmv_dispatch_f32(const bsk::Geom& g, const SpmvArgs& a, cudaStr
 // every width use chunk_nv = 8, so a column's fp32 summation order does not depend on the pass width
 // (NV = 2, 4, 8 accumulate each column in the same order), i.e. on N.
 static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const void* x, int64_t ldx, void* y,
-                                  int64_t ldy, int ncols, int nv, int chunk_nv, unsigned flags, cudaStream_t s) {
+                                  int64_t ldy, int ncols, int nv, int chunk_nv, unsigned flags, cudaStream_t s,
+                                  const void* bias = nullptr, int act = 0) {
   SpmvArgs a;
+  a.bias = nv == 1 ? bias : nullptr;
+  a.act = nv == 1 ? act : 0;
+  a.bias_off = 0;
   a.pdl = (flags & BS_SPMV_PDL) != 0;
   a.w_early = a.pdl && (flags & BS_SPMV_W_STATIC) != 0;
   const uint8_t* base = (const uint8_t*)packed;
@@ -82,8 +86,8 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
 }
 
 cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, unsigned flags,
-                            cudaStream_t s) {
-  return launch_spmv_nv(g, packed, x, 0, y, 0, 1, 1, 1, flags, s);
+                            cudaStream_t s, const void* bias, int act) {
+  return launch_spmv_nv(g, packed, x, 0, y, 0, 1, 1, 1, flags, s, bias, act);
 }
 
 // Batched product on the SPMV layout (16-bit): passes of up to 8 batch columns, each one stream of W;

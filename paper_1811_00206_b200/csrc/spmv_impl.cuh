@@ -79,7 +79,20 @@ struct SpmvArgs {
   int ncols;         // valid batch columns in this pass (NV > 1)
   int w_early;       // PDL: W may be streamed before griddepcontrol.wait (BS_SPMV_W_STATIC)
   int pdl;           // host: launch with programmatic stream serialization (BS_SPMV_PDL)
+  const void* bias;  // NV = 1: optional per-row bias (M elements of D), Eq. 1's +B
+  int act;           // NV = 1: bs_act applied after the bias (BS_ACT_NONE = 0)
+  uint32_t bias_off; // shared-memory byte offset of the CTA's bias rows (fp32)
 };
+
+// Layer epilogue y = act(W·x + b) in fp32 before the single rounding to D (bs_spmv_fused).
+__device__ __forceinline__ float apply_act(float v, int act) {
+  switch (act) {
+    case BS_ACT_RELU: return fmaxf(v, 0.f);
+    case BS_ACT_SIGMOID: return 1.f / (1.f + expf(-v));
+    case BS_ACT_TANH: return tanhf(v);
+    default: return v;
+  }
+}
 
 // Programmatic dependent launch (PDL). launch_dependents lets the next kernel on the stream be
 // scheduled while this one runs; wait blocks until the previous kernel has completed and its writes
@@ -342,11 +355,17 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   const int64_t nrows = rb + (warp + 1) * nr / nw - wr0;
   const int64_t S = a.NBf * a.k;  // full-panel steps per row
   const int NS = a.NS;
-  const uint32_t sx = (uint32_t)__cvta_generic_to_shared(smem);
+  // XALIGN (5-bit runs): the x slots start on a 4 KB boundary, so a gather address is
+  // panel_base | (o << 7) (the panel base has bits 7..11 clear) plus an immediate: one LOP3 instead of
+  // LOP3 + IADD per nonzero. The host reserves the 4 KB of slack.
+  constexpr bool XALIGN = IS == 5 && NV == 1;
+  const uint32_t sx0 = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t xoff = XALIGN ? ((sx0 + 4095u) & ~4095u) - sx0 : 0u;
+  const uint32_t sx = sx0 + xoff;
   const uint32_t ring = sx + a.xbytes + (uint32_t)(warp * NS) * SB;
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[warp][0]);
   BS_MARK(0);
-  float* part = (float*)(smem + a.xbytes + (size_t)nw * NS * SB) - rb * NV;  // fp32 partials [row][NV] (MULTI)
+  float* part = (float*)(smem + xoff + a.xbytes + (size_t)nw * NS * SB) - rb * NV;  // fp32 partials [row][NV] (MULTI)
   const int64_t kT = (int64_t)a.k * a.T;  // entries of one row's tail
   // A tail stage holds R rows: the value run (from the 16-byte-aligned address at or below it, offset
   // dv), then, at the next 16-byte boundary, the index run (offset di).
@@ -464,8 +483,40 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
       return (lane & ((32 >> LOGNV) - 1)) == 0;
     }
   };
+  // the CTA's bias rows are staged into shared memory with the first x staging (their loads go out
+  // before the x loads and land while x is staged), so the epilogue adds no global round trip
+  const bool has_bias = NV == 1 && a.bias != nullptr;
+  float* sbias = (float*)(smem + xoff + a.bias_off);
+  // each thread prefetches up to 4 bias rows into registers before the x loads; stored after them
+  float bp0 = 0.f, bp1 = 0.f, bp2 = 0.f, bp3 = 0.f;
+  bool bias_done = false;
+  auto bias_ld = [&](uint32_t i) { return bsk::to_float<DT>(__ldg((const raw_t*)a.bias + rb + i)); };
+  auto bias_issue = [&]() {
+    if (has_bias && !bias_done) {
+      const uint32_t i = threadIdx.x;
+      if (i < nr) bp0 = bias_ld(i);
+      if (i + NT < nr) bp1 = bias_ld(i + NT);
+      if (i + 2 * NT < nr) bp2 = bias_ld(i + 2 * NT);
+      if (i + 3 * NT < nr) bp3 = bias_ld(i + 3 * NT);
+    }
+  };
+  auto bias_store = [&]() {
+    if (has_bias && !bias_done) {
+      const uint32_t i = threadIdx.x;
+      if (i < nr) sbias[i] = bp0;
+      if (i + NT < nr) sbias[i + NT] = bp1;
+      if (i + 2 * NT < nr) sbias[i + 2 * NT] = bp2;
+      if (i + 3 * NT < nr) sbias[i + 3 * NT] = bp3;
+      for (uint32_t j = i + 4 * NT; j < nr; j += NT) sbias[j] = bias_ld(j);
+    }
+    bias_done = true;
+  };
   auto store_y = [&](int64_t r, int col, float y) {
-    if (NV == 1) ((raw_t*)a.y)[r] = (raw_t)bsk::from_float<DT>(y);
+    if (NV == 1) {
+      if (has_bias) y += sbias[r - rb];
+      if (a.act) y = apply_act(y, a.act);
+      ((raw_t*)a.y)[r] = (raw_t)bsk::from_float<DT>(y);
+    }
     else if (col < a.ncols) ((raw_t*)a.y)[col * a.ldy + r] = (raw_t)bsk::from_float<DT>(y);
   };
 
@@ -486,8 +537,10 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
     const int64_t npc = (a.NBf - (int64_t)c * a.PC) < a.PC ? (a.NBf - (int64_t)c * a.PC) : a.PC;
     const int64_t g1 = last && a.tail_in_last ? (a.NB + 31) / 32 : g0 + npc * V;
     if (c > 0) __syncthreads();  // all warps are done with the previous chunk's x
+    if (c == 0) bias_issue();
     if constexpr (NV == 1) stage_x<ES, BT, PAIR>(a, sx, g0, g1, arm_once);
     else stage_xn<NV, BT>(a, sx, g0, g1, arm_once);
+    if (c == 0) bias_store();
     if (c == 0) BS_MARK(6);
     __syncthreads();
     if (c == 0) BS_MARK(2);
@@ -523,12 +576,23 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
           else iv[0] = lds_u8(ai);
 #pragma unroll
           for (int v = 0; v < V; ++v) {
-            uint32_t o;
-            if constexpr (IS == 5) o = (v < 7 ? __funnelshift_r(iv[0], iv[1], 5 * v) : iv[1] >> 3) & 31u;
-            else if constexpr (IS == 1) o = byte_of(iv[v >> 2], v & 3);
-            else o = (iv[v >> 1] >> (16 * (v & 1))) & 0xffffu;
             const uint32_t w = ES == 2 ? (wv[v >> 1] >> (16 * (v & 1))) & 0xffffu : wv[v];
-            gather_fma(pb, o, v, w);
+            if constexpr (XALIGN) {
+              // o << 7 straight out of the 40-bit field (o = bits 5v..5v+4), OR-ed into the panel base
+              uint32_t o7;
+              if (v == 0) o7 = iv[0] << 7;
+              else if (v == 1) o7 = iv[0] << 2;
+              else if (v == 7) o7 = iv[1] << 4;
+              else o7 = __funnelshift_r(iv[0], iv[1], 5 * v - 7);
+              const uint32_t ad = (pb | (o7 & 0xF80u)) + (uint32_t)(v >> 1) * 2u * GSW + (uint32_t)(v & 1) * 2u;
+              bsk::fma_acc<DT>(acc[v], w, lds_x<DT>(ad));
+            } else {
+              uint32_t o;
+              if constexpr (IS == 5) o = (v < 7 ? __funnelshift_r(iv[0], iv[1], 5 * v) : iv[1] >> 3) & 31u;
+              else if constexpr (IS == 1) o = byte_of(iv[v >> 2], v & 3);
+              else o = (iv[v >> 1] >> (16 * (v & 1))) & 0xffffu;
+              gather_fma(pb, o, v, w);
+            }
           }
           if (++t == k) {
             t = 0;
@@ -566,8 +630,10 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
       tbase = sx + (uint32_t)(gt0 - (int64_t)(a.nchunks - 1) * a.PC * V) * GSW;
     } else {
       __syncthreads();
+      bias_issue();
       if constexpr (NV == 1) stage_x<ES, BT, PAIR>(a, sx, gt0, gt1, arm_once);
       else stage_xn<NV, BT>(a, sx, gt0, gt1, arm_once);
+      bias_store();
       __syncthreads();
       tbase = sx;
     }
@@ -619,7 +685,12 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
         finish_row(wr0 + i);
       }
     }
-  } else if (S == 0) {  // k == 0: y = 0
+  } else if (S == 0) {  // k == 0: y = act(0 + b)
+    if (has_bias) {
+      bias_issue();
+      bias_store();
+      __syncthreads();
+    }
     for (int64_t i = lane; i < nrows * NV; i += 32) store_y(wr0 + i / NV, (int)(i % NV), 0.f);
   } else if (MULTI) {
     __syncwarp();
@@ -660,12 +731,15 @@ cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   const int64_t need = (a.M + (NT / 32) - 1) / (NT / 32);
   if (grid > need) grid = need;
   const int64_t scratch = MULTI ? ((a.M + grid - 1) / grid + 1) * 4 * NV : 0;
-  const int64_t avail = dp.smem_optin - static_smem - a.xbytes - scratch;
+  const int64_t bias_bytes = a.bias ? ((a.M + grid - 1) / grid + 1) * 4 : 0;
+  const int64_t xslack = (IS == 5 && NV == 1) ? 4096 : 0;  // XALIGN in the kernel
+  const int64_t avail = dp.smem_optin - static_smem - a.xbytes - scratch - bias_bytes - xslack;
   int NS = (int)(avail / ((NT / 32) * (int64_t)SB));
   if (NS > 4) NS = 4;
   if (NS < 1) return cudaErrorInvalidConfiguration;
   a.NS = NS;
-  const int64_t smem_all = a.xbytes + (int64_t)(NT / 32) * NS * SB + scratch;
+  a.bias_off = (uint32_t)(a.xbytes + (int64_t)(NT / 32) * NS * SB + scratch);
+  const int64_t smem_all = xslack + a.xbytes + (int64_t)(NT / 32) * NS * SB + scratch + bias_bytes;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(NT);

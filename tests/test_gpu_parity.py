@@ -181,6 +181,53 @@ def test_spmv_launch_modes_and_dependencies(bs):
         bs.spmv(mats[0], x0, flags=4)
 
 
+@pytest.mark.parametrize("act", ["none", "relu", "sigmoid", "tanh"])
+@pytest.mark.parametrize("M,K,dname", [(300, 25088, "f16"), (257, 3008, "bf16"), (130, 4096, "f32"), (64, 64, "f32")])
+def test_spmv_fused_epilogue(bs, M, K, dname, act):
+    """bs_spmv_fused: y = act(W_bs·x + bias) against the fp64 oracle (Eq. 1 with its +B). Tolerance: the
+    north-star tau times (sum|w||x| + |bias|) (every activation is 1-Lipschitz), plus one unit in the last
+    place of D for the final rounding of a value that the bound does not scale (e.g. sigmoid(0) = 0.5)."""
+    B = 32 if K % 32 == 0 and K > 64 else 16
+    k = 3 if B == 32 else 8
+    W = synth.matrix(M, K, dname, seed=synth.seed_for(8, M + K))
+    vals, idx, ov, oi = _prune_parity(bs, W, dname, B, k)
+    A = bs.pack(vals, idx, K, B)
+    x = synth.vector(K, dname, seed=synth.seed_for(8, 1))
+    bias = synth.vector(M, dname, seed=synth.seed_for(8, 2))
+    y = bs.spmv(A, x.cuda(), bias=bias.cuda(), act=act)
+    yr, bound = oracle.spmv_act(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(x), synth.to_numpy(bias), act)
+    ulp = {"f32": 2.0 ** -23, "f16": 2.0 ** -10, "bf16": 2.0 ** -7}[dname]
+    err = np.abs(oracle.to_double(synth.to_numpy(y), DT[dname]) - yr)
+    tol = oracle.TAU[DT[dname]] * bound + ulp * np.abs(yr) + 1e-6
+    assert np.all(err <= tol), f"worst err/tol {float(np.max(err / tol)):.3g}"
+    if act == "relu":
+        assert (synth.to_numpy(y).astype(np.float32) >= 0).all()
+    # no bias, no activation: bit-identical to bs_spmv; bias only: the same as act = none
+    y0 = bs.spmv(A, x.cuda())
+    y1 = bs.spmv(A, x.cuda(), act="none")
+    assert torch.equal(y0, y1)
+
+
+def test_spmv_fused_k0_and_errors(bs):
+    """k = 0: W_bs = 0, so y = act(bias); SP24 has no fused epilogue; unknown activations are rejected."""
+    M, K, B = 100, 640, 32
+    W = synth.matrix(M, K, "f16", seed=71).cuda()
+    v, i, _ = bs.prune(W, B, k=0)
+    A = bs.pack(v, i, K, B)
+    x = synth.vector(K, "f16", seed=72).cuda()
+    bias = synth.vector(M, "f16", seed=73).cuda()
+    y = bs.spmv(A, x, bias=bias, act="tanh")
+    ref = torch.tanh(bias.float())
+    assert torch.allclose(y.float(), ref, atol=2e-3, rtol=0)
+    W4 = synth.matrix(64, 256, "f16", seed=74).cuda()
+    v4, i4, _ = bs.prune(W4, 4, k=2)
+    A4 = bs.pack(v4, i4, 256, 4, layout="sp24")
+    with pytest.raises(bs.BSError):
+        bs.spmv(A4, synth.vector(256, "f16", seed=75).cuda(), act="relu")
+    with pytest.raises(ValueError):
+        bs.spmv(A, x, act="gelu")
+
+
 @pytest.mark.parametrize("N", [1, 2, 3, 8, 13, 32, 64])
 @pytest.mark.parametrize("dname", ["f16", "bf16", "f32"])
 def test_spmm_small(bs, N, dname):

@@ -516,3 +516,44 @@ def test_ideal_time_S531():
     g = _gold("spec_examples.json")["ideal_time_S531"]
     assert oracle.ideal_time(g["d_time"], g["o_time"], g["sparsity"]) == pytest.approx(g["i_time"], abs=1e-12)
     assert oracle.ideal_time(50.0, 10.0, 0.0) == 50.0  # s = 0 -> dense time
+
+
+# ------------------------------------------------------------------ layer epilogue (Eq. 1's +B, NEXT-2)
+
+def test_act_closed_forms():
+    """The activations at points where they have exact closed forms: sigmoid(0) = 1/2, sigmoid(ln 3) = 3/4,
+    tanh(ln 2) = 3/5, tanh(-ln 3) = -4/5, ReLU on both signs; tanh is odd; sigmoid(v) + sigmoid(-v) = 1."""
+    import math
+    assert oracle.act(0.0, "sigmoid") == 0.5
+    assert abs(oracle.act(math.log(3.0), "sigmoid") - 0.75) < 1e-15
+    assert abs(oracle.act(math.log(2.0), "tanh") - 0.6) < 1e-15
+    assert abs(oracle.act(-math.log(3.0), "tanh") + 0.8) < 1e-15
+    assert oracle.act(-2.5, "relu") == 0.0 and oracle.act(2.5, "relu") == 2.5 and oracle.act(0.0, "relu") == 0.0
+    assert oracle.act(-7.25, "none") == -7.25
+    for v in (0.1, 1.7, 5.0, 30.0):
+        assert oracle.act(-v, "tanh") == -oracle.act(v, "tanh")
+        assert abs(oracle.act(v, "sigmoid") + oracle.act(-v, "sigmoid") - 1.0) < 1e-15
+    assert oracle.act(40.0, "tanh") == 1.0 and oracle.act(-40.0, "tanh") == -1.0
+
+
+def test_spmv_act_structure():
+    """act = none with a bias is the plain SpMV plus the bias; ReLU is the positive part of that; with
+    x = 0 the layer output is act(bias) for every activation; bound grows by |bias|."""
+    M, K, B, k = 24, 512, 32, 3
+    W = synth.to_numpy(synth.matrix(M, K, "f32", seed=61))
+    vals, idx = oracle.prune(W, oracle.F32, B, k)
+    x = synth.to_numpy(synth.vector(K, "f32", seed=62))
+    bias = synth.to_numpy(synth.vector(M, "f32", seed=63))
+    y0, b0 = oracle.spmv(vals, idx, oracle.F32, M, K, B, k, x)
+    y1, b1 = oracle.spmv_act(vals, idx, oracle.F32, M, K, B, k, x, bias, "none")
+    np.testing.assert_array_equal(y1, y0 + bias.astype(np.float64))
+    np.testing.assert_array_equal(b1, b0 + np.abs(bias.astype(np.float64)))
+    yr, _ = oracle.spmv_act(vals, idx, oracle.F32, M, K, B, k, x, bias, "relu")
+    np.testing.assert_array_equal(yr, np.maximum(y1, 0.0))
+    assert (yr == 0).any() and (yr > 0).any()
+    yn, _ = oracle.spmv_act(vals, idx, oracle.F32, M, K, B, k, x, None, "none")
+    np.testing.assert_array_equal(yn, y0)
+    z = np.zeros(K, dtype=np.float32)
+    for name in ("relu", "sigmoid", "tanh"):
+        yz, _ = oracle.spmv_act(vals, idx, oracle.F32, M, K, B, k, z, bias, name)
+        np.testing.assert_array_equal(yz, [oracle.act(float(b), name) for b in bias.astype(np.float64)])
