@@ -309,19 +309,43 @@ def main():
             layer.local = mats[i % C]
             out = layer.forward(xd, y_local_buf=y_loc, y_full_buf=y_full)
             yh.copy_(out, non_blocking=True)
+        for i in range(3):
+            e2e_step(i)
+        e2e_ms = time_loop(e2e_step, max(10, a.steps // 4), stream)
     else:
+        # two streams, each with its own pinned host x/y and device x/y: step i's H2D(x) and D2H(y) overlap
+        # the neighbouring steps' kernels (a serving pipeline); every step still moves its own bytes
+        streams = [stream, torch.cuda.Stream(device=dev)]
+        xhs = [xh, xh.clone().pin_memory()]
+        yhs = [yh, torch.empty_like(yh).pin_memory()]
+        xds = [xd, torch.empty_like(xd)]
+        yds = [y_loc, torch.empty_like(y_loc)]
+
         def e2e_step(i):
-            bs.spmv_host(mats[i % C], xh, yh, xd, y_loc)
-    for i in range(3):
-        e2e_step(i)
-    e2e_ms = time_loop(e2e_step, max(10, a.steps // 4), stream)
+            j = i & 1
+            with torch.cuda.stream(streams[j]):
+                bs.spmv_host(mats[i % C], xhs[j], yhs[j], xds[j], yds[j])
+        for i in range(4):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        n_e2e = max(10, a.steps // 4)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(streams[0])
+        streams[1].wait_event(ev0)
+        for i in range(n_e2e):
+            e2e_step(i)
+        streams[0].wait_stream(streams[1])
+        ev1.record(streams[0])
+        torch.cuda.synchronize()
+        e2e_ms = ev0.elapsed_time(ev1) / n_e2e
     if world > 1:
         tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt[0])
     e2e = {"value": round(bytes_job / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(e2e_ms, 4),
            "h2d_bytes_per_step": K * es, "d2h_bytes_per_step": (M if world > 1 else Ml) * es,
-           "path": "bs_spmv_host (C ABI, pinned host buffers)" if world == 1 else "RowShardedBS + host copies"}
+           "path": "bs_spmv_host (C ABI, pinned host buffers), steps alternating over 2 streams" if world == 1
+                   else "RowShardedBS + host copies"}
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps,
