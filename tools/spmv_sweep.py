@@ -22,6 +22,9 @@ def child():
     import torch
     import paper_1811_00206_b200 as bs
     import synth
+    if os.environ.get("BS_LIB"):  # A/B runs against another build of the same ABI
+        bs.LIB_PATH = os.environ["BS_LIB"]
+        bs._lib = bs._load()
     dev = torch.device("cuda", 0)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     shapes = [s for s in SHAPES if s[0] in os.environ.get("SHAPES", "big,fc6,fc7,ptb,ctc_ih,ctc_hh").split(",")]
@@ -60,7 +63,7 @@ def child():
             pk = A.nbytes + K * 2 + M * 2
             print(json.dumps({
                               "shape": name, "s": s, "us": round(us, 2), "GBps": round(pk / us / 1e3, 1),
-                              "copies": C, "flags": FLAGS}), flush=True)
+                              "copies": C, "flags": FLAGS, "lib": os.path.basename(os.environ.get("BS_LIB", "libbs.so"))}), flush=True)
             del mats, A
 
 
