@@ -379,6 +379,56 @@ def test_big_65536_sampled_rows(bs):
     assert ok, worst
 
 
+def test_big_fused_epilogue_sampled_rows(bs):
+    """The fused layer at scale: 320000 x 4096 (2163 rows per CTA, more than the 4 bias rows per thread the
+    kernel prefetches in registers), bias + ReLU, W_STATIC launch; checked on sampled rows against the
+    oracle's SpMV plus the bias and the activation from their definitions."""
+    M, K, B, k = 320000, 4096, 32, 3
+    W = synth.matrix(M, K, "bf16", seed=synth.seed_for(7, 0), device="cuda")
+    x = synth.vector(K, "bf16", seed=synth.seed_for(7, 1), device="cuda")
+    b = synth.vector(M, "bf16", seed=synth.seed_for(7, 2), device="cuda")
+    vals, idx, _ = bs.prune(W, B, k=k)
+    A = bs.pack(vals, idx, K, B)
+    y = bs.spmv(A, x, bias=b, act="relu", flags=bs.SPMV_PDL | bs.SPMV_W_STATIC)
+    rng = np.random.default_rng(2)
+    rows = np.unique(np.concatenate([rng.choice(M, 1500, replace=False), [0, 2162, 2163, 2164, M - 1]]))
+    rt = torch.from_numpy(rows).cuda()
+    ov, oi = oracle.prune(synth.to_numpy(W[rt]), oracle.BF16, B, k)
+    s_, bound = oracle.spmv_rowslice(ov, oi, oracle.BF16, K, B, k, synth.to_numpy(x))
+    bb = oracle.to_double(synth.to_numpy(b[rt]), oracle.BF16)
+    yr = np.array([oracle.act(v, "relu") for v in s_ + bb])
+    err = np.abs(oracle.to_double(synth.to_numpy(y[rt]), oracle.BF16) - yr)
+    assert np.all(err <= 1e-2 * (bound + np.abs(bb)) + 2.0 ** -7 * np.abs(yr) + 1e-6)
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_shapes(bs, case):
+    """Seeded random shapes across the parameter space (M, K = NB·B, B, k, dtype, family): prune masks and
+    packed bytes bit-exact, SpMV and a small-batch SpMM within the north-star tolerance."""
+    rng = np.random.default_rng(1000 + case)
+    B = int(rng.choice([2, 4, 8, 16, 20, 25, 32, 64, 100, 300]))
+    NB = int(rng.integers(1, 600)) if B <= 64 else int(rng.integers(1, 40))
+    K, M = NB * B, int(rng.integers(1, 700))
+    k = int(rng.integers(0, B + 1)) if case % 4 == 0 else int(rng.integers(1, max(2, B // 4 + 1)))
+    dname = ["f16", "bf16", "f32"][case % 3]
+    family = ["gaussian", "ties", "sameoffset"][case % 3 if B <= 64 else 0]
+    W = synth.matrix(M, K, dname, family=family, seed=synth.seed_for(6, case), B=B)
+    vals, idx, ov, oi = _prune_parity(bs, W, dname, B, k)
+    A = bs.pack(vals, idx, K, B)
+    np.testing.assert_array_equal(A.packed.cpu().numpy(), oracle.pack(ov, oi, M, K, B, k, DT[dname], oracle.SPMV))
+    x = synth.vector(K, dname, seed=synth.seed_for(6, 100 + case))
+    y = bs.spmv(A, x.cuda())
+    yr, bound = oracle.spmv(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(x))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(y), DT[dname]), yr, bound, oracle.TAU[DT[dname]])
+    assert ok, f"spmv worst {worst}"
+    N = int(rng.integers(2, 12))
+    X = synth.vector(K, dname, seed=synth.seed_for(6, 200 + case), n=N)
+    Y = bs.spmm(A, X.cuda())
+    Yr, Yb = oracle.spmm(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(X))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y), DT[dname]), Yr, Yb, oracle.TAU[DT[dname]])
+    assert ok, f"spmm worst {worst}"
+
+
 # ---------------------------------------------------------------- 2:4 (B = 4, k = 2): SP24 layout
 
 @pytest.mark.parametrize("N", [1, 2, 8, 16, 64, 200])
