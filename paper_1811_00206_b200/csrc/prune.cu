@@ -175,6 +175,144 @@ __global__ void __launch_bounds__(256) prune_wide(const typename KeyOf<DT>::raw_
   }
 }
 
+// Thread per block (B in {4, 8, 16, 32}, rows 16-byte aligned): a thread loads its whole block with
+// 16-byte loads (a warp reads 32 consecutive blocks: coalesced) and selects in registers, so the
+// kernel streams W at HBM speed instead of one 2-byte load per lane per warp step (prune_narrow).
+// Selection, with keys as above and ties to the lower offset:
+//   - min(k, B - k) <= 6: k passes of "largest untaken key, first in offset order" (or B - k passes
+//     of "smallest kept key, last in offset order", removed), over a 32-bit taken mask;
+//   - otherwise the radix select of prune_narrow on the thread's B keys (kBits counting passes).
+// The kept set is the same as prune_narrow's (the top k under (key desc, offset asc)): bit-exact.
+// Block-wide copy of `bytes` from shared to global memory: 16-byte stores where both sides are 16-byte
+// aligned (the destination of a CTA step is, when vals/idx are), then the remaining bytes one by one.
+__device__ __forceinline__ void copy_out(uint8_t* dst, const uint8_t* src, int64_t bytes) {
+  int64_t head = 0;
+  if (((uintptr_t)dst & 15) == 0) {
+    const int64_t n16 = bytes / 16;
+    for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) ((uint4*)dst)[i] = ((const uint4*)src)[i];
+    head = n16 * 16;
+  }
+  for (int64_t i = head + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+
+template <int DT, int B>
+__global__ void __launch_bounds__(256) prune_thread(const typename KeyOf<DT>::raw_t* __restrict__ W,
+                                                    int64_t M, int64_t NB, int64_t ldw, int k,
+                                                    typename KeyOf<DT>::raw_t* __restrict__ vals,
+                                                    uint16_t* __restrict__ idx) {
+  using raw_t = typename KeyOf<DT>::raw_t;
+  constexpr int ES = sizeof(raw_t);
+  constexpr int NV = B * ES / 16;  // 16-byte loads per block
+  extern __shared__ __align__(16) uint8_t sm_out[];  // staged outputs: 256·k values, then 256·k indices
+  raw_t* sv = (raw_t*)sm_out;
+  uint16_t* si = (uint16_t*)(sm_out + bsk::align_up(256LL * k * ES, 16));
+  const int64_t nblocks = M * NB;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // the next block's loads are issued before the current block's selection (register double buffer)
+  auto load = [&](int64_t g, uint32_t (&w)[B * ES / 4]) {
+    const int64_t r = g / NB, b = g - r * NB;
+    const uint4* src = (const uint4*)(W + r * ldw + b * B);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const uint4 v = __ldcs(src + q);  // streamed once: do not keep W in L2
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+  };
+  uint32_t wn[B * ES / 4];
+  int64_t base = (int64_t)blockIdx.x * blockDim.x;
+  if (base + threadIdx.x < nblocks) load(base + threadIdx.x, wn);
+  for (; base < nblocks; base += stride) {  // CTA-uniform: the CTA's 256 blocks are consecutive
+    const int64_t gid = base + threadIdx.x;
+    const bool valid = gid < nblocks;
+    uint32_t w[B * ES / 4];
+#pragma unroll
+    for (int q = 0; q < B * ES / 4; ++q) w[q] = wn[q];
+    if (gid + stride < nblocks) load(gid + stride, wn);
+    uint32_t key[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const uint32_t raw = ES == 2 ? (w[j >> 1] >> (16 * (j & 1))) & 0xffffu : w[j];
+      key[j] = KeyOf<DT>::key(raw);
+    }
+    uint32_t taken = 0;
+    if (k <= 6 && ES == 2) {
+      // 16-bit keys: v_j = (key_j + 1) << 5 | (31 - j) is unique, and its maximum is the largest key,
+      // ties to the lower offset. A pass is a max tree (no serial chain); taken entries become 0.
+      uint32_t v[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) v[j] = ((key[j] + 1u) << 5) | (31u - j);
+      for (int p = 0; p < k; ++p) {
+        uint32_t m[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) m[j] = v[j];
+#pragma unroll
+        for (int h = B / 2; h > 0; h >>= 1)
+#pragma unroll
+          for (int j = 0; j < h; ++j) m[j] = max(m[j], m[j + h]);
+        taken |= 1u << (31u - (m[0] & 31u));
+#pragma unroll
+        for (int j = 0; j < B; ++j) v[j] = v[j] == m[0] ? 0u : v[j];
+      }
+    } else if (k <= 6) {
+      for (int p = 0; p < k; ++p) {
+        int best = -1, bi = 0;
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (!((taken >> j) & 1u) && (int)key[j] > best) { best = (int)key[j]; bi = j; }
+        taken |= 1u << bi;
+      }
+    } else if (B - k <= 6) {
+      uint32_t dropped = 0;
+      for (int p = 0; p < B - k; ++p) {
+        uint32_t best = 0xffffffffu;
+        int bi = 0;
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (!((dropped >> j) & 1u) && key[j] <= best) { best = key[j]; bi = j; }
+        dropped |= 1u << bi;
+      }
+      taken = ~dropped & (B == 32 ? 0xffffffffu : ((1u << B) - 1u));
+    } else {
+      uint32_t T = 0;
+#pragma unroll
+      for (int bit = KeyOf<DT>::kBits - 1; bit >= 0; --bit) {
+        const uint32_t cand = T | (1u << bit);
+        int c[4] = {0, 0, 0, 0};  // four independent counters: the count is not one serial chain
+#pragma unroll
+        for (int j = 0; j < B; ++j) c[j & 3] += key[j] >= cand;
+        if ((c[0] + c[1]) + (c[2] + c[3]) >= k) T = cand;
+      }
+      int need = k;
+#pragma unroll
+      for (int j = 0; j < B; ++j) need -= key[j] > T;
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const bool keep = key[j] > T || (key[j] == T && need > 0);
+        if (key[j] == T && need > 0) --need;
+        taken |= (uint32_t)keep << j;
+      }
+    }
+    // kept entries in offset order into shared memory, then the CTA writes its contiguous output run
+    // with 16-byte stores (per-thread stores at stride k would touch a sector per 2-byte element)
+    if (valid) {
+      int t = threadIdx.x * k;
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        if ((taken >> j) & 1u) {
+          sv[t] = (raw_t)(ES == 2 ? (w[j >> 1] >> (16 * (j & 1))) & 0xffffu : w[j]);
+          si[t] = (uint16_t)j;
+          ++t;
+        }
+      }
+    }
+    __syncthreads();
+    const int64_t nv = ((nblocks - base) < 256 ? (nblocks - base) : 256) * k;  // entries of this CTA step
+    copy_out((uint8_t*)(vals + base * k), (const uint8_t*)sv, nv * ES);
+    copy_out((uint8_t*)(idx + base * k), (const uint8_t*)si, nv * 2);
+    __syncthreads();
+  }
+}
+
 template <int DT>
 cudaError_t launch_prune_t(const void* W, int64_t M, int64_t K, int64_t ldw, int B, int k, void* vals,
                            uint16_t* idx, cudaStream_t s) {
@@ -182,6 +320,23 @@ cudaError_t launch_prune_t(const void* W, int64_t M, int64_t K, int64_t ldw, int
   const int64_t NB = K / B;
   const int threads = 256;
   const int sms = bsk::dev_props().sms;
+  const bool aligned16 = ((uintptr_t)W & 15) == 0 && (ldw * (int64_t)sizeof(raw_t)) % 16 == 0;
+  if (aligned16 && k > 0 && (B == 32 || B == 16 || B == 8 || (B == 4 && sizeof(raw_t) == 4))) {
+    int64_t blocks = (M * NB + 255) / 256;
+    blocks = blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8;
+    const size_t smem = (size_t)bsk::align_up(256LL * k * sizeof(raw_t), 16) + 256 * (size_t)k * 2;
+    auto run = [&](auto kern) {
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<(unsigned)blocks, 256, smem, s>>>((const raw_t*)W, M, NB, ldw, k, (raw_t*)vals, idx);
+    };
+    switch (B) {
+      case 32: run(prune_thread<DT, 32>); break;
+      case 16: run(prune_thread<DT, 16>); break;
+      case 8: run(prune_thread<DT, 8>); break;
+      default: if constexpr (sizeof(raw_t) == 4) run(prune_thread<DT, 4>); break;
+    }
+    return cudaGetLastError();
+  }
   if (B <= 32) {
     const int nseg = 32 / B;
     const int64_t warps_needed = (M * NB + nseg - 1) / nseg;
