@@ -645,7 +645,36 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
     };
     // one row's tail; ldv/ldi load entry e (position t·T + v·32 + l) of the value / index runs
     auto tail_row = [&](auto ldv, auto ldi) {
-      for (int tt = 0; tt < a.k; ++tt) {
+      int tt = 0;
+      if constexpr (NV == 1) {
+        // four entries per block at a time: their loads and gathers are issued before the FMAs (the
+        // shared-memory loads are volatile, so they are issued in program order); the FMAs into acc[v]
+        // stay in tt order, so the sum is the same as one entry at a time
+        for (; tt + 4 <= a.k; tt += 4) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const int bl = v * 32 + lane;
+            if (v < Vt && bl < a.T) {
+              uint32_t w[4], o[4], xv[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                w[u] = ldv((uint32_t)(tt + u) * (uint32_t)a.T + bl);
+                o[u] = ldi((uint32_t)(tt + u) * (uint32_t)a.T + bl);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const uint32_t base = tbase + lane * LSLB;
+                const uint32_t ad = PAIR ? base + o[u] * XROW + (uint32_t)(v >> 1) * 2u * GSW + (uint32_t)(v & 1) * 2u
+                                         : base + o[u] * ROWB + v * GSW;
+                xv[u] = lds_x<DT>(ad);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) bsk::fma_acc<DT>(acc[v], w[u], xv[u]);
+            }
+          }
+        }
+      }
+      for (; tt < a.k; ++tt) {
         const uint32_t e0 = (uint32_t)tt * (uint32_t)a.T;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
