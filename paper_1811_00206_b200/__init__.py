@@ -26,7 +26,7 @@ DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 LAYOUTS = {"spmv": 1, "spmm": 2, "sp24": 3}
 
 EXPORTS = ("bs_k_from_sparsity", "bs_packed_bytes", "bs_status_str", "bs_version", "bs_prune", "bs_prune_k",
-           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm")
+           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm", "bs_choose_layout")
 ACTS = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}  # bs_act (include/bs.h)
 SPMV_PDL, SPMV_W_STATIC = 1, 2  # bs_spmv_ex flags (include/bs.h)
 
@@ -52,6 +52,8 @@ def _load() -> ctypes.CDLL:
     L.bs_k_from_sparsity.restype = ci
     L.bs_packed_bytes.argtypes = [i64, i64, ci, ci, ci, ci]
     L.bs_packed_bytes.restype = ctypes.c_size_t
+    L.bs_choose_layout.argtypes = [i64, i64, ci, ci, ci, i64]
+    L.bs_choose_layout.restype = ci
     L.bs_status_str.argtypes = [ci]
     L.bs_status_str.restype = ctypes.c_char_p
     L.bs_version.argtypes = []
@@ -167,10 +169,22 @@ def prune(W: torch.Tensor, block: int, sparsity: float | None = None, k: int | N
     return vals, idx, k
 
 
-def pack(vals: torch.Tensor, idx: torch.Tensor, K: int, block: int, layout: str = "spmv") -> BSMatrix:
-    """Permute canonical (vals, idx) into a device layout (docs/layout.md)."""
+def choose_layout(M: int, K: int, block: int, k: int, dtype: torch.dtype, batch: int) -> str:
+    """bs_choose_layout: the layout bs_spmm runs fastest on for `batch` columns (include/bs.h)."""
+    code = _lib.bs_choose_layout(M, K, block, k, DTYPES[dtype], batch)
+    if code < 0:
+        raise ValueError("bs_choose_layout rejected the arguments")
+    return {v: n for n, v in LAYOUTS.items()}[code]
+
+
+def pack(vals: torch.Tensor, idx: torch.Tensor, K: int, block: int, layout: str = "spmv",
+         batch: int | None = None) -> BSMatrix:
+    """Permute canonical (vals, idx) into a device layout (docs/layout.md). layout="auto" takes
+    bs_choose_layout's pick for `batch` columns (default 1)."""
     _need_cuda(vals, idx)
     M, NB, k = vals.shape
+    if layout == "auto":
+        layout = choose_layout(M, K, block, k, vals.dtype, batch or 1)
     vals = vals.contiguous()
     idx = idx.contiguous()
     n = packed_bytes(M, K, block, k, vals.dtype, layout)

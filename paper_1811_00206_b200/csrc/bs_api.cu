@@ -76,6 +76,14 @@ size_t bs_packed_bytes(int64_t M, int64_t K, int block, int k, int dt, int layou
   return (size_t)g.total;
 }
 
+int bs_choose_layout(int64_t M, int64_t K, int block, int k, int dt, int64_t N) {
+  if (!valid_dt(dt) || check_shape(M, K, block, k) || N < 1) return -1;
+  const bool half = dt != BS_F32;
+  if (block == 4 && k == 2 && half && K % 128 == 0) return BS_LAYOUT_SP24;
+  if (N > 8 && half && 64 % block == 0) return BS_LAYOUT_SPMM;
+  return BS_LAYOUT_SPMV;
+}
+
 const char* bs_status_str(int status) {
   switch (status) {
     case BS_OK: return "BS_OK";

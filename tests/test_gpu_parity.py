@@ -429,6 +429,21 @@ def test_random_shapes(bs, case):
     assert ok, f"spmm worst {worst}"
 
 
+@pytest.mark.parametrize("B,k,N", [(32, 3, 1), (32, 3, 8), (32, 3, 32), (4, 2, 1), (4, 2, 48)])
+def test_spmm_auto_layout(bs, B, k, N):
+    """pack(layout="auto", batch=N) (bs_choose_layout) followed by bs_spmm, against the oracle."""
+    M, K = 300, 2048
+    W = synth.matrix(M, K, "f16", seed=synth.seed_for(9, 300 + N + B))
+    vals, idx, ov, oi = _prune_parity(bs, W, "f16", B, k)
+    A = bs.pack(vals, idx, K, B, layout="auto", batch=N)
+    assert A.layout == bs.choose_layout(M, K, B, k, torch.float16, N)
+    X = synth.vector(K, "f16", seed=synth.seed_for(9, 301), n=N)
+    Y = bs.spmm(A, X.cuda())
+    Yr, Yb = oracle.spmm(ov, oi, oracle.F16, M, K, B, k, synth.to_numpy(X))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y), oracle.F16), Yr, Yb, 1e-2)
+    assert ok, worst
+
+
 # ---------------------------------------------------------------- 2:4 (B = 4, k = 2): SP24 layout
 
 @pytest.mark.parametrize("N", [1, 2, 8, 16, 64, 200])

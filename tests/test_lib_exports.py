@@ -60,6 +60,23 @@ def test_packed_bytes_matches_oracle(bs):
                 assert bs.packed_bytes(M, K, B, k, tdt[dt], lay[L]) == oracle.packed_bytes(M, K, B, k, dt, L)
 
 
+def test_choose_layout(bs):
+    """bs_choose_layout (host helper): 2:4 shapes -> sp24; batch <= 8 -> spmv; larger 16-bit batches with
+    B | 64 -> spmm; f32 -> spmv; invalid arguments rejected."""
+    import torch
+    f16, f32 = torch.float16, torch.float32
+    assert bs.choose_layout(4096, 2048, 4, 2, f16, 1) == "sp24"
+    assert bs.choose_layout(4096, 2048, 4, 2, f16, 64) == "sp24"
+    assert bs.choose_layout(4096, 2000, 4, 2, f16, 64) == "spmm"  # K mod 128 != 0: no TMA chunking
+    for N in (1, 2, 8):
+        assert bs.choose_layout(4096, 25088, 32, 3, f16, N) == "spmv"
+    assert bs.choose_layout(4096, 25088, 32, 3, f16, 32) == "spmm"
+    assert bs.choose_layout(4096, 25088, 32, 3, f32, 32) == "spmv"
+    assert bs.choose_layout(64, 1000, 25, 8, f16, 32) == "spmv"  # 25 does not divide 64
+    with pytest.raises(ValueError):
+        bs.choose_layout(64, 1000, 32, 3, f16, 4)  # K mod B != 0
+
+
 def test_no_oracle_in_product_path():
     """The product package never imports, links or runs anything under oracle/."""
     pkg = os.path.join(ROOT, "paper_1811_00206_b200")
