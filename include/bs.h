@@ -70,8 +70,9 @@ size_t bs_packed_bytes(int64_t M, int64_t K, int block, int k, int dt, int layou
 
 /* The layout bs_spmm runs fastest on for a batch of N columns, from the round-1 measurements
  * (bench.py `spmm`): the 2:4 shape (block 4, k 2, f16/bf16, K mod 128 = 0) -> SP24
- * (sparse tensor cores for N >= 2, a CUDA-core SpMV at N = 1); otherwise N <= 8 -> SPMV (the batched
- * CUDA-core path streams W once per 8 columns) and N > 8 with f16/bf16 and block | 64 -> SPMM
+ * (sparse tensor cores for N >= 2, a CUDA-core SpMV at N = 1); otherwise N <= 8, or N <= 16 with
+ * K <= 3072, -> SPMV (the batched CUDA-core path streams W once per 8 or 16 columns) and larger
+ * batches with f16/bf16 and block | 64 -> SPMM
  * (decompressed tiles on tcgen05.mma); f32 -> SPMV. The choice depends only on the arguments, never on
  * the data, and every layout gives results within the same tolerance. Returns -1 on invalid arguments. */
 int bs_choose_layout(int64_t M, int64_t K, int block, int k, int dt, int64_t N);

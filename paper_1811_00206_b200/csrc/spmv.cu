@@ -91,16 +91,30 @@ cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* 
 }
 
 // Batched product on the SPMV layout (16-bit): passes of up to 8 batch columns, each one stream of W;
-// a pass of w columns uses x slots of NV = 2, 4 or 8 columns (the smallest >= w).
+// a pass of w columns uses x slots of NV = 2, 4 or 8 columns (the smallest >= w). When 9..16 columns
+// remain and 32-byte slots fit in shared memory (K up to about 3000 columns: the CTC layers), one pass
+// of NV = 16 streams W once for all of them. Every pass uses the K-chunking of NV = 8, so column n's
+// summation order does not depend on N.
 cudaError_t bsk_launch_spmv_batch(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,
                                   void* Y, int64_t ldy, cudaStream_t s) {
   if (g.es != 2) return cudaErrorNotSupported;
-  for (int64_t n0 = 0; n0 < N; n0 += 8) {
+  for (int64_t n0 = 0; n0 < N;) {
+    if (N - n0 > 8) {
+      const int nc = (int)((N - n0) < 16 ? (N - n0) : 16);
+      cudaError_t e = launch_spmv_nv(g, packed, (const uint16_t*)X + n0 * ldx, ldx, (uint16_t*)Y + n0 * ldy, ldy, nc,
+                                     16, 8, BS_SPMV_PDL, s);
+      if (e == cudaSuccess) {
+        n0 += nc;
+        continue;
+      }
+      if (e != cudaErrorInvalidConfiguration) return e;  // 32-byte slots do not fit: passes of 8
+    }
     const int nc = (int)((N - n0) < 8 ? (N - n0) : 8);
     const int nv = nc <= 2 ? 2 : nc <= 4 ? 4 : 8;
     cudaError_t e =
         launch_spmv_nv(g, packed, (const uint16_t*)X + n0 * ldx, ldx, (uint16_t*)Y + n0 * ldy, ldy, nc, nv, 8, BS_SPMV_PDL, s);
     if (e != cudaSuccess) return e;
+    n0 += nc;
   }
   return cudaSuccess;
 }

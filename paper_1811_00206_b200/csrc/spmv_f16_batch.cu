@@ -1,4 +1,4 @@
-// spmv_f16_batch.cu: f16 instantiations of the batched SpMV kernel (spmv_impl.cuh): NV = 2, 4, 8
+// spmv_f16_batch.cu: f16 instantiations of the batched SpMV kernel (spmv_impl.cuh): NV = 2, 4, 8, 16
 // batch columns per x slot.
 #include "spmv_impl.cuh"
 
@@ -6,6 +6,7 @@ cudaError_t bsk_spmv_dispatch_f16_batch(const bsk::Geom& g, const bsk_spmv::Spmv
   switch (nv) {
     case 2: return bsk_spmv::dispatch_is<BS_F16, 2>(g, a, s);
     case 4: return bsk_spmv::dispatch_is<BS_F16, 4>(g, a, s);
+    case 16: return bsk_spmv::dispatch_is<BS_F16, 16>(g, a, s);
     default: return bsk_spmv::dispatch_is<BS_F16, 8>(g, a, s);
   }
 }

@@ -250,7 +250,10 @@ __device__ __forceinline__ void stage_xn(const SpmvArgs& a, uint32_t sx, int64_t
             const uint32_t w = e < 2 ? (e == 0 ? v[n].x : v[n].x) : e < 4 ? v[n].y : e < 6 ? v[n].z : v[n].w;
             h[n] = (w >> (16 * (e & 1))) & 0xffffu;
           }
-          if constexpr (NV == 8) bsk::sts_v4(col + e * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+          if constexpr (NV == 16) {
+            bsk::sts_v4(col + e * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+            bsk::sts_v4(col + e * ROWB + 16, h[8] | (h[9] << 16), h[10] | (h[11] << 16), h[12] | (h[13] << 16), h[14] | (h[15] << 16));
+          } else if constexpr (NV == 8) bsk::sts_v4(col + e * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
           else if constexpr (NV == 4) asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(col + e * ROWB), "r"(h[0] | (h[1] << 16)), "r"(h[2] | (h[3] << 16)));
           else bsk::sts_u32(col + e * ROWB, h[0] | (h[1] << 16));
         }
@@ -267,7 +270,10 @@ __device__ __forceinline__ void stage_xn(const SpmvArgs& a, uint32_t sx, int64_t
         uint32_t h[NV];
 #pragma unroll
         for (int n = 0; n < NV; ++n) h[n] = n < a.ncols ? (uint32_t)__ldg((const uint16_t*)a.x + n * a.ldx + b * B + o) : 0u;
-        if constexpr (NV == 8) bsk::sts_v4(col + o * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+        if constexpr (NV == 16) {
+          bsk::sts_v4(col + o * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+          bsk::sts_v4(col + o * ROWB + 16, h[8] | (h[9] << 16), h[10] | (h[11] << 16), h[12] | (h[13] << 16), h[14] | (h[15] << 16));
+        } else if constexpr (NV == 8) bsk::sts_v4(col + o * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
         else if constexpr (NV == 4) asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(col + o * ROWB), "r"(h[0] | (h[1] << 16)), "r"(h[2] | (h[3] << 16)));
         else bsk::sts_u32(col + o * ROWB, h[0] | (h[1] << 16));
       }
@@ -459,9 +465,12 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
                                : base + o * ROWB + v * GSW;
       bsk::fma_acc<DT>(acc[v], w, lds_x<DT>(ad));
     } else {
-      uint32_t xw[4];
+      uint32_t xw[NV / 2 > 4 ? NV / 2 : 4];
       const uint32_t ad = base + o * ROWB + v * GSW;
-      if constexpr (NV == 8) bsk::lds_v4(ad, xw[0], xw[1], xw[2], xw[3]);
+      if constexpr (NV == 16) {
+        bsk::lds_v4(ad, xw[0], xw[1], xw[2], xw[3]);
+        bsk::lds_v4(ad + 16, xw[4], xw[5], xw[6], xw[7]);
+      } else if constexpr (NV == 8) bsk::lds_v4(ad, xw[0], xw[1], xw[2], xw[3]);
       else if constexpr (NV == 4) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(xw[0]), "=r"(xw[1]) : "r"(ad));
       else xw[0] = bsk::lds_u32(ad);
 #pragma unroll
@@ -469,7 +478,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
     }
   };
   // row total: SpMV -> one value (lane 0 holds it); NV > 1 -> lane l holds column l >> (5 - log2 NV)
-  constexpr int LOGNV = NV == 8 ? 3 : NV == 4 ? 2 : NV == 2 ? 1 : 0;
+  constexpr int LOGNV = NV == 16 ? 4 : NV == 8 ? 3 : NV == 4 ? 2 : NV == 2 ? 1 : 0;
   auto row_total = [&](float& tot, int& col) -> bool {
     if constexpr (NV == 1) {
       tot = warp_total<V>(acc);
@@ -765,7 +774,7 @@ cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   const int64_t avail = dp.smem_optin - static_smem - a.xbytes - scratch - bias_bytes - xslack;
   int NS = (int)(avail / ((NT / 32) * (int64_t)SB));
   if (NS > 4) NS = 4;
-  if (NS < 1) return cudaErrorInvalidConfiguration;
+  if (NS < (NV == 16 ? 2 : 1)) return cudaErrorInvalidConfiguration;  // NV = 16: the caller falls back to passes of 8
   a.NS = NS;
   a.bias_off = (uint32_t)(a.xbytes + (int64_t)(NT / 32) * NS * SB + scratch);
   const int64_t smem_all = xslack + a.xbytes + (int64_t)(NT / 32) * NS * SB + scratch + bias_bytes;

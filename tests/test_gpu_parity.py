@@ -255,6 +255,24 @@ def test_spmm_column_independence(bs):
         assert torch.equal(bs.spmm(A, X[n0:n1].contiguous()), Y64[n0:n1])
 
 
+@pytest.mark.parametrize("K,N", [(2048, 16), (1024, 13), (3008, 12), (2048, 40)])
+def test_spmm_spmv_layout_sixteen_wide(bs, K, N):
+    """Passes of 16 columns (32-byte x slots, CTC-sized K) give the same columns bit for bit as passes of
+    8 and 1, and match the oracle."""
+    M, B, k = 333, 32, 4
+    W = synth.matrix(M, K, "bf16", seed=synth.seed_for(9, 400 + K))
+    X = synth.vector(K, "bf16", seed=synth.seed_for(9, 401), n=N)
+    vals, idx, ov, oi = _prune_parity(bs, W, "bf16", B, k)
+    A = bs.pack(vals, idx, K, B, layout="spmv")
+    Xd = X.cuda()
+    Y = bs.spmm(A, Xd)
+    for n0, n1 in ((0, 8), (8, N), (N - 1, N)):
+        assert torch.equal(bs.spmm(A, Xd[n0:n1].contiguous()), Y[n0:n1]), (n0, n1)
+    Yr, bound = oracle.spmm(ov, oi, oracle.BF16, M, K, B, k, synth.to_numpy(X))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y), oracle.BF16), Yr, bound, oracle.TAU[oracle.BF16])
+    assert ok, worst
+
+
 def test_spmm_spmv_layout_pass_widths(bs):
     """SPMV-layout SpMM: passes of 1..8 columns (x slots NV = 2, 4, 8) share one K-chunking, so column
     n is bit-identical for every N (K spans several x chunks plus a tail), and matches the oracle."""
@@ -265,7 +283,7 @@ def test_spmm_spmv_layout_pass_widths(bs):
     A = bs.pack(vals, idx, K, B, layout="spmv")
     Xd = X.cuda()
     Y13 = bs.spmm(A, Xd)
-    for n0, n1 in ((0, 1), (3, 5), (5, 9), (9, 12), (12, 13)):
+    for n0, n1 in ((0, 1), (3, 5), (5, 9), (9, 12), (12, 13), (0, 8)):
         assert torch.equal(bs.spmm(A, Xd[n0:n1].contiguous()), Y13[n0:n1]), (n0, n1)
     Yr, bound = oracle.spmm(ov, oi, oracle.F16, M, K, B, k, synth.to_numpy(X))
     ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y13), oracle.F16), Yr, bound, oracle.TAU[oracle.F16])

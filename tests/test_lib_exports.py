@@ -71,6 +71,9 @@ def test_choose_layout(bs):
     for N in (1, 2, 8):
         assert bs.choose_layout(4096, 25088, 32, 3, f16, N) == "spmv"
     assert bs.choose_layout(4096, 25088, 32, 3, f16, 32) == "spmm"
+    assert bs.choose_layout(4096, 25088, 32, 3, f16, 16) == "spmm"
+    assert bs.choose_layout(4096, 2048, 32, 4, f16, 16) == "spmv"  # one 16-column pass (CTC)
+    assert bs.choose_layout(4096, 2048, 32, 4, f16, 17) == "spmm"
     assert bs.choose_layout(4096, 25088, 32, 3, f32, 32) == "spmv"
     assert bs.choose_layout(64, 1000, 25, 8, f16, 32) == "spmv"  # 25 does not divide 64
     with pytest.raises(ValueError):
