@@ -545,6 +545,7 @@ def spmm_rows(a, bs, hbm_peak, l2):
     (SPMM layout), K5 = tcgen05.mma.sp (SP24 layout)."""
     rows = []
     dev = torch.device("cuda")
+    tc_peak = tensor_peak()
     shapes = [("configs[2] VGG fc6 4096x25088", 4096, 25088, [0.9], [32]),
               ("configs[2] VGG fc7 4096x4096", 4096, 4096, [0.5, 0.9], [32]),
               ("configs[3] CTC W_ih 4096x2048", 4096, 2048, [0.875], [1, 2, 4, 8, 16, 32, 64, 128, 256]),
@@ -583,6 +584,11 @@ def spmm_rows(a, bs, hbm_peak, l2):
                     pk = mats[0].nbytes + N * (K + M) * W.element_size()
                     row[f"{kn}_us"] = round(t, 2)
                     row[f"{kn}_packed_GBps"] = round(pk / t / 1e3, 1)
+                    row[f"{kn}_hbm_frac"] = round(pk / t / 1e3 / hbm_peak, 3)
+                    if kn in ("K5", "K6"):  # tensor pipe: the MMA flops the kernel issues vs the measured peak
+                        # K6: dense MMAs on the decompressed tiles; K5: 2:4 MMAs, nominally 2x the dense rate
+                        mma = 2.0 * M * K * N / t / 1e6
+                        row[f"{kn}_tensor_frac"] = round(mma / (tc_peak * (2.0 if kn == "K5" else 1.0)), 4)
                     if best is None or t < best[1]:
                         best = (kn, t)
                 row["best"] = best[0]
@@ -592,7 +598,19 @@ def spmm_rows(a, bs, hbm_peak, l2):
             del packed, Wbs
         del W
     return {"spmm": rows, "spmm_note": "graph-timed, rotating copies (> 3x L2); TFLOPs_nnz counts 2 flops per stored "
-                                       "nonzero per batch column; packed_GBps = (packed W + X + Y) / time"}
+                                       "nonzero per batch column; packed_GBps = (packed W + X + Y) / time; hbm_frac "
+                                       "against MEASURED_PEAKS hbm_gbs; tensor_frac = issued MMA flops (K6: dense "
+                                       f"2MKN on decompressed tiles; K5: 2:4, against 2x) / the measured bf16 peak "
+                                       f"{tc_peak} TFLOP/s (sustained; f16 runs at the bf16 rate)"}
+
+
+def tensor_peak() -> float:
+    """Measured dense bf16 TFLOP/s (sustained) from MEASURED_PEAKS.json, else the guide's nominal 2250."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f).get("bf16_tflops_sustained", 2250.0))
+    return 2250.0
 
 
 def extras(a, bs, W, A, vals, idx, x, k, es, hbm_peak, stream):
