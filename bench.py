@@ -365,7 +365,8 @@ def main():
                      "packed_frac": round(packed_l / (kern_ms * 1e-3) / 1e9 / hbm_peak, 4), "peak_source": peak_src},
         "e2e": e2e,
         "gpu_launches": a.steps,
-        "legs": legs,
+        "legs": legs if world == 1 else dict(legs, spmv_ms=round(kern_ms_max, 5),
+                                                 allgather_ms=round(max(0.0, ms - kern_ms_max), 5)),
     }
     # clocks
     out["clocks"] = clk.summary()
