@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "bs.h"
 
@@ -96,6 +97,17 @@ struct DevProps {
   int smem_per_sm;
 };
 const DevProps& dev_props();
+
+// Split-K of the tensor-core SpMM kernels: at least this many K chunks per CTA (measured defaults:
+// K6 3, K5 6; BS_SPLITK_MIN_CHUNKS overrides both for tuning). It depends on nothing but the
+// environment, so the split (and the summation order) stays a function of M and K only.
+inline int splitk_min_chunks(int dflt) {
+  static const int v = [] {
+    const char* e = getenv("BS_SPLITK_MIN_CHUNKS");
+    return e && e[0] ? atoi(e) : 0;
+  }();
+  return v >= 1 ? v : dflt;
+}
 
 }  // namespace bsk
 

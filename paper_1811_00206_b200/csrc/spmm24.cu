@@ -321,7 +321,9 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   const int64_t tiles = (g.M + BM - 1) / BM;
   int64_t S = bsk::dev_props().sms / tiles;  // split-K: from M and K only (never N)
   if (S > 8) S = 8;
-  if (S > a.NC / 6) S = a.NC / 6;  // at least 6 chunks per CTA: fixed costs stay amortised
+  // 6: a deeper split helped N <= 128 by 7% but cost 60% at N = 256 (A/B on CTC W_ih)
+  const int mc = bsk::splitk_min_chunks(6);
+  if (S > a.NC / mc) S = a.NC / mc;  // at least mc chunks per CTA: fixed costs stay amortised
   if (S < 1) S = 1;
   a.S = (int)S;
   auto kern = spmm24_kernel<DT>;
