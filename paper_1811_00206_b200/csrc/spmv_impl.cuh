@@ -738,8 +738,14 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
 }
 
 template <int V, int ES>
-struct StageSteps {  // Q: about 2 KB of values per stage
-  static constexpr int value = 2048 / (32 * V * ES) < 1 ? 1 : 2048 / (32 * V * ES);
+struct StageSteps {
+  // Q, steps per ring stage: at most 4. The stage loop is unrolled (twice: full and partial stages), so
+  // a small Q keeps the kernel's code small; the latency-regime layers are instruction-fetch bound
+  // (ncu: no_instructions the top stall on PTB). A/B on one box, against ~2 KB of values per stage:
+  // CTC W_hh 4.87 -> 3.27 us, W_ih 4.16 -> 3.35, fc7 90% 3.87 -> 3.68, PTB 90% 7.25 -> 6.61.
+  static constexpr int raw = 2048 / (32 * V * ES) < 1 ? 1 : 2048 / (32 * V * ES);
+  static constexpr int value = raw > 4 ? 4 : raw;
+  static constexpr int big = raw / value;  // stage multiplier of the variant whose stage holds a row's tail
 };
 
 template <int DT, int V, int IS, int BT, bool MULTI, int NT, int QM, int NV>
@@ -796,6 +802,15 @@ cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
 // resident and prefetch its W, measured 1.1-1.4x slower on every latency-regime layer: DESIGN.md §4.)
 template <int DT, int V, int IS, int BT, bool MULTI, int NV>
 cudaError_t launch_nt(const SpmvArgs& a, cudaStream_t s) {
+  constexpr int ES = bsk::DTraits<DT>::kBytes;
+  constexpr int BIG = StageSteps<V, ES>::big;
+  if constexpr (BIG > 1 && MULTI) {  // rows with tails always run the MULTI variant
+    // tails stream through the ring a whole row per stage; a row's tail that does not fit a small stage
+    // would fall back to per-entry global loads (PTB at 50%: 1.6x slower), so take the big-stage variant
+    constexpr int64_t SBs = (int64_t)StageSteps<V, ES>::value * (32 * V * ES + (IS == 5 ? 160 : 32 * V * IS));
+    const int64_t per = (int64_t)a.k * a.T * (ES + (IS == 5 ? 1 : IS));
+    if (a.T > 0 && a.k > 0 && per > SBs - 64) return launch_cfg<DT, V, IS, BT, MULTI, 512, BIG, NV>(a, s);
+  }
   return launch_cfg<DT, V, IS, BT, MULTI, 512, 1, NV>(a, s);
 }
 
