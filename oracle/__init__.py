@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
         L.orc_spmv_act.argtypes = [_vp, _vp, ctypes.c_int, _c_i64, _c_i64, ctypes.c_int, ctypes.c_int, _vp, _vp,
                                    ctypes.c_int, _vp, _vp]
         L.orc_spmv_act.restype = ctypes.c_int
+        L.orc_block_rank.argtypes = [_vp, ctypes.c_int, _c_i64, _c_i64, _c_i64, ctypes.c_int, _vp]
+        L.orc_block_rank.restype = ctypes.c_int
         L.orc_elem.argtypes = [_vp, ctypes.c_int, _c_i64]
         L.orc_elem.restype = ctypes.c_double
         _lib = L
@@ -159,6 +161,16 @@ def spmv(vals, idx, dt, M, K, block, k, x, rows=None):
     if lib().orc_spmv_rows(_ptr(vals), _ptr(idx), dt, M, K, block, k, _ptr(x), rp, n, _ptr(y), _ptr(bound)) != 0:
         raise ValueError("orc_spmv_rows rejected the arguments")
     return y, bound
+
+
+def block_rank(W: np.ndarray, dt: int, B: int) -> np.ndarray:
+    """Position of every element in its block's stable magnitude order (orc_block_rank): uint8 [M][K]."""
+    W = _check(np.ascontiguousarray(W), dt)
+    M, K = W.shape
+    out = np.zeros((M, K), dtype=np.uint8)
+    if lib().orc_block_rank(_ptr(W), dt, M, K, K, B, _ptr(out)) != 0:
+        raise ValueError("orc_block_rank rejected the arguments")
+    return out
 
 
 ACT = {"none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}

@@ -163,6 +163,39 @@ int orc_decode(const void* vals, const uint16_t* idx, int dt, int64_t M, int64_t
   return 0;
 }
 
+/* Position of every element in its block's magnitude order (Alg. 1's "sorts the weights in each block
+ * by their absolute magnitude"; ties to the lower offset, NaN above Inf, as orc_prune):
+ * rank[r*K + c] = position of W[r][c] in the stable descending sort of its block. A pruning step at
+ * any k keeps exactly the entries with rank < k, so one rank pass gives the masks of a whole gradual
+ * schedule (Alg. 1's outer loop) without retraining. Requires B <= 256 (u8 ranks). */
+int orc_block_rank(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int B, uint8_t* rank) {
+  if (M < 1 || K < 1 || B < 1 || B > 256 || K % B != 0 || ldw < K) return -1;
+  int64_t NB = K / B;
+  int* order = (int*)malloc(sizeof(int) * (size_t)B);
+  double* mag = (double*)malloc(sizeof(double) * (size_t)B);
+  for (int64_t r = 0; r < M; ++r)
+    for (int64_t b = 0; b < NB; ++b) {
+      int64_t c0 = r * ldw + b * B;
+      for (int j = 0; j < B; ++j) {
+        mag[j] = orc_elem(W, dt, c0 + j);
+        order[j] = j;
+      }
+      for (int i = 1; i < B; ++i) { /* the same stable insertion sort as orc_prune */
+        int cur = order[i];
+        int j = i - 1;
+        while (j >= 0 && mag_above(mag[cur], mag[order[j]])) {
+          order[j + 1] = order[j];
+          --j;
+        }
+        order[j + 1] = cur;
+      }
+      for (int t = 0; t < B; ++t) rank[r * K + b * B + order[t]] = (uint8_t)t;
+    }
+  free(order);
+  free(mag);
+  return 0;
+}
+
 /* ------------------------------------------------------------------ layouts (docs/layout.md) */
 
 static int64_t align256(int64_t n) { return (n + 255) / 256 * 256; }

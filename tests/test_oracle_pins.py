@@ -557,3 +557,26 @@ def test_spmv_act_structure():
     for name in ("relu", "sigmoid", "tanh"):
         yz, _ = oracle.spmv_act(vals, idx, oracle.F32, M, K, B, k, z, bias, name)
         np.testing.assert_array_equal(yz, [oracle.act(float(b), name) for b in bias.astype(np.float64)])
+
+
+# ------------------------------------------------------------------ block ranks (the mask schedule, NEXT-4)
+
+@pytest.mark.parametrize("B,family", [(4, "ties"), (8, "gaussian"), (16, "ties"), (32, "gaussian")])
+def test_block_rank_brute_force(B, family):
+    """rank_j = #{i : |w_i| > |w_j|} + #{i < j : |w_i| = |w_j|} per block, counted directly in numpy (not
+    by sorting); every block's ranks are a permutation of 0..B-1; rank < k is exactly orc_prune's mask."""
+    M, K = 6, 4 * B
+    W = synth.to_numpy(synth.matrix(M, K, "f32", family=family, seed=90 + B, B=B))
+    R = oracle.block_rank(W, oracle.F32, B)
+    A = np.abs(W.astype(np.float64)).reshape(M, K // B, B)
+    gt = (A[..., None, :] > A[..., :, None]).sum(-1)
+    eq_before = np.tril(A[..., None, :] == A[..., :, None], -1).sum(-1)
+    np.testing.assert_array_equal(R.reshape(M, K // B, B), gt + eq_before)
+    assert (np.sort(R.reshape(-1, B), axis=1) == np.arange(B)).all()
+    for k in (0, 1, B // 2, B):
+        vals, idx = oracle.prune(W, oracle.F32, B, k)
+        mask = np.zeros((M, K // B, B), dtype=bool)
+        for r in range(M):
+            for b in range(K // B):
+                mask[r, b, idx[r, b]] = True
+        np.testing.assert_array_equal(R.reshape(M, K // B, B) < k, mask)
