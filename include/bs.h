@@ -102,6 +102,16 @@ int bs_prune_k(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int blo
 int bs_prune(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block, double sparsity,
              int* k_out, void* vals, uint16_t* idx, void* stream);
 
+/* bs_block_rank: every element's position in its block's magnitude order (Alg. 1 "sorts the weights in
+ * each block by their absolute magnitude"; ties to the lower offset, NaN above Inf, as
+ * bs_prune_k). A pruning step at any k keeps exactly the entries with rank < k, so one pass yields the
+ * masks of a whole gradual sparsity schedule (Alg. 1's outer loop) without retraining.
+ *   W     device, M×K of dtype dt, row-major, leading dimension ldw >= K elements
+ *   rank  device out, M×K uint8 (row-major, leading dimension K)
+ * Errors: as bs_prune_k; BS_ERR_UNSUPPORTED unless block is 1, 2, 4, 8, 16 or 32. */
+int bs_block_rank(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block, uint8_t* rank,
+                  void* stream);
+
 /* bs_pack: permute canonical (vals, idx) into the device layout `layout` and narrow the indices
  * (docs/layout.md). This is a pure permutation, so the output is byte-exact. The paper stores "the
  * same number of non-zero values in each block partition", so the format needs no row

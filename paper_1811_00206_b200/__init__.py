@@ -26,7 +26,7 @@ DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 LAYOUTS = {"spmv": 1, "spmm": 2, "sp24": 3}
 
 EXPORTS = ("bs_k_from_sparsity", "bs_packed_bytes", "bs_status_str", "bs_version", "bs_prune", "bs_prune_k",
-           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm", "bs_choose_layout")
+           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm", "bs_choose_layout", "bs_block_rank")
 ACTS = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}  # bs_act (include/bs.h)
 SPMV_PDL, SPMV_W_STATIC = 1, 2  # bs_spmv_ex flags (include/bs.h)
 
@@ -52,6 +52,8 @@ def _load() -> ctypes.CDLL:
     L.bs_k_from_sparsity.restype = ci
     L.bs_packed_bytes.argtypes = [i64, i64, ci, ci, ci, ci]
     L.bs_packed_bytes.restype = ctypes.c_size_t
+    L.bs_block_rank.argtypes = [vp, ci, i64, i64, i64, ci, vp, vp]
+    L.bs_block_rank.restype = ci
     L.bs_choose_layout.argtypes = [i64, i64, ci, ci, ci, i64]
     L.bs_choose_layout.restype = ci
     L.bs_status_str.argtypes = [ci]
@@ -167,6 +169,21 @@ def prune(W: torch.Tensor, block: int, sparsity: float | None = None, k: int | N
                              idx.data_ptr() if idx.numel() else None, _stream(W.device))
     _check(st, "bs_prune_k")
     return vals, idx, k
+
+
+def block_rank(W: torch.Tensor, block: int) -> torch.Tensor:
+    """Every element's position in its block's magnitude order (bs_block_rank): uint8 [M, K]. The mask
+    of a pruning step at any k is rank < k (Alg. 1's schedule without retraining)."""
+    _need_cuda(W)
+    M, K = W.shape
+    if W.stride(1) != 1:
+        W = W.contiguous()
+    rank = torch.empty((M, K), dtype=torch.uint8, device=W.device)
+    with torch.cuda.device(W.device):
+        st = _lib.bs_block_rank(W.data_ptr(), DTYPES[W.dtype], M, K, W.stride(0), block, rank.data_ptr(),
+                                _stream(W.device))
+    _check(st, "bs_block_rank")
+    return rank
 
 
 def choose_layout(M: int, K: int, block: int, k: int, dtype: torch.dtype, batch: int) -> str:

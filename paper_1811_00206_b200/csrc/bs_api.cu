@@ -111,6 +111,16 @@ int bs_prune_k(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int blo
   return from_cuda(bsk_launch_prune(W, dt, M, K, ldw, block, k, vals, idx, (cudaStream_t)stream));
 }
 
+int bs_block_rank(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block, uint8_t* rank,
+                  void* stream) {
+  if (!valid_dt(dt)) return BS_ERR_DTYPE;
+  int st = check_shape(M, K, block, 0);
+  if (st) return st;
+  if (!W || !rank || ldw < K) return BS_ERR_ARG;
+  if (block > 32 || (block & (block - 1)) != 0) return BS_ERR_UNSUPPORTED;
+  return from_cuda(bsk_launch_block_rank(W, dt, M, K, ldw, block, rank, (cudaStream_t)stream));
+}
+
 int bs_prune(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block, double sparsity, int* k_out,
              void* vals, uint16_t* idx, void* stream) {
   if (!(sparsity >= 0.0) || !(sparsity < 1.0)) return BS_ERR_ARG;

@@ -114,6 +114,8 @@ inline int splitk_min_chunks(int dflt) {
 // Launchers implemented in the kernel translation units. All return cudaError_t of the launch.
 cudaError_t bsk_launch_prune(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int B, int k,
                              void* vals, uint16_t* idx, cudaStream_t s);
+cudaError_t bsk_launch_block_rank(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int B, uint8_t* rank,
+                                  cudaStream_t s);
 cudaError_t bsk_launch_pack(const void* vals, const uint16_t* idx, const bsk::Geom& g, void* packed,
                             cudaStream_t s);
 cudaError_t bsk_launch_unpack(const void* packed, const bsk::Geom& g, void* vals, uint16_t* idx,

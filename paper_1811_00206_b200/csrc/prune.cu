@@ -313,6 +313,82 @@ __global__ void __launch_bounds__(256) prune_thread(const typename KeyOf<DT>::ra
   }
 }
 
+// Block ranks (bs_block_rank): thread per block (B <= 32). rank_j = #{i : key_i > key_j} +
+// #{i < j : key_i == key_j}, the position of element j in the block's stable descending magnitude
+// order; the count is integer-exact, so it equals the oracle's sort bit for bit.
+template <int DT, int B>
+__global__ void __launch_bounds__(256) block_rank_kernel(const typename KeyOf<DT>::raw_t* __restrict__ W,
+                                                         int64_t M, int64_t NB, int64_t ldw,
+                                                         uint8_t* __restrict__ rank, bool vec) {
+  const int64_t nblocks = M * NB;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t K = NB * B;
+  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < nblocks; gid += stride) {
+    const int64_t r = gid / NB, b = gid - r * NB;
+    using raw_t = typename KeyOf<DT>::raw_t;
+    constexpr int ES = sizeof(raw_t);
+    const raw_t* src = W + r * ldw + b * B;
+    uint32_t key[B];
+    if constexpr (B * ES % 16 == 0) {
+      if (vec) {  // 16-byte loads (rows 16-byte aligned)
+        uint32_t w[B * ES / 4];
+#pragma unroll
+        for (int q = 0; q < B * ES / 16; ++q) {
+          const uint4 v = __ldcs((const uint4*)src + q);
+          w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j) key[j] = KeyOf<DT>::key(ES == 2 ? (w[j >> 1] >> (16 * (j & 1))) & 0xffffu : w[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < B; ++j) key[j] = KeyOf<DT>::key((uint32_t)__ldg(src + j));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < B; ++j) key[j] = KeyOf<DT>::key((uint32_t)__ldg(src + j));
+    }
+    uint8_t* dst = rank + r * K + b * B;
+    uint32_t packed[(B + 3) / 4];
+#pragma unroll
+    for (int q = 0; q < (B + 3) / 4; ++q) packed[q] = 0;
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      int c = 0;
+#pragma unroll
+      for (int i = 0; i < B; ++i) c += (key[i] > key[j]) || (i < j && key[i] == key[j]);
+      packed[j >> 2] |= (uint32_t)c << (8 * (j & 3));
+    }
+    if constexpr (B % 4 == 0) {  // the rank row is 4-byte aligned (K and B multiples of 4)
+#pragma unroll
+      for (int q = 0; q < B / 4; ++q) ((uint32_t*)dst)[q] = packed[q];
+    } else {
+#pragma unroll
+      for (int j = 0; j < B; ++j) dst[j] = (uint8_t)(packed[j >> 2] >> (8 * (j & 3)));
+    }
+  }
+}
+
+template <int DT>
+cudaError_t launch_block_rank_t(const void* W, int64_t M, int64_t K, int64_t ldw, int B, uint8_t* rank, cudaStream_t s) {
+  using raw_t = typename KeyOf<DT>::raw_t;
+  const int64_t NB = K / B;
+  int64_t blocks = (M * NB + 255) / 256;
+  const int sms = bsk::dev_props().sms;
+  blocks = blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8;
+  const bool vec = ((uintptr_t)W & 15) == 0 && (ldw * (int64_t)sizeof(raw_t)) % 16 == 0;
+  auto run = [&](auto kern) { kern<<<(unsigned)blocks, 256, 0, s>>>((const raw_t*)W, M, NB, ldw, rank, vec); };
+  switch (B) {
+    case 32: run(block_rank_kernel<DT, 32>); break;
+    case 16: run(block_rank_kernel<DT, 16>); break;
+    case 8: run(block_rank_kernel<DT, 8>); break;
+    case 4: run(block_rank_kernel<DT, 4>); break;
+    case 2: run(block_rank_kernel<DT, 2>); break;
+    case 1: run(block_rank_kernel<DT, 1>); break;
+    default: return cudaErrorNotSupported;
+  }
+  return cudaGetLastError();
+}
+
 template <int DT>
 cudaError_t launch_prune_t(const void* W, int64_t M, int64_t K, int64_t ldw, int B, int k, void* vals,
                            uint16_t* idx, cudaStream_t s) {
@@ -359,5 +435,14 @@ cudaError_t bsk_launch_prune(const void* W, int dt, int64_t M, int64_t K, int64_
     case BS_F32: return launch_prune_t<BS_F32>(W, M, K, ldw, B, k, vals, idx, s);
     case BS_F16: return launch_prune_t<BS_F16>(W, M, K, ldw, B, k, vals, idx, s);
     default: return launch_prune_t<BS_BF16>(W, M, K, ldw, B, k, vals, idx, s);
+  }
+}
+
+cudaError_t bsk_launch_block_rank(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int B, uint8_t* rank,
+                                  cudaStream_t s) {
+  switch (dt) {
+    case BS_F32: return launch_block_rank_t<BS_F32>(W, M, K, ldw, B, rank, s);
+    case BS_F16: return launch_block_rank_t<BS_F16>(W, M, K, ldw, B, rank, s);
+    default: return launch_block_rank_t<BS_BF16>(W, M, K, ldw, B, rank, s);
   }
 }

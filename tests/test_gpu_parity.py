@@ -462,6 +462,29 @@ def test_spmm_auto_layout(bs, B, k, N):
     assert ok, worst
 
 
+@pytest.mark.parametrize("B,dname,family", [(32, "f16", "gaussian"), (16, "bf16", "ties"), (8, "f32", "gaussian"),
+                                             (4, "f16", "ties"), (32, "f32", "ties"), (2, "bf16", "gaussian")])
+def test_block_rank(bs, B, dname, family):
+    """bs_block_rank equals the oracle's sort positions bit for bit, and rank < k is bs_prune's mask for a
+    whole schedule of k (Alg. 1's gradual sparsity without retraining)."""
+    M, K = 257, 64 * B
+    W = synth.matrix(M, K, dname, family=family, seed=synth.seed_for(9, 500 + B), B=B)
+    R = bs.block_rank(W.cuda(), B)
+    np.testing.assert_array_equal(R.cpu().numpy(), oracle.block_rank(synth.to_numpy(W), DT[dname], B))
+    for k in sorted({1, B // 4, B // 2, B - 1} - {0}):
+        _, idx, _ = bs.prune(W.cuda(), B, k=k)
+        mask = torch.zeros((M, K // B, B), dtype=torch.bool, device="cuda")
+        mask.scatter_(2, idx.to(torch.int64), True)
+        assert torch.equal(R.view(M, K // B, B) < k, mask)
+
+
+def test_block_rank_special_values(bs):
+    for dname in ("f32", "f16", "bf16"):
+        W = synth.special_block_matrix(dname)
+        R = bs.block_rank(W.cuda(), 16)
+        np.testing.assert_array_equal(R.cpu().numpy(), oracle.block_rank(synth.to_numpy(W), DT[dname], 16))
+
+
 # ---------------------------------------------------------------- 2:4 (B = 4, k = 2): SP24 layout
 
 @pytest.mark.parametrize("N", [1, 2, 8, 16, 64, 200])

@@ -26,7 +26,7 @@ def bs():
 
 def test_header_declares_the_boundary():
     syms = _declared_symbols()
-    for s in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm",
+    for s in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm", "bs_block_rank",
               "bs_packed_bytes", "bs_k_from_sparsity", "bs_status_str", "bs_version"):
         assert s in syms
 
