@@ -75,6 +75,17 @@ def lib() -> ctypes.CDLL:
         L.orc_spmv_act.restype = ctypes.c_int
         L.orc_block_rank.argtypes = [_vp, ctypes.c_int, _c_i64, _c_i64, _c_i64, ctypes.c_int, _vp]
         L.orc_block_rank.restype = ctypes.c_int
+        L.orc_schedule.argtypes = [ctypes.c_double, ctypes.c_int, ctypes.c_int]
+        L.orc_schedule.restype = ctypes.c_double
+        L.orc_prune_dense.argtypes = [_vp, ctypes.c_int, _c_i64, _c_i64, _c_i64, ctypes.c_int, ctypes.c_int, _vp]
+        L.orc_prune_dense.restype = ctypes.c_int
+        L.orc_keep_count.argtypes = [_c_i64, ctypes.c_double]
+        L.orc_keep_count.restype = _c_i64
+        L.orc_random_mask.argtypes = [_vp, ctypes.c_int, _c_i64, _c_i64, _c_i64, ctypes.c_double, _vp]
+        L.orc_random_mask.restype = ctypes.c_int
+        L.orc_block_mask.argtypes = [_vp, ctypes.c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, ctypes.c_double,
+                                     ctypes.c_int, _vp]
+        L.orc_block_mask.restype = ctypes.c_int
         L.orc_elem.argtypes = [_vp, ctypes.c_int, _c_i64]
         L.orc_elem.restype = ctypes.c_double
         _lib = L
@@ -248,6 +259,48 @@ def to_double(a: np.ndarray, dt: int) -> np.ndarray:
     L = lib()
     p = _ptr(flat)
     return np.array([L.orc_elem(p, dt, i) for i in range(flat.size)], dtype=np.float64).reshape(a.shape)
+
+
+def schedule(target: float, n: int, i: int) -> float:
+    """GraduallyIncrease (Alg. 1), cubic per S:205: target·(1 − (1 − i/n)^3)."""
+    return lib().orc_schedule(float(target), int(n), int(i))
+
+
+def prune_dense(W: np.ndarray, dt: int, block: int, k: int) -> np.ndarray:
+    """Alg. 1's pruned matrix M_p after one step at k per block: kept entries bit-copied, +0 elsewhere."""
+    W = _check(np.ascontiguousarray(W), dt)
+    M, K = W.shape
+    out = np.zeros((M, K), dtype=_vdtype(dt))
+    if lib().orc_prune_dense(_ptr(W), dt, M, K, K, block, k, _ptr(out)) != 0:
+        raise ValueError("orc_prune_dense rejected the arguments")
+    return out
+
+
+def keep_count(n: int, sparsity: float) -> int:
+    """Units kept at sparsity s: lround((1 − s)·n)."""
+    return int(lib().orc_keep_count(int(n), float(sparsity)))
+
+
+def random_mask(W: np.ndarray, dt: int, sparsity: float) -> np.ndarray:
+    """Random sparsity (global magnitude pruning): uint8 keep mask [M][K]."""
+    W = _check(np.ascontiguousarray(W), dt)
+    M, K = W.shape
+    out = np.zeros((M, K), dtype=np.uint8)
+    if lib().orc_random_mask(_ptr(W), dt, M, K, K, float(sparsity), _ptr(out)) != 0:
+        raise ValueError("orc_random_mask rejected the arguments")
+    return out
+
+
+def block_mask(W: np.ndarray, dt: int, bh: int, bw: int, sparsity: float, criterion: str = "max") -> np.ndarray:
+    """Block sparsity with bh×bw tiles scored by max or mean |w|; vector sparsity is
+    bh = 1, bw = K (rows) or bh = M, bw = 1 (columns) with "mean". uint8 keep mask [M][K]."""
+    W = _check(np.ascontiguousarray(W), dt)
+    M, K = W.shape
+    out = np.zeros((M, K), dtype=np.uint8)
+    crit = {"max": 0, "mean": 1}[criterion]
+    if lib().orc_block_mask(_ptr(W), dt, M, K, K, int(bh), int(bw), float(sparsity), crit, _ptr(out)) != 0:
+        raise ValueError("orc_block_mask rejected the arguments")
+    return out
 
 
 def ideal_time(d_time: float, o_time: float, sparsity: float) -> float:

@@ -196,6 +196,137 @@ int orc_block_rank(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int
   return 0;
 }
 
+/* ------------------------------------------------------------------ Alg. 1's outer loop and the comparison patterns */
+
+/* GraduallyIncrease (Alg. 1 line "tmp_sparsity = GraduallyIncrease(tmp_sparsity)"): "This threshold
+ * percentage is gradually increased from 0 to the target sparsity while the increase rate decreases with
+ * pruning iteration". The paper gives no formula; SPEC S:205 fixes the cubic trajectory
+ * s_i = target * (1 - (1 - i/n)^3), i = 0..n (rate 3·target/n·(1 - i/n)^2, decreasing). Returns -1 on
+ * bad arguments (n < 1, i outside [0, n], target outside [0, 1)). */
+double orc_schedule(double target, int n, int i) {
+  if (n < 1 || i < 0 || i > n || !(target >= 0.0) || !(target < 1.0)) return -1.0;
+  double u = 1.0 - (double)i / (double)n;
+  return target * (1.0 - u * u * u);
+}
+
+/* The pruned matrix M_p of Alg. 1 (its output) in dense form after one pruning step at k kept
+ * per block: Wp[r][c] = W[r][c] (bit copy) if (r, c) is kept by orc_prune, else +0 of dtype dt.
+ * Wp is M×K with leading dimension K. */
+int orc_prune_dense(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int B, int k, void* Wp) {
+  if (M < 1 || K < 1 || B < 1 || K % B != 0 || k < 0 || k > B || ldw < K) return -1;
+  int64_t NB = K / B;
+  int es = dtype_size(dt);
+  void* vals = malloc((size_t)(M * NB * (k > 0 ? k : 1)) * (size_t)es);
+  uint16_t* idx = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)(M * NB * (k > 0 ? k : 1)));
+  if (orc_prune(W, dt, M, K, ldw, B, k, vals, idx)) {
+    free(vals);
+    free(idx);
+    return -1;
+  }
+  memset(Wp, 0, (size_t)(M * K) * (size_t)es);
+  for (int64_t r = 0; r < M; ++r)
+    for (int64_t b = 0; b < NB; ++b)
+      for (int t = 0; t < k; ++t) {
+        int64_t pos = (r * NB + b) * k + t;
+        memcpy((unsigned char*)Wp + (r * K + b * B + idx[pos]) * es, (const unsigned char*)vals + pos * es, es);
+      }
+  free(vals);
+  free(idx);
+  return 0;
+}
+
+/* A scored unit (an element or a tile) for the global selections below. */
+typedef struct {
+  double score;  /* magnitude, or a tile score; NaN = above everything */
+  int64_t index; /* row-major position of the element / tile */
+} orc_unit;
+
+/* Descending score, NaN first (all NaNs equal), then ascending index: a total order. */
+static int unit_cmp(const void* pa, const void* pb) {
+  const orc_unit* a = (const orc_unit*)pa;
+  const orc_unit* b = (const orc_unit*)pb;
+  int an = isnan(a->score), bn = isnan(b->score);
+  if (an != bn) return an ? -1 : 1;
+  if (!an && a->score != b->score) return a->score > b->score ? -1 : 1;
+  return a->index < b->index ? -1 : (a->index > b->index ? 1 : 0);
+}
+
+/* keep[u] = 1 for the `keep` first units in unit_cmp order (a library sort as one step). */
+static void select_top(orc_unit* units, int64_t n, int64_t keep, uint8_t* keep_flag) {
+  qsort(units, (size_t)n, sizeof(orc_unit), unit_cmp);
+  memset(keep_flag, 0, (size_t)n);
+  for (int64_t i = 0; i < keep && i < n; ++i) keep_flag[units[i].index] = 1;
+}
+
+/* Number of units kept at sparsity s: lround((1 - s) * n), the same rounding as k. */
+int64_t orc_keep_count(int64_t n, double s) {
+  if (n < 0 || !(s >= 0.0) || !(s < 1.0)) return -1;
+  return (int64_t)llround((1.0 - s) * (double)n);
+}
+
+/* Random sparsity (Han et al.; "performs pruning in each independent weight
+ * matrix"): magnitude pruning over the WHOLE matrix. Keeps the keep_count(M·K, s) entries of largest
+ * |w| (NaN above Inf; ties to the lower row-major index). mask[r*K + c] = 1 if kept. */
+int orc_random_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, double s, uint8_t* mask) {
+  if (M < 1 || K < 1 || ldw < K) return -1;
+  int64_t n = M * K, keep = orc_keep_count(n, s);
+  if (keep < 0) return -1;
+  orc_unit* u = (orc_unit*)malloc(sizeof(orc_unit) * (size_t)n);
+  for (int64_t r = 0; r < M; ++r)
+    for (int64_t c = 0; c < K; ++c) {
+      double v = orc_elem(W, dt, r * ldw + c);
+      u[r * K + c].score = isnan(v) ? NAN : fabs(v);
+      u[r * K + c].index = r * K + c;
+    }
+  select_top(u, n, keep, mask);
+  free(u);
+  return 0;
+}
+
+/* Block sparsity (Narang et al.): the matrix is tiled into bh×bw tiles (row-major tile
+ * order); each tile is scored by "the maximum magnitude or the average magnitude of the weights within
+ * one block as a representative": criterion 0 = max |w| (NaN above Inf), criterion 1 =
+ * mean |w|, compared as the fp64 sum of |w| in row-major order inside the tile (the mean times the fixed
+ * tile size; a NaN sum ranks above everything). The keep_count(#tiles, s) best tiles survive whole
+ * (ties to the lower tile index). mask[r*K + c] = 1 if (r, c) lies in a kept tile.
+ * Vector sparsity (Mao et al.) is the same rule with whole rows (bh = 1, bw = K) or whole columns
+ * (bh = M, bw = 1) as the unit and the mean criterion. */
+int orc_block_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int64_t bh, int64_t bw, double s,
+                   int criterion, uint8_t* mask) {
+  if (M < 1 || K < 1 || ldw < K || bh < 1 || bw < 1 || M % bh || K % bw || criterion < 0 || criterion > 1)
+    return -1;
+  int64_t TR = M / bh, TC = K / bw, n = TR * TC, keep = orc_keep_count(n, s);
+  if (keep < 0) return -1;
+  orc_unit* u = (orc_unit*)malloc(sizeof(orc_unit) * (size_t)n);
+  uint8_t* tk = (uint8_t*)malloc((size_t)n);
+  for (int64_t tr = 0; tr < TR; ++tr)
+    for (int64_t tc = 0; tc < TC; ++tc) {
+      double score = criterion == 0 ? -1.0 : 0.0;
+      int seen_nan = 0;
+      for (int64_t i = 0; i < bh; ++i)
+        for (int64_t j = 0; j < bw; ++j) {
+          double v = orc_elem(W, dt, (tr * bh + i) * ldw + tc * bw + j);
+          if (isnan(v)) {
+            seen_nan = 1;
+            continue;
+          }
+          if (criterion == 0) {
+            if (fabs(v) > score) score = fabs(v);
+          } else {
+            score += fabs(v);
+          }
+        }
+      u[tr * TC + tc].score = seen_nan ? NAN : score;
+      u[tr * TC + tc].index = tr * TC + tc;
+    }
+  select_top(u, n, keep, tk);
+  for (int64_t r = 0; r < M; ++r)
+    for (int64_t c = 0; c < K; ++c) mask[r * K + c] = tk[(r / bh) * TC + c / bw];
+  free(u);
+  free(tk);
+  return 0;
+}
+
 /* ------------------------------------------------------------------ layouts (docs/layout.md) */
 
 static int64_t align256(int64_t n) { return (n + 255) / 256 * 256; }

@@ -580,3 +580,170 @@ def test_block_rank_brute_force(B, family):
             for b in range(K // B):
                 mask[r, b, idx[r, b]] = True
         np.testing.assert_array_equal(R.reshape(M, K // B, B) < k, mask)
+
+
+# ------------------------------------------------------------------ Alg. 1's outer loop and the comparison patterns (NEXT-4)
+
+def test_schedule_S195_and_boundaries():
+    g = _gold("spec_examples.json")["schedule_S195"]
+    assert oracle.schedule(g["target"], g["n"], g["i"]) == pytest.approx(g["value"], abs=1e-15)
+    for target in (0.5, 0.9, 0.97):
+        for n in (1, 3, 10, 37):
+            assert oracle.schedule(target, n, 0) == 0.0
+            assert oracle.schedule(target, n, n) == pytest.approx(target, abs=1e-15)
+    for bad in ((0.9, 0, 0), (0.9, 10, 11), (0.9, 10, -1), (1.0, 10, 3), (-0.1, 10, 3)):
+        assert oracle.schedule(*bad) == -1.0
+
+
+def test_schedule_rate_decreases():
+    """increased from 0 to the target "while the increase rate decreases with pruning iteration"."""
+    for target, n in ((0.9, 10), (0.5, 7), (0.97, 25)):
+        s = [oracle.schedule(target, n, i) for i in range(n + 1)]
+        d = np.diff(s)
+        assert np.all(d > 0)
+        assert np.all(np.diff(d) < 0)
+
+
+def _rank_count(Wn: np.ndarray, B: int) -> np.ndarray:
+    """Independent rank count per block (not the oracle's sort): #{greater} + #{equal at a lower offset}."""
+    M, K = Wn.shape
+    mag = np.where(np.isnan(Wn), np.inf, np.abs(Wn)).reshape(M, K // B, B).astype(np.float64)
+    nan = np.isnan(Wn).reshape(M, K // B, B)
+    key = np.where(nan, 2.0, 1.0)  # NaN class above every number
+    gt = (key[..., :, None] > key[..., None, :]) | ((key[..., :, None] == key[..., None, :]) & (mag[..., :, None] > mag[..., None, :]))
+    eq = (key[..., :, None] == key[..., None, :]) & ((mag[..., :, None] == mag[..., None, :]) | nan[..., :, None])
+    lower = np.arange(B)[:, None] < np.arange(B)[None, :]
+    rank = gt.sum(axis=-2) + (eq & lower).sum(axis=-2)  # rank of j: count over i
+    return rank.reshape(M, K)
+
+
+@pytest.mark.parametrize("dname,family,B", [("f32", "gaussian", 16), ("f16", "ties", 8), ("bf16", "ties", 32)])
+def test_prune_dense_against_rank_count(dname, family, B):
+    """M_p: kept entries are bit copies, the rest +0; kept iff the independent rank count is < k."""
+    dt = {"f32": oracle.F32, "f16": oracle.F16, "bf16": oracle.BF16}[dname]
+    W = synth.to_numpy(synth.matrix(12, 4 * B, dname, family=family, seed=91))
+    Wf = oracle.to_double(W, dt)
+    rank = _rank_count(Wf, B)
+    for k in (0, 1, B // 3, B - 1, B):
+        P = oracle.prune_dense(W, dt, B, k)
+        keep = rank < k
+        raw = W.view(np.uint32 if W.itemsize == 4 else np.uint16)
+        praw = P.view(raw.dtype)
+        np.testing.assert_array_equal(praw[keep], raw[keep])
+        assert np.all(praw[~keep] == 0)
+        assert keep.reshape(12, 4, B).sum(-1).min() == k == keep.reshape(12, 4, B).sum(-1).max()
+
+
+def test_gradual_schedule_without_retraining_nests():
+    """Alg. 1 without retraining: each iteration prunes the previous M_p at k_i = lround((1 - s_i)·B);
+    survivors shrink monotonically and the end point equals one step at the target."""
+    B, target, n = 32, 0.9, 10
+    W = synth.to_numpy(synth.matrix(20, 4 * B, "f16", seed=92))
+    cur = W.copy()
+    prev_keep = np.ones(W.shape, dtype=bool)
+    for i in range(1, n + 1):
+        k = oracle.k_from_sparsity(B, oracle.schedule(target, n, i))
+        cur = oracle.prune_dense(cur, oracle.F16, B, k)
+        keep = cur.view(np.uint16) != 0
+        assert np.all(keep <= prev_keep)
+        prev_keep = keep
+    np.testing.assert_array_equal(cur.view(np.uint16), oracle.prune_dense(W, oracle.F16, B, 3).view(np.uint16))
+
+
+def test_random_mask_S163():
+    g = _gold("spec_examples.json")["random_S163"]
+    W = np.array(g["W"], dtype=np.float32)
+    for s, want in g["cases"]:
+        np.testing.assert_array_equal(oracle.random_mask(W, oracle.F32, s), np.array(want, dtype=np.uint8))
+
+
+@pytest.mark.parametrize("family,s", [("gaussian", 0.9), ("ties", 0.5), ("ties", 0.75), ("gaussian", 0.0)])
+def test_random_mask_optimal_and_ties(family, s):
+    """Exactly keep_count kept; no dropped magnitude exceeds a kept one; at the threshold magnitude the
+    kept entries precede the dropped ones in row-major order."""
+    W = synth.to_numpy(synth.matrix(17, 40, "f32", family=family, seed=93))
+    m = oracle.random_mask(W, oracle.F32, s).reshape(-1).astype(bool)
+    a = np.abs(W.reshape(-1).astype(np.float64))
+    assert m.sum() == oracle.keep_count(W.size, s)
+    if m.all():
+        return
+    T = a[m].min()
+    assert a[~m].max() <= T
+    eq = np.flatnonzero(a == T)
+    kept_eq, drop_eq = eq[m[eq]], eq[~m[eq]]
+    if kept_eq.size and drop_eq.size:
+        assert kept_eq.max() < drop_eq.min()
+
+
+def test_random_mask_one_row_is_balanced_with_block_K():
+    """random pruning of a single row equals balanced pruning with one block of width K."""
+    for family in ("gaussian", "ties"):
+        W = synth.to_numpy(synth.matrix(1, 64, "f16", family=family, seed=94))
+        for s in (0.5, 0.75, 0.9):
+            k = oracle.k_from_sparsity(64, s)
+            _, idx = oracle.prune(W, oracle.F16, 64, k)
+            want = np.zeros((1, 64), dtype=np.uint8)
+            want[0, idx.reshape(-1)] = 1
+            np.testing.assert_array_equal(oracle.random_mask(W, oracle.F16, s), want)
+
+
+def test_random_mask_sign_and_nan():
+    W = synth.to_numpy(synth.matrix(9, 32, "f32", seed=95))
+    np.testing.assert_array_equal(oracle.random_mask(W, oracle.F32, 0.8), oracle.random_mask(-W, oracle.F32, 0.8))
+    W2 = W.copy()
+    W2[3, 7] = np.nan
+    W2[5, 1] = np.inf
+    m = oracle.random_mask(W2, oracle.F32, 0.99)  # keep lround(0.01·288) = 3: NaN, Inf, then the largest
+    assert m[3, 7] == 1 and m[5, 1] == 1 and m.sum() == 3
+
+
+def test_block_mask_S172_S173():
+    g = _gold("spec_examples.json")["block_S172"]
+    W = np.array(g["W"], dtype=np.float32)
+    np.testing.assert_array_equal(oracle.block_mask(W, oracle.F32, 2, 2, 0.5, "max"), np.array(g["max_keep"], dtype=np.uint8))
+    W2 = np.array(g["meanmax_W"], dtype=np.float32)
+    np.testing.assert_array_equal(oracle.block_mask(W2, oracle.F32, 2, 2, 0.5, "max"), np.array(g["meanmax_max"], dtype=np.uint8))
+    np.testing.assert_array_equal(oracle.block_mask(W2, oracle.F32, 2, 2, 0.5, "mean"), np.array(g["meanmax_mean"], dtype=np.uint8))
+
+
+def test_block_mask_tile_scores_brute_force():
+    """Integer weights (exact tile sums): kept tiles are the keep_count best by (score desc, tile index
+    asc), scored independently here with numpy; every element of a kept tile is kept."""
+    M, K, bh, bw = 16, 48, 4, 8
+    W = synth.to_numpy(synth.matrix(M, K, "f32", family="ties", seed=96))
+    A = np.abs(W.astype(np.float64)).reshape(M // bh, bh, K // bw, bw)
+    for crit, score in (("max", A.max(axis=(1, 3))), ("mean", A.sum(axis=(1, 3)))):
+        for s in (0.25, 0.5, 0.9):
+            m = oracle.block_mask(W, oracle.F32, bh, bw, s, crit)
+            flat = score.reshape(-1)
+            order = sorted(range(flat.size), key=lambda t: (-flat[t], t))
+            keep = np.zeros(flat.size, dtype=np.uint8)
+            keep[order[:oracle.keep_count(flat.size, s)]] = 1
+            want = np.repeat(np.repeat(keep.reshape(M // bh, K // bw), bh, axis=0), bw, axis=1)
+            np.testing.assert_array_equal(m, want, err_msg=f"{crit} s={s}")
+
+
+def test_block_mask_unit_tiles_equal_random():
+    """1×1 tiles with the max criterion score each element by |w|: the random-sparsity mask."""
+    W = synth.to_numpy(synth.matrix(10, 24, "bf16", family="ties", seed=97))
+    for s in (0.3, 0.8):
+        np.testing.assert_array_equal(oracle.block_mask(W, oracle.BF16, 1, 1, s, "max"), oracle.random_mask(W, oracle.BF16, s))
+
+
+def test_vector_mask_S181_and_transpose():
+    g = _gold("spec_examples.json")["vector_S181"]
+    W = np.array(g["W"], dtype=np.float32)
+    m = oracle.block_mask(W, oracle.F32, 1, W.shape[1], g["sparsity"], "mean")
+    np.testing.assert_array_equal(m[:, 0], np.array(g["row_keep"], dtype=np.uint8))
+    assert np.all(m == m[:, :1])
+    mt = oracle.block_mask(np.ascontiguousarray(W.T), oracle.F32, W.T.shape[0], 1, g["sparsity"], "mean")
+    np.testing.assert_array_equal(mt, m.T)
+
+
+def test_pattern_masks_reject_bad_shapes():
+    W = np.zeros((6, 10), dtype=np.float32)
+    with pytest.raises(ValueError):
+        oracle.block_mask(W, oracle.F32, 4, 5, 0.5)
+    with pytest.raises(ValueError):
+        oracle.random_mask(W, oracle.F32, 1.0)
+    assert oracle.keep_count(10, 0.9) == 1 and oracle.keep_count(100, 0.9) == 10 and oracle.keep_count(7, 0.5) == 4
