@@ -107,9 +107,63 @@ int bs_prune(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block
  * bs_prune_k). A pruning step at any k keeps exactly the entries with rank < k, so one pass yields the
  * masks of a whole gradual sparsity schedule (Alg. 1's outer loop) without retraining.
  *   W     device, M×K of dtype dt, row-major, leading dimension ldw >= K elements
- *   rank  device out, M×K uint8 (row-major, leading dimension K)
+ *   rank  device out, M×K uint8 (row-major, leading dimension K); any alignment (32-bit stores are
+ *         used only when rank is 4-byte aligned)
  * Errors: as bs_prune_k; BS_ERR_UNSUPPORTED unless block is 1, 2, 4, 8, 16 or 32. */
 int bs_block_rank(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int block, uint8_t* rank,
+                  void* stream);
+
+/* ---------------------------------------------------------------- Alg. 1's schedule and the comparison patterns */
+
+/* GraduallyIncrease (Alg. 1): the threshold sparsity of pruning iteration i of n. The paper says
+ * only that it "is gradually increased from 0 to the target sparsity while the increase rate decreases
+ * with pruning iteration"; the trajectory is SPEC's cubic (reading A20):
+ *   s_i = target · (1 - (1 - i/n)^3),  i = 0..n   (s_0 = 0, s_n = target: 0.9, 10, 5 -> 0.7875).
+ * Host, pure. Returns -1 if n < 1, i outside [0, n] or target outside [0, 1). */
+double bs_schedule_sparsity(double target, int n, int i);
+
+/* Units kept at sparsity s by the global patterns below: lround((1 - s) · n), the rounding of k
+ * (reading A1 applied to the whole unit count, A8, A22). Host, pure. -1 on bad arguments. */
+int64_t bs_keep_count(int64_t n, double sparsity);
+
+/* bs_decode: the dense W_bs, i.e. Alg. 1's output "the pruned matrix M_p", from canonical
+ * (vals, idx): W[r][b·B + idx[r][b][t]] = vals[r][b][t] (bit copies), +0 everywhere else.
+ * bs_prune_k followed by bs_decode is one pruning iteration of Alg. 1 on a dense matrix (in place
+ * when W is the pruned matrix itself: bs_prune_k reads it completely before bs_decode writes, in
+ * stream order); iterating it along bs_schedule_sparsity is Alg. 1's schedule without retraining.
+ *   vals, idx  device, canonical [M][K/B][k] (bs_prune_k's output)
+ *   W          device out, M×K of dtype dt, row-major, leading dimension ldw >= K
+ * Errors: as bs_pack for the shape arguments; BS_ERR_ARG for NULL pointers or ldw < K. */
+int bs_decode(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int block, int k, int dt,
+              void* W, int64_t ldw, void* stream);
+
+/* Device scratch the mask generators below need (bh = bw = 0 for bs_random_mask): selection state,
+ * per-CTA counters and, for tiles, one 8-byte score and one byte per tile. Host, pure. */
+size_t bs_pattern_workspace_bytes(int64_t M, int64_t K, int64_t bh, int64_t bw);
+
+/* bs_random_mask: random sparsity, the paper's main comparison pattern (Han et al.; P:39, P:230,
+ * "performs pruning in each independent weight matrix"): magnitude pruning over the WHOLE
+ * matrix, mask[r·K + c] = 1 for the bs_keep_count(M·K, s) entries of largest |w| (the magnitude key of
+ * bs_prune_k: NaN above Inf; ties -> lower row-major index), 0 elsewhere.
+ *   W          device, M×K of dt, leading dimension ldw >= K;  mask  device out, M×K uint8
+ *   workspace  device scratch of at least bs_pattern_workspace_bytes(M, K, 0, 0) bytes
+ * A radix select over the keys (integer decisions only: the mask is exact).
+ * Errors: BS_ERR_ARG for bad sparsity, NULL pointers, ldw < K or a short workspace. */
+int bs_random_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, double sparsity, uint8_t* mask,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* bs_block_mask: block sparsity (Narang et al., Table brange's 4×4 / 8×8 / 16×16):
+ * bh×bw tiles in row-major tile order, each scored by "the maximum magnitude or the average magnitude
+ * of the weights within one block as a representative":
+ *   criterion 0: max |w| (as the magnitude key: NaN above Inf);
+ *   criterion 1: mean |w|, compared as the fp64 sum of |w| taken in row-major order inside the tile
+ *                (the mean times the fixed tile size; any NaN ranks the tile above all others).
+ * The bs_keep_count(#tiles, s) best tiles are kept whole (ties -> lower tile index); mask as above.
+ * Vector sparsity (Mao et al.; "a whole row or column ... as a basic pruning unit") is this call
+ * with bh = 1, bw = K (rows) or bh = M, bw = 1 (columns) and criterion 1.
+ * Errors: BS_ERR_SHAPE if M mod bh or K mod bw != 0; BS_ERR_ARG as bs_random_mask or criterion not 0/1. */
+int bs_block_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int64_t bh, int64_t bw,
+                  double sparsity, int criterion, uint8_t* mask, void* workspace, size_t workspace_bytes,
                   void* stream);
 
 /* bs_pack: permute canonical (vals, idx) into the device layout `layout` and narrow the indices
@@ -176,8 +230,14 @@ int bs_spmv_host(const bs_matrix* A, const void* x_host, void* y_host, void* x_d
  *   Y  device out, column n at Y + n·ldy (M elements each), i.e. torch [N, M]
  * Layout SPMM (128-row tiles): f16/bf16 with B dividing 64 run on the tensor cores (tcgen05.mma,
  * decompressed W tiles, fp32 accumulate in tensor memory); other cases use CUDA cores. Layout SPMV:
- * one SpMV per column. Column n of Y depends only on column n of X, with a fixed order of fp32
- * accumulation over K, so batch-sharded SpMM reproduces the unsharded columns.
+ * passes of up to 16 columns through the SpMV kernel (16-bit), one SpMV per column (f32). Layout
+ * SP24: the sparse tensor cores (tcgen05.mma.sp) at every N, including N = 1 (bs_spmv is the batch-1
+ * CUDA-core path; its order differs).
+ * Column n of Y depends only on column n of X, with a fixed order of fp32 accumulation over K that
+ * does not depend on N, so batch-sharded SpMM reproduces the unsharded columns bit for bit. The order
+ * does depend on the operand class: the tensor-core layouts need X rows 16-byte aligned with
+ * ldx % 8 == 0 (contiguous torch tensors with K % 8 == 0) and otherwise take a CUDA-core kernel;
+ * shards compared bit for bit must share that class.
  * Errors: BS_ERR_ARG if N < 1, ldx < K or ldy < M. */
 int bs_spmm(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, void* Y, int64_t ldy,
             void* stream);

@@ -2,7 +2,9 @@
 
 Every step of the path runs in the CUDA kernels behind the C ABI (include/bs.h). This module only
 marshals arguments: it turns torch CUDA tensors into device pointers and passes the current CUDA
-stream. There is no CPU fallback. If libbs.so is missing, importing this package raises.
+stream. There is no CPU fallback: libbs.so is loaded on first use (every entry point below), and if it is
+missing that call raises ImportError. Only the host-side helpers of `dist` (slice ranges, the shard
+policy) work without it.
 
     import paper_1811_00206_b200 as bs
     vals, idx, k = bs.prune(W, block=32, sparsity=0.9)    # Alg. 1 step
@@ -26,14 +28,16 @@ DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 LAYOUTS = {"spmv": 1, "spmm": 2, "sp24": 3}
 
 EXPORTS = ("bs_k_from_sparsity", "bs_packed_bytes", "bs_status_str", "bs_version", "bs_prune", "bs_prune_k",
-           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm", "bs_choose_layout", "bs_block_rank")
+           "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm", "bs_choose_layout", "bs_block_rank",
+           "bs_schedule_sparsity", "bs_keep_count", "bs_decode", "bs_pattern_workspace_bytes", "bs_random_mask",
+           "bs_block_mask")
 ACTS = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}  # bs_act (include/bs.h)
 SPMV_PDL, SPMV_W_STATIC = 1, 2  # bs_spmv_ex flags (include/bs.h)
 
 
 class BSError(RuntimeError):
     def __init__(self, status: int, where: str):
-        super().__init__(f"{where}: {_lib.bs_status_str(status).decode()} ({status})")
+        super().__init__(f"{where}: {lib().bs_status_str(status).decode()} ({status})")
         self.status = status
 
 
@@ -69,20 +73,35 @@ def _load() -> ctypes.CDLL:
     L.bs_spmv_fused.argtypes = [ctypes.POINTER(_Matrix), vp, vp, ci, vp, ctypes.c_uint, vp]
     L.bs_spmv_host.argtypes = [ctypes.POINTER(_Matrix), vp, vp, vp, vp, vp]
     L.bs_spmm.argtypes = [ctypes.POINTER(_Matrix), vp, i64, i64, vp, i64, vp]
+    L.bs_schedule_sparsity.argtypes = [ctypes.c_double, ci, ci]
+    L.bs_schedule_sparsity.restype = ctypes.c_double
+    L.bs_keep_count.argtypes = [i64, ctypes.c_double]
+    L.bs_keep_count.restype = i64
+    L.bs_decode.argtypes = [vp, vp, i64, i64, ci, ci, ci, vp, i64, vp]
+    L.bs_pattern_workspace_bytes.argtypes = [i64, i64, i64, i64]
+    L.bs_pattern_workspace_bytes.restype = ctypes.c_size_t
+    L.bs_random_mask.argtypes = [vp, ci, i64, i64, i64, ctypes.c_double, vp, vp, ctypes.c_size_t, vp]
+    L.bs_block_mask.argtypes = [vp, ci, i64, i64, i64, i64, i64, ctypes.c_double, ci, vp, vp, ctypes.c_size_t, vp]
+    for f in ("bs_decode", "bs_random_mask", "bs_block_mask"):
+        getattr(L, f).restype = ci
     for f in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm"):
         getattr(L, f).restype = ci
     return L
 
 
-_lib = _load()
+_LIB = None
 
 
 def lib() -> ctypes.CDLL:
-    return _lib
+    """libbs.so, loaded on first use (raises ImportError if it was not built)."""
+    global _LIB
+    if _LIB is None:
+        _LIB = _load()
+    return _LIB
 
 
 def version() -> str:
-    return _lib.bs_version().decode()
+    return lib().bs_version().decode()
 
 
 def _stream(device=None) -> int:
@@ -107,13 +126,34 @@ def _need_cuda(*ts):
             raise ValueError("tensors must live on a CUDA device (there is no CPU path)")
 
 
+def _same_device(A: "BSMatrix", *ts):
+    for t in ts:
+        if t is not None and A.packed.numel() and t.device != A.packed.device:
+            raise ValueError(f"tensor on {t.device} but the matrix lives on {A.packed.device}")
+
+
+def _check_out(out: torch.Tensor, A: "BSMatrix", shape: tuple):
+    """A caller-supplied output buffer: the kernel writes through its raw pointer, so its dtype, device,
+    size and strides must match exactly (a short buffer would be an out-of-bounds device write)."""
+    _need_cuda(out)
+    if out.dtype != A.dtype:
+        raise ValueError(f"out has dtype {out.dtype}, expected {A.dtype}")
+    if tuple(out.shape) != shape:
+        raise ValueError(f"out has shape {tuple(out.shape)}, expected {shape}")
+    if out.stride(-1) != 1 or (len(shape) == 1 and not out.is_contiguous()):
+        raise ValueError("out must have unit stride along M")
+    if len(shape) == 2 and shape[0] > 1 and out.stride(0) < shape[1]:
+        raise ValueError("out rows overlap (stride(0) < M)")
+    _same_device(A, out)
+
+
 def k_from_sparsity(block: int, sparsity: float) -> int:
     """k = lround((1 - s)·B)."""
-    return _lib.bs_k_from_sparsity(int(block), float(sparsity))
+    return lib().bs_k_from_sparsity(int(block), float(sparsity))
 
 
 def packed_bytes(M: int, K: int, block: int, k: int, dtype: torch.dtype, layout: str = "spmv") -> int:
-    return int(_lib.bs_packed_bytes(M, K, block, k, DTYPES[dtype], LAYOUTS[layout]))
+    return int(lib().bs_packed_bytes(M, K, block, k, DTYPES[dtype], LAYOUTS[layout]))
 
 
 @dataclass
@@ -165,7 +205,7 @@ def prune(W: torch.Tensor, block: int, sparsity: float | None = None, k: int | N
     vals = torch.empty((M, NB, max(k, 0)), dtype=W.dtype, device=W.device)
     idx = torch.empty((M, NB, max(k, 0)), dtype=torch.int16, device=W.device)
     with torch.cuda.device(W.device):
-        st = _lib.bs_prune_k(W.data_ptr(), _dt(W), M, K, W.stride(0), block, k, vals.data_ptr() if vals.numel() else None,
+        st = lib().bs_prune_k(W.data_ptr(), _dt(W), M, K, W.stride(0), block, k, vals.data_ptr() if vals.numel() else None,
                              idx.data_ptr() if idx.numel() else None, _stream(W.device))
     _check(st, "bs_prune_k")
     return vals, idx, k
@@ -175,12 +215,15 @@ def block_rank(W: torch.Tensor, block: int) -> torch.Tensor:
     """Every element's position in its block's magnitude order (bs_block_rank): uint8 [M, K]. The mask
     of a pruning step at any k is rank < k (Alg. 1's schedule without retraining)."""
     _need_cuda(W)
+    if W.dim() != 2:
+        raise ValueError("W must be a 2-D tensor")
+    dt = _dt(W)
     M, K = W.shape
     if W.stride(1) != 1:
         W = W.contiguous()
     rank = torch.empty((M, K), dtype=torch.uint8, device=W.device)
     with torch.cuda.device(W.device):
-        st = _lib.bs_block_rank(W.data_ptr(), DTYPES[W.dtype], M, K, W.stride(0), block, rank.data_ptr(),
+        st = lib().bs_block_rank(W.data_ptr(), dt, M, K, W.stride(0), block, rank.data_ptr(),
                                 _stream(W.device))
     _check(st, "bs_block_rank")
     return rank
@@ -188,7 +231,7 @@ def block_rank(W: torch.Tensor, block: int) -> torch.Tensor:
 
 def choose_layout(M: int, K: int, block: int, k: int, dtype: torch.dtype, batch: int) -> str:
     """bs_choose_layout: the layout bs_spmm runs fastest on for `batch` columns (include/bs.h)."""
-    code = _lib.bs_choose_layout(M, K, block, k, DTYPES[dtype], batch)
+    code = lib().bs_choose_layout(M, K, block, k, DTYPES[dtype], batch)
     if code < 0:
         raise ValueError("bs_choose_layout rejected the arguments")
     return {v: n for n, v in LAYOUTS.items()}[code]
@@ -209,7 +252,7 @@ def pack(vals: torch.Tensor, idx: torch.Tensor, K: int, block: int, layout: str 
         raise BSError(BS_ERR_UNSUPPORTED, "bs_packed_bytes")
     out = torch.empty(n, dtype=torch.uint8, device=vals.device)
     with torch.cuda.device(vals.device):
-        st = _lib.bs_pack(vals.data_ptr() if vals.numel() else None, idx.data_ptr() if idx.numel() else None, M, K,
+        st = lib().bs_pack(vals.data_ptr() if vals.numel() else None, idx.data_ptr() if idx.numel() else None, M, K,
                           block, k, _dt(vals), LAYOUTS[layout], out.data_ptr() if n else None, _stream(vals.device))
     _check(st, "bs_pack")
     return BSMatrix(M, K, block, k, vals.dtype, layout, out)
@@ -221,7 +264,7 @@ def unpack(A: BSMatrix):
     vals = torch.empty((A.M, NB, A.k), dtype=A.dtype, device=A.packed.device)
     idx = torch.empty((A.M, NB, A.k), dtype=torch.int16, device=A.packed.device)
     with torch.cuda.device(A.packed.device):
-        st = _lib.bs_unpack(A.packed.data_ptr() if A.packed.numel() else None, A.M, A.K, A.block, A.k, DTYPES[A.dtype], LAYOUTS[A.layout],
+        st = lib().bs_unpack(A.packed.data_ptr() if A.packed.numel() else None, A.M, A.K, A.block, A.k, DTYPES[A.dtype], LAYOUTS[A.layout],
                             vals.data_ptr() if vals.numel() else None, idx.data_ptr() if idx.numel() else None,
                             _stream(A.packed.device))
     _check(st, "bs_unpack")
@@ -237,7 +280,12 @@ def spmv(A: BSMatrix, x: torch.Tensor, out: torch.Tensor | None = None, flags: i
     _need_cuda(x)
     if x.dtype != A.dtype or x.numel() != A.K:
         raise ValueError("x must have A.K elements of A.dtype")
+    _same_device(A, x)
     x = x.contiguous()
+    if out is not None:
+        _check_out(out, A, (A.M,))
+        if out.device != x.device:
+            raise ValueError("out and x must live on the same device")
     y = out if out is not None else torch.empty(A.M, dtype=A.dtype, device=x.device)
     m = A.cstruct()
     with torch.cuda.device(x.device):
@@ -246,16 +294,17 @@ def spmv(A: BSMatrix, x: torch.Tensor, out: torch.Tensor | None = None, flags: i
                 raise ValueError(f"act must be one of {sorted(k for k in ACTS if k)}")
             if bias is not None:
                 _need_cuda(bias)
+                _same_device(A, bias)
                 if bias.dtype != A.dtype or bias.numel() != A.M:
                     raise ValueError("bias must have A.M elements of A.dtype")
                 bias = bias.contiguous()
-            st = _lib.bs_spmv_fused(ctypes.byref(m), x.data_ptr(), bias.data_ptr() if bias is not None else None,
+            st = lib().bs_spmv_fused(ctypes.byref(m), x.data_ptr(), bias.data_ptr() if bias is not None else None,
                                     ACTS[act], y.data_ptr(), bs_flags_default() if flags is None else flags,
                                     _stream(x.device))
         elif flags is None:
-            st = _lib.bs_spmv(ctypes.byref(m), x.data_ptr(), y.data_ptr(), _stream(x.device))
+            st = lib().bs_spmv(ctypes.byref(m), x.data_ptr(), y.data_ptr(), _stream(x.device))
         else:
-            st = _lib.bs_spmv_ex(ctypes.byref(m), x.data_ptr(), y.data_ptr(), flags, _stream(x.device))
+            st = lib().bs_spmv_ex(ctypes.byref(m), x.data_ptr(), y.data_ptr(), flags, _stream(x.device))
     _check(st, "bs_spmv")
     return y
 
@@ -268,9 +317,18 @@ def bs_flags_default() -> int:
 def spmv_host(A: BSMatrix, x_host: torch.Tensor, y_host: torch.Tensor, x_dev: torch.Tensor, y_dev: torch.Tensor):
     """End-to-end product through the C ABI with host buffers: H2D(x) -> SpMV -> D2H(y), enqueued on the
     current stream (bs_spmv_host). y_host is valid after the stream synchronises."""
+    if x_host.dtype != A.dtype or y_host.dtype != A.dtype or x_host.numel() < A.K or y_host.numel() < A.M:
+        raise ValueError("x_host / y_host must hold A.K / A.M elements of A.dtype")
+    if x_host.is_cuda or y_host.is_cuda or not (x_host.is_contiguous() and y_host.is_contiguous()):
+        raise ValueError("x_host and y_host must be contiguous host tensors")
+    _need_cuda(x_dev)
+    _check_out(y_dev, A, (A.M,))
+    if x_dev.dtype != A.dtype or x_dev.numel() != A.K or not x_dev.is_contiguous():
+        raise ValueError("x_dev must be a contiguous device buffer of A.K elements of A.dtype")
+    _same_device(A, x_dev)
     m = A.cstruct()
     with torch.cuda.device(x_dev.device):
-        st = _lib.bs_spmv_host(ctypes.byref(m), x_host.data_ptr(), y_host.data_ptr(), x_dev.data_ptr(),
+        st = lib().bs_spmv_host(ctypes.byref(m), x_host.data_ptr(), y_host.data_ptr(), x_dev.data_ptr(),
                                y_dev.data_ptr(), _stream(x_dev.device))
     _check(st, "bs_spmv_host")
 
@@ -280,10 +338,120 @@ def spmm(A: BSMatrix, X: torch.Tensor, out: torch.Tensor | None = None) -> torch
     _need_cuda(X)
     if X.dim() != 2 or X.shape[1] != A.K or X.dtype != A.dtype or X.stride(1) != 1:
         raise ValueError("X must be [N, K] of A.dtype with unit column stride")
+    _same_device(A, X)
     N = X.shape[0]
+    if out is not None:
+        _check_out(out, A, (N, A.M))
+        if out.device != X.device:
+            raise ValueError("out and X must live on the same device")
     Y = out if out is not None else torch.empty((N, A.M), dtype=A.dtype, device=X.device)
     m = A.cstruct()
     with torch.cuda.device(X.device):
-        st = _lib.bs_spmm(ctypes.byref(m), X.data_ptr(), N, X.stride(0), Y.data_ptr(), Y.stride(0), _stream(X.device))
+        st = lib().bs_spmm(ctypes.byref(m), X.data_ptr(), N, X.stride(0), Y.data_ptr(), Y.stride(0), _stream(X.device))
     _check(st, "bs_spmm")
     return Y
+
+
+# ---------------------------------------------------------------- Alg. 1's schedule and the comparison patterns
+
+def schedule(target: float, n: int, i: int) -> float:
+    """GraduallyIncrease (Alg. 1, P:114/P:131): s_i = target·(1 − (1 − i/n)^3) (bs_schedule_sparsity)."""
+    v = lib().bs_schedule_sparsity(float(target), int(n), int(i))
+    if v < 0:
+        raise ValueError("schedule needs n >= 1, 0 <= i <= n and 0 <= target < 1")
+    return v
+
+
+def keep_count(n: int, sparsity: float) -> int:
+    """Units kept at sparsity s: lround((1 − s)·n) (bs_keep_count)."""
+    return int(lib().bs_keep_count(int(n), float(sparsity)))
+
+
+def decode(vals: torch.Tensor, idx: torch.Tensor, K: int, block: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Dense W_bs (Alg. 1's pruned matrix M_p) from canonical (vals, idx) (bs_decode)."""
+    _need_cuda(vals, idx)
+    M, NB, k = vals.shape
+    vals = vals.contiguous()
+    idx = idx.contiguous()
+    if out is None:
+        out = torch.empty((M, K), dtype=vals.dtype, device=vals.device)
+    else:
+        _need_cuda(out)
+        if out.dtype != vals.dtype or tuple(out.shape) != (M, K) or out.stride(1) != 1 or out.device != vals.device:
+            raise ValueError("out must be [M, K] of vals.dtype on vals.device with unit column stride")
+    with torch.cuda.device(vals.device):
+        st = lib().bs_decode(vals.data_ptr() if vals.numel() else None, idx.data_ptr() if idx.numel() else None, M, K,
+                             block, k, _dt(vals), out.data_ptr(), out.stride(0), _stream(vals.device))
+    _check(st, "bs_decode")
+    return out
+
+
+def prune_dense(W: torch.Tensor, block: int, sparsity: float | None = None, k: int | None = None,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """One pruning iteration of Alg. 1 on a dense matrix: W with all but the k largest-magnitude entries of
+    every block set to +0 (bs_prune_k + bs_decode). out=W prunes in place."""
+    vals, idx, k = prune(W, block, sparsity=sparsity, k=k)
+    return decode(vals, idx, W.shape[1], block, out=out)
+
+
+def gradual_prune(W: torch.Tensor, block: int, target: float, n: int, retrain=None):
+    """Alg. 1: n pruning iterations at the GraduallyIncrease sparsities s_1..s_n (schedule),
+    each followed by ``retrain(W)`` if given (the paper's "pruning followed by a retraining is one
+    iteration"; the callback may update W in place, pruned entries must stay zero for the pattern
+    to hold). Works on a copy of W; returns (M_p, [k_1..k_n]). Without retraining the survivors nest and
+    M_p equals a single step at the target."""
+    cur = W.clone()
+    ks = []
+    for i in range(1, n + 1):
+        k = k_from_sparsity(block, schedule(target, n, i))
+        prune_dense(cur, block, k=k, out=cur)
+        ks.append(k)
+        if retrain is not None:
+            retrain(cur)
+    return cur, ks
+
+
+def _workspace(M: int, K: int, bh: int, bw: int, device) -> torch.Tensor:
+    n = int(lib().bs_pattern_workspace_bytes(M, K, bh, bw))
+    if n == 0:
+        raise BSError(BS_ERR_SHAPE, "bs_pattern_workspace_bytes")
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def random_mask(W: torch.Tensor, sparsity: float) -> torch.Tensor:
+    """Random sparsity (global magnitude pruning): uint8 keep mask [M, K] (bs_random_mask)."""
+    _need_cuda(W)
+    if W.dim() != 2 or W.stride(1) != 1:
+        raise ValueError("W must be a 2-D tensor with unit column stride")
+    M, K = W.shape
+    mask = torch.empty((M, K), dtype=torch.uint8, device=W.device)
+    ws = _workspace(M, K, 0, 0, W.device)
+    with torch.cuda.device(W.device):
+        st = lib().bs_random_mask(W.data_ptr(), _dt(W), M, K, W.stride(0), float(sparsity), mask.data_ptr(),
+                                  ws.data_ptr(), ws.numel(), _stream(W.device))
+    _check(st, "bs_random_mask")
+    return mask
+
+
+def block_mask(W: torch.Tensor, bh: int, bw: int, sparsity: float, criterion: str = "max") -> torch.Tensor:
+    """Block sparsity: bh×bw tiles scored by max or mean |w|, the best lround((1−s)·#tiles)
+    kept whole. uint8 keep mask [M, K] (bs_block_mask)."""
+    _need_cuda(W)
+    if W.dim() != 2 or W.stride(1) != 1:
+        raise ValueError("W must be a 2-D tensor with unit column stride")
+    M, K = W.shape
+    crit = {"max": 0, "mean": 1}[criterion]
+    mask = torch.empty((M, K), dtype=torch.uint8, device=W.device)
+    ws = _workspace(M, K, bh, bw, W.device)
+    with torch.cuda.device(W.device):
+        st = lib().bs_block_mask(W.data_ptr(), _dt(W), M, K, W.stride(0), int(bh), int(bw), float(sparsity), crit,
+                                 mask.data_ptr(), ws.data_ptr(), ws.numel(), _stream(W.device))
+    _check(st, "bs_block_mask")
+    return mask
+
+
+def vector_mask(W: torch.Tensor, sparsity: float, axis: str = "row") -> torch.Tensor:
+    """Vector sparsity: whole rows (axis="row") or columns scored by mean |w| (bs_block_mask with a
+    1×K or M×1 tile)."""
+    M, K = W.shape
+    return block_mask(W, 1, K, sparsity, "mean") if axis == "row" else block_mask(W, M, 1, sparsity, "mean")

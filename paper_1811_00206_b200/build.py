@@ -26,7 +26,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", f"-I{INCLUDE}", f"-I{CSRC}"]
 
-SOURCES = ["bs_api.cu", "prune.cu", "pack.cu", "spmv.cu", "spmv_f16.cu", "spmv_bf16.cu", "spmv_f16_batch.cu", "spmv_bf16_batch.cu", "spmv_f32.cu", "spmm.cu", "spmm24.cu"]
+SOURCES = ["bs_api.cu", "prune.cu", "pack.cu", "spmv.cu", "spmv_f16.cu", "spmv_bf16.cu", "spmv_f16_batch.cu", "spmv_bf16_batch.cu", "spmv_f32.cu", "spmm.cu", "spmm24.cu", "patterns.cu"]
 
 
 def _deps_mtime() -> float:

@@ -1,7 +1,9 @@
 // bs_api.cu: the C ABI of libbs.so (include/bs.h). It validates arguments and dispatches to the
 // kernels. It never allocates device memory and never synchronises.
 #include <math.h>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "bs_common.cuh"
 
@@ -27,6 +29,27 @@ const DevProps& dev_props() {
     have[dev] = true;
   }
   return props[dev];
+}
+
+int prepare_func(const void* func, cudaError_t* err) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int optin = dev_props().smem_optin;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({func, dev});
+  if (it != done.end()) return it->second;
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, func);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  if (e != cudaSuccess) {
+    *err = e;
+    return -1;
+  }
+  done[{func, dev}] = (int)fa.sharedSizeBytes;
+  return (int)fa.sharedSizeBytes;
 }
 
 }  // namespace bsk
@@ -156,6 +179,51 @@ int bs_unpack(const void* packed, int64_t M, int64_t K, int block, int k, int dt
   return from_cuda(bsk_launch_unpack(packed, g, vals, idx, (cudaStream_t)stream));
 }
 
+double bs_schedule_sparsity(double target, int n, int i) {
+  if (n < 1 || i < 0 || i > n || !(target >= 0.0) || !(target < 1.0)) return -1.0;
+  const double u = 1.0 - (double)i / (double)n;
+  return target * (1.0 - u * u * u);
+}
+
+int64_t bs_keep_count(int64_t n, double sparsity) {
+  if (n < 0 || !(sparsity >= 0.0) || !(sparsity < 1.0)) return -1;
+  return (int64_t)llround((1.0 - sparsity) * (double)n);
+}
+
+int bs_decode(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int block, int k, int dt, void* W,
+              int64_t ldw, void* stream) {
+  if (!valid_dt(dt)) return BS_ERR_DTYPE;
+  int st = check_shape(M, K, block, k);
+  if (st) return st;
+  if (!W || ldw < K || (k > 0 && (!vals || !idx))) return BS_ERR_ARG;
+  return from_cuda(bsk_launch_decode(vals, idx, M, K, block, k, dt, W, ldw, (cudaStream_t)stream));
+}
+
+size_t bs_pattern_workspace_bytes(int64_t M, int64_t K, int64_t bh, int64_t bw) {
+  if (M < 1 || K < 1 || bh < 0 || bw < 0 || (bh > 0 && M % bh) || (bw > 0 && K % bw)) return 0;
+  return bsk_pattern_workspace_bytes(M, K, bh, bw);
+}
+
+int bs_random_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, double sparsity, uint8_t* mask,
+                   void* workspace, size_t workspace_bytes, void* stream) {
+  if (!valid_dt(dt)) return BS_ERR_DTYPE;
+  if (M < 1 || K < 1) return BS_ERR_SHAPE;
+  if (!W || !mask || !workspace || ldw < K || !(sparsity >= 0.0) || !(sparsity < 1.0)) return BS_ERR_ARG;
+  if (workspace_bytes < bsk_pattern_workspace_bytes(M, K, 0, 0)) return BS_ERR_ARG;
+  return from_cuda(bsk_launch_random_mask(W, dt, M, K, ldw, sparsity, mask, workspace, (cudaStream_t)stream));
+}
+
+int bs_block_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int64_t bh, int64_t bw, double sparsity,
+                  int criterion, uint8_t* mask, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!valid_dt(dt)) return BS_ERR_DTYPE;
+  if (M < 1 || K < 1 || bh < 1 || bw < 1 || M % bh || K % bw) return BS_ERR_SHAPE;
+  if (!W || !mask || !workspace || ldw < K || !(sparsity >= 0.0) || !(sparsity < 1.0)) return BS_ERR_ARG;
+  if (criterion != 0 && criterion != 1) return BS_ERR_ARG;
+  if (workspace_bytes < bsk_pattern_workspace_bytes(M, K, bh, bw)) return BS_ERR_ARG;
+  return from_cuda(
+      bsk_launch_block_mask(W, dt, M, K, ldw, bh, bw, sparsity, criterion, mask, workspace, (cudaStream_t)stream));
+}
+
 int bs_spmv_ex(const bs_matrix* A, const void* x, void* y, unsigned flags, void* stream) {
   bsk::Geom g;
   int st = matrix_geom(A, &g);
@@ -163,7 +231,7 @@ int bs_spmv_ex(const bs_matrix* A, const void* x, void* y, unsigned flags, void*
   if (!x || !y) return BS_ERR_ARG;
   if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC)) return BS_ERR_ARG;
   if (g.layout == BS_LAYOUT_SP24)  // 2:4: CUDA-core path with 2-bit metadata
-    return from_cuda(bsk_launch_sp24(g, A->packed, x, 1, g.K, y, g.M, (cudaStream_t)stream));
+    return from_cuda(bsk_launch_sp24(g, A->packed, x, 1, g.K, y, g.M, (cudaStream_t)stream, true));
   if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;  // SPMM tiles feed bs_spmm
   return from_cuda(bsk_launch_spmv(g, A->packed, x, y, flags, (cudaStream_t)stream));
 }
@@ -206,7 +274,7 @@ int bs_spmm(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, void* Y, 
   if (st) return st;
   if (!X || !Y || N < 1 || ldx < g.K || ldy < g.M) return BS_ERR_ARG;
   if (g.layout == BS_LAYOUT_SP24)  // 2:4: sparse tensor cores (tcgen05.mma.sp) or CUDA cores
-    return from_cuda(bsk_launch_sp24(g, A->packed, X, N, ldx, Y, ldy, (cudaStream_t)stream));
+    return from_cuda(bsk_launch_sp24(g, A->packed, X, N, ldx, Y, ldy, (cudaStream_t)stream, false));
   cudaError_t e = bsk_launch_spmm(g, A->packed, X, N, ldx, Y, ldy, (cudaStream_t)stream);
   if (e != cudaErrorNotSupported) return from_cuda(e);
   // SPMV layout: passes of 8 batch columns through the SpMV kernel (16-bit), or one SpMV per column

@@ -98,6 +98,12 @@ struct DevProps {
 };
 const DevProps& dev_props();
 
+// Opts kernel `func` into the current device's largest dynamic shared memory allocation and returns
+// its static shared memory bytes. Done once per (function, device) under the library mutex: the
+// attribute belongs to the device context, so a process that drives several GPUs sets it on each.
+// Returns a negative value (and leaves *err set) on failure.
+int prepare_func(const void* func, cudaError_t* err);
+
 // Split-K of the tensor-core SpMM kernels: at least this many K chunks per CTA (measured defaults:
 // K6 3, K5 6; BS_SPLITK_MIN_CHUNKS overrides both for tuning). It depends on nothing but the
 // environment, so the split (and the summation order) stays a function of M and K only.
@@ -118,13 +124,22 @@ cudaError_t bsk_launch_block_rank(const void* W, int dt, int64_t M, int64_t K, i
                                   cudaStream_t s);
 cudaError_t bsk_launch_pack(const void* vals, const uint16_t* idx, const bsk::Geom& g, void* packed,
                             cudaStream_t s);
+cudaError_t bsk_launch_decode(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int B, int k, int dt,
+                              void* W, int64_t ldw, cudaStream_t s);
+size_t bsk_pattern_workspace_bytes(int64_t M, int64_t K, int64_t bh, int64_t bw);
+cudaError_t bsk_launch_random_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, double sparsity,
+                                   uint8_t* mask, void* ws, cudaStream_t s);
+cudaError_t bsk_launch_block_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int64_t bh, int64_t bw,
+                                  double sparsity, int criterion, uint8_t* mask, void* ws, cudaStream_t s);
 cudaError_t bsk_launch_unpack(const void* packed, const bsk::Geom& g, void* vals, uint16_t* idx,
                               cudaStream_t s);
 cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, unsigned flags,
                             cudaStream_t s, const void* bias = nullptr, int act = 0);
 cudaError_t bsk_launch_spmv_batch(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,
                                   void* Y, int64_t ldy, cudaStream_t s);
+// spmv: the batch-1 product of bs_spmv (CUDA cores, HBM-bound). Otherwise the batched product of bs_spmm,
+// whose per-column summation order does not depend on N (tensor cores whenever the operands allow).
 cudaError_t bsk_launch_sp24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
-                            int64_t ldy, cudaStream_t s);
+                            int64_t ldy, cudaStream_t s, bool spmv);
 cudaError_t bsk_launch_spmm(const bsk::Geom& g, const void* packed, const void* X, int64_t N,
                             int64_t ldx, void* Y, int64_t ldy, cudaStream_t s);

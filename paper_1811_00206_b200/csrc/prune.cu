@@ -17,38 +17,11 @@
 #include <cuda_fp16.h>
 
 #include "bs_common.cuh"
+#include "bs_keys.cuh"
 
 namespace {
 
-template <int DT>
-struct KeyOf;
-template <>
-struct KeyOf<BS_F32> {
-  using raw_t = uint32_t;
-  static constexpr int kBits = 31;
-  __device__ static uint32_t key(uint32_t u) {
-    uint32_t a = u & 0x7fffffffu;
-    return a > 0x7f800000u ? 0x7f800001u : a;
-  }
-};
-template <>
-struct KeyOf<BS_F16> {
-  using raw_t = uint16_t;
-  static constexpr int kBits = 15;
-  __device__ static uint32_t key(uint32_t u) {
-    uint32_t a = u & 0x7fffu;
-    return a > 0x7c00u ? 0x7c01u : a;
-  }
-};
-template <>
-struct KeyOf<BS_BF16> {
-  using raw_t = uint16_t;
-  static constexpr int kBits = 15;
-  __device__ static uint32_t key(uint32_t u) {
-    uint32_t a = u & 0x7fffu;
-    return a > 0x7f80u ? 0x7f81u : a;
-  }
-};
+using bsk::KeyOf;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -319,7 +292,7 @@ __global__ void __launch_bounds__(256) prune_thread(const typename KeyOf<DT>::ra
 template <int DT, int B>
 __global__ void __launch_bounds__(256) block_rank_kernel(const typename KeyOf<DT>::raw_t* __restrict__ W,
                                                          int64_t M, int64_t NB, int64_t ldw,
-                                                         uint8_t* __restrict__ rank, bool vec) {
+                                                         uint8_t* __restrict__ rank, bool vec, bool rvec) {
   const int64_t nblocks = M * NB;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t K = NB * B;
@@ -358,9 +331,11 @@ __global__ void __launch_bounds__(256) block_rank_kernel(const typename KeyOf<DT
       for (int i = 0; i < B; ++i) c += (key[i] > key[j]) || (i < j && key[i] == key[j]);
       packed[j >> 2] |= (uint32_t)c << (8 * (j & 3));
     }
-    if constexpr (B % 4 == 0) {  // the rank row is 4-byte aligned (K and B multiples of 4)
+    bool wide = false;
+    if constexpr (B % 4 == 0) wide = rvec;  // 32-bit stores when `rank` is 4-byte aligned (K, B multiples of 4)
+    if (wide) {
 #pragma unroll
-      for (int q = 0; q < B / 4; ++q) ((uint32_t*)dst)[q] = packed[q];
+      for (int q = 0; q < (B + 3) / 4; ++q) ((uint32_t*)dst)[q] = packed[q];
     } else {
 #pragma unroll
       for (int j = 0; j < B; ++j) dst[j] = (uint8_t)(packed[j >> 2] >> (8 * (j & 3)));
@@ -376,7 +351,8 @@ cudaError_t launch_block_rank_t(const void* W, int64_t M, int64_t K, int64_t ldw
   const int sms = bsk::dev_props().sms;
   blocks = blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8;
   const bool vec = ((uintptr_t)W & 15) == 0 && (ldw * (int64_t)sizeof(raw_t)) % 16 == 0;
-  auto run = [&](auto kern) { kern<<<(unsigned)blocks, 256, 0, s>>>((const raw_t*)W, M, NB, ldw, rank, vec); };
+  const bool rvec = ((uintptr_t)rank & 3) == 0;  // bs.h does not require an aligned `rank`
+  auto run = [&](auto kern) { kern<<<(unsigned)blocks, 256, 0, s>>>((const raw_t*)W, M, NB, ldw, rank, vec, rvec); };
   switch (B) {
     case 32: run(block_rank_kernel<DT, 32>); break;
     case 16: run(block_rank_kernel<DT, 16>); break;

@@ -355,16 +355,9 @@ cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int
   a.blob_max = (int)(bsk::align_up((int64_t)BM * g.V * g.k * 2, 16) + bsk::align_up((int64_t)BM * g.V * g.k, 16));
   a.S = split_k(g.P, g.NBf);
   auto kern = spmm_tc_kernel<DT>;
-  static int static_smem = -1;
-  if (static_smem < 0) {
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             bsk::dev_props().smem_optin - (int)fa.sharedSizeBytes);
-    if (e != cudaSuccess) return e;
-    static_smem = (int)fa.sharedSizeBytes;
-  }
+  cudaError_t perr = cudaSuccess;
+  const int static_smem = bsk::prepare_func((const void*)kern, &perr);
+  if (static_smem < 0) return perr;
   // NA dense A tiles + NSB stages of (X tile, blob): BN as large as 4 stages allow with NA = 4 (<= 256);
   // NA = 8 when 8 stages still fit (more chunks in flight hide the MMA completion latency), else 4.
   const int64_t avail = bsk::dev_props().smem_optin - static_smem - 1024;  // 1024: alignment slack

@@ -327,14 +327,10 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   if (S < 1) S = 1;
   a.S = (int)S;
   auto kern = spmm24_kernel<DT>;
-  static int configured = 0;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         bsk::dev_props().smem_optin - 1024);
-    if (e != cudaSuccess) return e;
-    configured = 1;
-  }
-  if (smem > bsk::dev_props().smem_optin - 1024) return cudaErrorNotSupported;
+  cudaError_t perr = cudaSuccess;
+  const int static_smem = bsk::prepare_func((const void*)kern, &perr);
+  if (static_smem < 0) return perr;
+  if (smem > bsk::dev_props().smem_optin - static_smem) return cudaErrorNotSupported;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(tiles * S), (unsigned)((N + BN - 1) / BN));
   cfg.blockDim = dim3(kThreads);
@@ -391,17 +387,16 @@ bool bsk_make_map_2d(CUtensorMap* m, int dt, const void* base, int64_t cols, int
          CUDA_SUCCESS;
 }
 
-// Y = W·X for W in SP24 layout. The tensor path needs f16/bf16, K % 128 == 0, 16-byte aligned X rows and
-// N >= 2 (batch 1 is memory-bound: the CUDA-core kernel serves it).
+// Y = W·X for W in SP24 layout.
+//   spmv (bs_spmv, N = 1): the HBM-bound CUDA-core SpMV with 16-byte loads.
+//   otherwise (bs_spmm): the sparse tensor cores whenever the operands allow it (f16/bf16, K % 128 == 0,
+//   16-byte aligned X rows), at every N including 1, so a column's summation order does not depend on N
+//   and batch-sharded products reproduce the unsharded columns (include/bs.h). Operands the tensor path
+//   cannot take (f32, unaligned X) use the scalar CUDA-core kernel at every N.
 cudaError_t bsk_launch_sp24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
-                            int64_t ldy, cudaStream_t s) {
-  const bool tc = g.es == 2 && g.K % KCH == 0 && N >= 2 && ((uintptr_t)X & 15) == 0 && (ldx % 8) == 0;
-  if (tc) {
-    cudaError_t e = g.dt == BS_BF16 ? launch_tc24<BS_BF16>(g, packed, X, N, ldx, Y, ldy, s)
-                                    : launch_tc24<BS_F16>(g, packed, X, N, ldx, Y, ldy, s);
-    if (e != cudaErrorNotSupported) return e;
-  }
-  if (N == 1 && g.es == 2 && g.K % 16 == 0 && ((uintptr_t)X & 15) == 0) {  // batch 1: HBM-bound SpMV
+                            int64_t ldy, cudaStream_t s, bool spmv) {
+  const bool aligned = ((uintptr_t)X & 15) == 0;
+  if (spmv && g.es == 2 && g.K % 16 == 0 && aligned) {  // batch 1: HBM-bound SpMV
     const uint8_t* base = (const uint8_t*)packed;
     int64_t blocks = (g.M + 7) / 8;
     if (blocks > (int64_t)bsk::dev_props().sms * 8) blocks = (int64_t)bsk::dev_props().sms * 8;
@@ -409,6 +404,12 @@ cudaError_t bsk_launch_sp24(const bsk::Geom& g, const void* packed, const void* 
     kern<<<(unsigned)blocks, 256, 0, s>>>((const uint16_t*)(base + g.offA), base + g.offB, (const uint16_t*)X,
                                           (uint16_t*)Y, g.M, g.K);
     return cudaGetLastError();
+  }
+  const bool tc = !spmv && g.es == 2 && g.K % KCH == 0 && aligned && (ldx % 8) == 0;
+  if (tc) {
+    cudaError_t e = g.dt == BS_BF16 ? launch_tc24<BS_BF16>(g, packed, X, N, ldx, Y, ldy, s)
+                                    : launch_tc24<BS_F16>(g, packed, X, N, ldx, Y, ldy, s);
+    if (e != cudaErrorNotSupported) return e;
   }
   switch (g.dt) {
     case BS_F32: return launch_cc24<BS_F32>(g, packed, X, N, ldx, Y, ldy, s);

@@ -753,17 +753,11 @@ cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int Q = StageSteps<V, ES>::value * QM;
   constexpr int SB = Q * (32 * V * ES + (IS == 5 ? 160 : 32 * V * IS));
-  static int static_smem = -1;  // per instantiation: static smem (the mbarriers)
   auto kern = spmv_kernel<DT, V, IS, Q, BT, MULTI, NT, NV>;
   const auto& dp = bsk::dev_props();
-  if (static_smem < 0) {
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dp.smem_optin - (int)fa.sharedSizeBytes);
-    if (e != cudaSuccess) return e;
-    static_smem = (int)fa.sharedSizeBytes;
-  }
+  cudaError_t perr = cudaSuccess;
+  const int static_smem = bsk::prepare_func((const void*)kern, &perr);
+  if (static_smem < 0) return perr;
   SpmvArgs a = a0;
   a.tail_rows = 0;
   if (a.T > 0 && a.k > 0) {  // whole rows of tail per ring stage (32 bytes of alignment slack)

@@ -1,7 +1,9 @@
 """World-size-2 gloo tests (CPU) of the multi-GPU host logic: row slices, padding, gather order, batch split.
 
 The local product is injected (`local_fn`) with an fp64-oracle stand-in, because there is no GPU here. On the
-GPU the same classes call the CUDA kernels and NCCL (bench.py --gpus N)."""
+GPU the same classes call the CUDA kernels and NCCL (bench.py --gpus N). Importing
+paper_1811_00206_b200.dist does not load libbs.so (the package loads it on first use), so these tests
+run on a checkout without the CUDA build."""
 import os
 import socket
 

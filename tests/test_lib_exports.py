@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared_symbols():
     src = open(os.path.join(ROOT, "include", "bs.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(bs_[a-z0-9_]+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|double|size_t|const char\*)\s+(bs_[a-z0-9_]+)\s*\(", src, re.M)))
 
 
 @pytest.fixture(scope="module")
@@ -88,3 +88,18 @@ def test_no_oracle_in_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text and "liboracle" not in text, f
+
+
+def test_schedule_and_keep_count_match_oracle(bs):
+    """Host helpers of Alg. 1's schedule (bs_schedule_sparsity, bs_keep_count) agree with the oracle."""
+    for target in (0.0, 0.5, 0.875, 0.9, 0.97):
+        for n in (1, 4, 10, 33):
+            for i in range(n + 1):
+                assert bs.schedule(target, n, i) == oracle.schedule(target, n, i)
+    with pytest.raises(ValueError):
+        bs.schedule(0.9, 10, 11)
+    for n in (1, 7, 64, 4096 * 4096, 65536 * 65536):
+        for s in (0.0, 0.3, 0.5, 0.9, 0.97):
+            assert bs.keep_count(n, s) == oracle.keep_count(n, s)
+    assert bs.lib().bs_pattern_workspace_bytes(64, 64, 8, 8) > bs.lib().bs_pattern_workspace_bytes(64, 64, 0, 0) > 0
+    assert bs.lib().bs_pattern_workspace_bytes(64, 64, 7, 8) == 0

@@ -12,7 +12,7 @@ import synth  # noqa: E402
 
 if len(sys.argv) > 1:
     bs.LIB_PATH = sys.argv[1]
-    bs._lib = bs._load()
+    bs._LIB = bs._load()
 for name, M, K, dt in (("big", 65536, 65536, "f16"), ("fc6", 4096, 25088, "f16"), ("fc6_f32", 4096, 25088, "f32")):
     W = synth.matrix(M, K, dt, seed=1, device="cuda")
     for k in (3, 8, 16, 1):

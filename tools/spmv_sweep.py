@@ -24,7 +24,7 @@ def child():
     import synth
     if os.environ.get("BS_LIB"):  # A/B runs against another build of the same ABI
         bs.LIB_PATH = os.environ["BS_LIB"]
-        bs._lib = bs._load()
+        bs._LIB = bs._load()
     dev = torch.device("cuda", 0)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     shapes = [s for s in SHAPES if s[0] in os.environ.get("SHAPES", "big,fc6,fc7,ptb,ctc_ih,ctc_hh").split(",")]

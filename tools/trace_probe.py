@@ -35,7 +35,7 @@ if __name__ == "__main__":
     name, s = sys.argv[1], float(sys.argv[2])
     M, K = SH[name]
     bs.LIB_PATH = LIB  # swap in the traced library (same ABI)
-    bs._lib = bs._load()
+    bs._LIB = bs._load()
     W = synth.matrix(M, K, "f16", seed=1, device="cuda")
     x = synth.vector(K, "f16", seed=2, device="cuda")
     v, i, k = bs.prune(W, 32, sparsity=s)
@@ -54,7 +54,7 @@ if __name__ == "__main__":
     torch.cuda.synchronize()
     n = 148 * 16 * 16
     buf = (ctypes.c_ulonglong * n)()
-    bs._lib.bs_trace_read(ctypes.byref(buf), n)
+    bs.lib().bs_trace_read(ctypes.byref(buf), n)
     t = np.frombuffer(buf, dtype=np.uint64).reshape(148, 16, 16).astype(np.int64)
     t0 = t[:, :, 0][t[:, :, 0] > 0].min()
     rel = np.where(t > 0, t - t0, -1)
