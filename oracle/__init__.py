@@ -86,6 +86,9 @@ def lib() -> ctypes.CDLL:
         L.orc_block_mask.argtypes = [_vp, ctypes.c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, ctypes.c_double,
                                      ctypes.c_int, _vp]
         L.orc_block_mask.restype = ctypes.c_int
+        L.orc_lstm_cell.argtypes = [_vp, _vp, ctypes.c_int, _c_i64, _c_i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp,
+                                    _vp, _vp, _vp, _vp]
+        L.orc_lstm_cell.restype = ctypes.c_int
         L.orc_elem.argtypes = [_vp, ctypes.c_int, _c_i64]
         L.orc_elem.restype = ctypes.c_double
         _lib = L
@@ -259,6 +262,27 @@ def to_double(a: np.ndarray, dt: int) -> np.ndarray:
     L = lib()
     p = _ptr(flat)
     return np.array([L.orc_elem(p, dt, i) for i in range(flat.size)], dtype=np.float64).reshape(a.shape)
+
+
+def lstm_cell(vals, idx, dt, M, K, block, k, x, pre, bias, c_prev):
+    """One LSTM step with balanced-sparse gate rows interleaved (row 4j+g = gate g of unit j; i, f, g, o):
+    z = W_bs·x + pre + bias (Eq. 1 with its +B), c = f·c_prev + i·g, h = o·tanh(c), fp64 (orc_lstm_cell).
+    pre / bias: M elements of dt or None. c_prev: M/4 floats. Returns (h, c, zbound) as float64 arrays."""
+    vals = _check(vals, dt)
+    x = _check(x, dt)
+    idx = np.ascontiguousarray(idx, dtype=np.uint16)
+    H = M // 4
+    cp = np.ascontiguousarray(c_prev, dtype=np.float64)
+    h = np.zeros(H, dtype=np.float64)
+    c = np.zeros(H, dtype=np.float64)
+    zb = np.zeros(M, dtype=np.float64)
+    pp = _ptr(_check(pre, dt)) if pre is not None else None
+    bp = _ptr(_check(bias, dt)) if bias is not None else None
+    keep = (pre, bias)  # noqa: F841 (the arrays stay alive through the call)
+    if lib().orc_lstm_cell(_ptr(vals), _ptr(idx), dt, M, K, block, k, _ptr(x), pp, bp, _ptr(cp), _ptr(h), _ptr(c),
+                           _ptr(zb)) != 0:
+        raise ValueError("orc_lstm_cell rejected the arguments")
+    return h, c, zb
 
 
 def schedule(target: float, n: int, i: int) -> float:

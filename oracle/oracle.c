@@ -591,6 +591,43 @@ int orc_spmv_act(const void* vals, const uint16_t* idx, int dt, int64_t M, int64
   return 0;
 }
 
+/* One LSTM step whose gate weights are balanced-sparse: the recurrent layers of the paper's PTB model
+ * ("2-layer LSTM ... 1500 hidden units"; the rows of [W_ih | W_hh] are BJ.configs[1]'s 6000 x 3000)
+ * and TIMIT Bi-LSTM (hidden 1024). The gate pre-activations are Eq. 1 with its +B:
+ *   z = W_bs·x + pre + bias,    x = [x_t ; h_{t-1}] (or h_{t-1} alone when pre holds W_ih·x_t),
+ * with the gate rows interleaved: row 4j + g is gate g of hidden unit j, g = 0 input, 1 forget,
+ * 2 cell candidate, 3 output. The cell is the standard LSTM:
+ *   i = sigmoid(z_i), f = sigmoid(z_f), g = tanh(z_g), o = sigmoid(z_o),
+ *   c_j = f·c_prev_j + i·g,   h_j = o·tanh(c_j),
+ * all in fp64 (orc_act's sigmoid and tanh). pre, bias: M elements of dt or NULL. c_prev, h, c: M/4
+ * doubles. zbound (M doubles, may be NULL): per gate row sum|w||x| + |pre| + |bias| (O-7's scale). */
+int orc_lstm_cell(const void* vals, const uint16_t* idx, int dt, int64_t M, int64_t K, int B, int k, const void* x,
+                  const void* pre, const void* bias, const double* c_prev, double* h, double* c, double* zbound) {
+  if (M < 4 || M % 4 != 0) return -1;
+  double* z = (double*)malloc(sizeof(double) * (size_t)M);
+  double* zb = (double*)malloc(sizeof(double) * (size_t)M);
+  if (orc_spmv_rows(vals, idx, dt, M, K, B, k, x, NULL, M, z, zb)) {
+    free(z);
+    free(zb);
+    return -1;
+  }
+  for (int64_t r = 0; r < M; ++r) {
+    double p = pre ? orc_elem(pre, dt, r) : 0.0, b = bias ? orc_elem(bias, dt, r) : 0.0;
+    z[r] += p + b;
+    zb[r] += fabs(p) + fabs(b);
+    if (zbound) zbound[r] = zb[r];
+  }
+  for (int64_t j = 0; j < M / 4; ++j) {
+    double ig = orc_act(z[4 * j + 0], 2), fg = orc_act(z[4 * j + 1], 2);
+    double gg = orc_act(z[4 * j + 2], 3), og = orc_act(z[4 * j + 3], 2);
+    c[j] = fg * c_prev[j] + ig * gg;
+    h[j] = og * orc_act(c[j], 3);
+  }
+  free(z);
+  free(zb);
+  return 0;
+}
+
 /* ------------------------------------------------------------------ reporting */
 
 /* The paper's ideal inference time: i_time = (d_time - o_time) * (1 - sparsity) + o_time. */

@@ -747,3 +747,50 @@ def test_pattern_masks_reject_bad_shapes():
     with pytest.raises(ValueError):
         oracle.random_mask(W, oracle.F32, 1.0)
     assert oracle.keep_count(10, 0.9) == 1 and oracle.keep_count(100, 0.9) == 10 and oracle.keep_count(7, 0.5) == 4
+
+
+# ------------------------------------------------------------------ LSTM step with balanced-sparse gates (NEXT-2)
+
+def test_lstm_cell_matches_torch_lstmcell():
+    """The LSTM step equals torch's LSTMCell (the library routine, in fp64) on the dense W_bs, after
+    undoing the gate-row interleave (row 4j+g <-> PyTorch's block row g·H + j)."""
+    In, H, B, k = 64, 48, 16, 5
+    K = In + H
+    W = synth.to_numpy(synth.matrix(4 * H, K, "f32", seed=101))
+    vals, idx = oracle.prune(W, oracle.F32, B, k)
+    Wd = oracle.decode(vals, idx, oracle.F32, 4 * H, K, B, k)
+    x = synth.to_numpy(synth.vector(K, "f32", seed=102))
+    bias = synth.to_numpy(synth.vector(4 * H, "f32", seed=103)) * np.float32(0.5)
+    c_prev = synth.to_numpy(synth.vector(H, "f32", seed=104)).astype(np.float64)
+    h, c, zb = oracle.lstm_cell(vals, idx, oracle.F32, 4 * H, K, B, k, x, None, bias, c_prev)
+    perm = np.array([4 * j + g for g in range(4) for j in range(H)])  # PyTorch row g·H + j = our row 4j + g
+    cell = torch.nn.LSTMCell(In, H).double()
+    with torch.no_grad():
+        cell.weight_ih.copy_(torch.from_numpy(Wd[perm, :In]))
+        cell.weight_hh.copy_(torch.from_numpy(Wd[perm, In:]))
+        cell.bias_ih.copy_(torch.from_numpy(bias.astype(np.float64)[perm]))
+        cell.bias_hh.zero_()
+        ht, ct = cell(torch.from_numpy(x[:In].astype(np.float64))[None], (torch.from_numpy(x[In:].astype(np.float64))[None],
+                                                                        torch.from_numpy(c_prev)[None]))
+    np.testing.assert_allclose(h, ht[0].numpy(), rtol=0, atol=1e-13)
+    np.testing.assert_allclose(c, ct[0].numpy(), rtol=0, atol=1e-13)
+    # pre (W_ih·x_t precomputed) + bias is the same as bias alone with pre folded in
+    h2, c2, _ = oracle.lstm_cell(vals, idx, oracle.F32, 4 * H, K, B, k, x, bias, None, c_prev)
+    np.testing.assert_array_equal(h2, h)
+    assert np.all(zb >= 0)
+
+
+def test_lstm_cell_closed_form():
+    """k = 0: z = bias. z_i = 0, z_f = ln 3, z_g = ln 2, z_o = 0, c_prev = 1:
+    c = 3/4 + 1/2·3/5 = 1.05 and h = tanh(1.05)/2."""
+    H, K, B = 3, 32, 16
+    vals = np.zeros((4 * H, K // B, 0), dtype=np.float32)
+    idx = np.zeros((4 * H, K // B, 0), dtype=np.uint16)
+    bias = np.tile(np.array([0.0, math.log(3.0), math.log(2.0), 0.0], dtype=np.float32), H)
+    x = np.zeros(K, dtype=np.float32)
+    h, c, _ = oracle.lstm_cell(vals, idx, oracle.F32, 4 * H, K, B, 0, x, None, bias, np.ones(H))
+    f = 1.0 / (1.0 + math.exp(-float(np.float32(math.log(3.0)))))
+    g = math.tanh(float(np.float32(math.log(2.0))))
+    np.testing.assert_allclose(c, f + 0.5 * g, rtol=0, atol=1e-15)
+    assert abs(c[0] - 1.05) < 1e-7 and abs(h[0] - math.tanh(1.05) / 2) < 1e-7
+    np.testing.assert_allclose(h, 0.5 * np.tanh(c), rtol=0, atol=1e-15)
