@@ -89,6 +89,12 @@ def lib() -> ctypes.CDLL:
         L.orc_lstm_cell.argtypes = [_vp, _vp, ctypes.c_int, _c_i64, _c_i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp,
                                     _vp, _vp, _vp, _vp]
         L.orc_lstm_cell.restype = ctypes.c_int
+        L.orc_im2col.argtypes = [_vp, ctypes.c_int, _c_i64, _c_i64, _c_i64, _c_i64, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_int, ctypes.c_int, _vp]
+        L.orc_im2col.restype = ctypes.c_int
+        L.orc_conv2d.argtypes = [_vp, _vp, ctypes.c_int, _c_i64, ctypes.c_int, ctypes.c_int, _vp, _c_i64, _c_i64,
+                                 _c_i64, _c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
+        L.orc_conv2d.restype = ctypes.c_int
         L.orc_elem.argtypes = [_vp, ctypes.c_int, _c_i64]
         L.orc_elem.restype = ctypes.c_double
         _lib = L
@@ -283,6 +289,37 @@ def lstm_cell(vals, idx, dt, M, K, block, k, x, pre, bias, c_prev):
                            _ptr(zb)) != 0:
         raise ValueError("orc_lstm_cell rejected the arguments")
     return h, c, zb
+
+
+def conv_out_hw(H: int, W: int, kh: int, kw: int, pad: int, stride: int):
+    return (H + 2 * pad - kh) // stride + 1, (W + 2 * pad - kw) // stride + 1
+
+
+def im2col(inp: np.ndarray, dt: int, kh: int, kw: int, pad: int, stride: int) -> np.ndarray:
+    """NHWC input [Nimg][H][W][C] -> X [Nimg·OH·OW][kh·kw·C] with columns (dy, dx, c) (reading A23)."""
+    inp = _check(np.ascontiguousarray(inp), dt)
+    Nimg, H, W, C = inp.shape
+    OH, OW = conv_out_hw(H, W, kh, kw, pad, stride)
+    X = np.zeros((Nimg * OH * OW, kh * kw * C), dtype=_vdtype(dt))
+    if lib().orc_im2col(_ptr(inp), dt, Nimg, H, W, C, kh, kw, pad, stride, _ptr(X)) != 0:
+        raise ValueError("orc_im2col rejected the arguments")
+    return X
+
+
+def conv2d(vals, idx, dt, Cout, block, k, inp, kh, kw, pad, stride):
+    """Direct fp64 convolution with the balanced-sparse Cout × (kh·kw·C) weight matrix; NHWC in, Y
+    [Nimg·OH·OW][Cout] and the tolerance scale out (orc_conv2d)."""
+    vals = _check(vals, dt)
+    idx = np.ascontiguousarray(idx, dtype=np.uint16)
+    inp = _check(np.ascontiguousarray(inp), dt)
+    Nimg, H, W, C = inp.shape
+    OH, OW = conv_out_hw(H, W, kh, kw, pad, stride)
+    Y = np.zeros((Nimg * OH * OW, Cout), dtype=np.float64)
+    bound = np.zeros_like(Y)
+    if lib().orc_conv2d(_ptr(vals), _ptr(idx), dt, Cout, block, k, _ptr(inp), Nimg, H, W, C, kh, kw, pad, stride,
+                        _ptr(Y), _ptr(bound)) != 0:
+        raise ValueError("orc_conv2d rejected the arguments")
+    return Y, bound
 
 
 def schedule(target: float, n: int, i: int) -> float:

@@ -628,6 +628,76 @@ int orc_lstm_cell(const void* vals, const uint16_t* idx, int dt, int64_t M, int6
   return 0;
 }
 
+/* Convolution as the paper runs it: "One popular implementation of convolution operation is using
+ * im2col that converts convolution operation to matrix-matrix multiplication", and "the weights
+ * of all kernels in one convolution layer are considered as one weight matrix". Reading A23: the
+ * activations are NHWC (channels last) and the weight matrix is Cout x (kh·kw·C) with its columns in
+ * (dy, dx, c) order, so that column (dy·kw + dx)·C + c multiplies input channel c at tap (dy, dx).
+ *
+ * orc_im2col: X[(n·OH + oy)·OW + ox][(dy·kw + dx)·C + c] = in[n][oy·stride + dy - pad][ox·stride + dx - pad][c],
+ * +0 where the tap falls outside the image; OH = (H + 2·pad - kh)/stride + 1 (same for OW). A pure copy
+ * of element bits. X has leading dimension kh·kw·C. */
+int orc_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw, int pad,
+               int stride, void* X) {
+  if (Nimg < 1 || H < 1 || W < 1 || C < 1 || kh < 1 || kw < 1 || pad < 0 || stride < 1) return -1;
+  int64_t OH = (H + 2 * pad - kh) / stride + 1, OW = (W + 2 * pad - kw) / stride + 1;
+  if (OH < 1 || OW < 1) return -1;
+  int es = dtype_size(dt);
+  int64_t Kc = (int64_t)kh * kw * C;
+  for (int64_t n = 0; n < Nimg; ++n)
+    for (int64_t oy = 0; oy < OH; ++oy)
+      for (int64_t ox = 0; ox < OW; ++ox)
+        for (int dy = 0; dy < kh; ++dy)
+          for (int dx = 0; dx < kw; ++dx)
+            for (int64_t c = 0; c < C; ++c) {
+              int64_t iy = oy * stride + dy - pad, ix = ox * stride + dx - pad;
+              unsigned char* dst = (unsigned char*)X + (((n * OH + oy) * OW + ox) * Kc + (dy * kw + dx) * C + c) * es;
+              if (iy < 0 || iy >= H || ix < 0 || ix >= W)
+                memset(dst, 0, (size_t)es);
+              else
+                memcpy(dst, (const unsigned char*)in + (((n * H + iy) * W + ix) * C + c) * es, (size_t)es);
+            }
+  return 0;
+}
+
+/* The convolution itself, written as its definition (no im2col): for output pixel (n, oy, ox) and
+ * output channel co,  y = sum_{dy,dx,c} W_bs[co][(dy·kw + dx)·C + c] · in[n][oy·s + dy - pad][ox·s + dx - pad][c]
+ * in fp64 over the canonical (vals, idx) of the Cout x (kh·kw·C) weight matrix. Output Y[pixel][co]
+ * (NHWC), and bound[pixel][co] = the same sum of |w|·|in| (O-7's tolerance scale). */
+int orc_conv2d(const void* vals, const uint16_t* idx, int dt, int64_t Cout, int B, int k, const void* in,
+               int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw, int pad, int stride, double* Y,
+               double* bound) {
+  int64_t Kc = (int64_t)kh * kw * C;
+  if (Kc % B != 0 || Cout < 1) return -1;
+  int64_t OH = (H + 2 * pad - kh) / stride + 1, OW = (W + 2 * pad - kw) / stride + 1;
+  if (OH < 1 || OW < 1) return -1;
+  int64_t NB = Kc / B;
+  for (int64_t n = 0; n < Nimg; ++n)
+    for (int64_t oy = 0; oy < OH; ++oy)
+      for (int64_t ox = 0; ox < OW; ++ox) {
+        int64_t p = (n * OH + oy) * OW + ox;
+        for (int64_t co = 0; co < Cout; ++co) {
+          double acc = 0.0, bnd = 0.0;
+          for (int64_t b = 0; b < NB; ++b)
+            for (int t = 0; t < k; ++t) {
+              int64_t pos = (co * NB + b) * k + t;
+              int64_t col = b * B + idx[pos];
+              int64_t tap = col / C, c = col % C;
+              int64_t dy = tap / kw, dx = tap % kw;
+              int64_t iy = oy * stride + dy - pad, ix = ox * stride + dx - pad;
+              if (iy < 0 || iy >= H || ix < 0 || ix >= W) continue;
+              double w = orc_elem(vals, dt, pos);
+              double v = orc_elem(in, dt, ((n * H + iy) * W + ix) * C + c);
+              acc += w * v;
+              bnd += fabs(w) * fabs(v);
+            }
+          Y[p * Cout + co] = acc;
+          if (bound) bound[p * Cout + co] = bnd;
+        }
+      }
+  return 0;
+}
+
 /* ------------------------------------------------------------------ reporting */
 
 /* The paper's ideal inference time: i_time = (d_time - o_time) * (1 - sparsity) + o_time. */

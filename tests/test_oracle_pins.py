@@ -794,3 +794,62 @@ def test_lstm_cell_closed_form():
     np.testing.assert_allclose(c, f + 0.5 * g, rtol=0, atol=1e-15)
     assert abs(c[0] - 1.05) < 1e-7 and abs(h[0] - math.tanh(1.05) / 2) < 1e-7
     np.testing.assert_allclose(h, 0.5 * np.tanh(c), rtol=0, atol=1e-15)
+
+
+# ------------------------------------------------------------------ convolution via im2col (NEXT-3)
+
+def _nhwc_weight_to_torch(Wd, Cout, C, kh, kw):
+    """Our Cout × (kh·kw·C) matrix with (dy, dx, c) columns -> torch's [Cout][C][kh][kw]."""
+    return Wd.reshape(Cout, kh, kw, C).transpose(0, 3, 1, 2)
+
+
+@pytest.mark.parametrize("kh,kw,pad,stride", [(3, 3, 1, 1), (3, 3, 1, 2), (1, 1, 0, 1), (3, 3, 0, 1), (5, 3, 2, 2)])
+def test_conv2d_matches_torch_conv2d(kh, kw, pad, stride):
+    """orc_conv2d equals torch.nn.functional.conv2d (the library routine, fp64) on the dense W_bs, and
+    the im2col route (orc_im2col, then the oracle's own SpMM) gives the same numbers."""
+    Nimg, H, W, C, Cout, B, k = 2, 7, 6, 16, 12, 16, 5
+    Kc = kh * kw * C
+    Wm = synth.to_numpy(synth.matrix(Cout, Kc, "f32", seed=111))
+    vals, idx = oracle.prune(Wm, oracle.F32, B, k)
+    Wd = oracle.decode(vals, idx, oracle.F32, Cout, Kc, B, k)
+    inp = synth.to_numpy(synth.vector(Nimg * H * W * C, "f32", seed=112)).reshape(Nimg, H, W, C)
+    Y, bound = oracle.conv2d(vals, idx, oracle.F32, Cout, B, k, inp, kh, kw, pad, stride)
+    ref = torch.nn.functional.conv2d(torch.from_numpy(inp.astype(np.float64)).permute(0, 3, 1, 2),
+                                     torch.from_numpy(np.ascontiguousarray(_nhwc_weight_to_torch(Wd, Cout, C, kh, kw))),
+                                     stride=stride, padding=pad)
+    np.testing.assert_allclose(Y, ref.permute(0, 2, 3, 1).reshape(-1, Cout).numpy(), rtol=0, atol=1e-12)
+    X = oracle.im2col(inp, oracle.F32, kh, kw, pad, stride)
+    Y2, _ = oracle.spmm(vals, idx, oracle.F32, Cout, Kc, B, k, X)
+    np.testing.assert_allclose(Y2, Y, rtol=0, atol=1e-12)
+    assert np.all(bound >= np.abs(Y) - 1e-12)
+
+
+def test_im2col_closed_forms():
+    """1×1 / stride 1 / pad 0 im2col is the NHWC tensor itself (rows = pixels); a 3×3 pad-1 patch of an
+    image holding its own coordinates reads the neighbours, and zeros past the border."""
+    inp = np.arange(2 * 4 * 5 * 3, dtype=np.float32).reshape(2, 4, 5, 3)
+    np.testing.assert_array_equal(oracle.im2col(inp, oracle.F32, 1, 1, 0, 1), inp.reshape(-1, 3))
+    img = np.zeros((1, 3, 3, 2), dtype=np.float32)
+    for y in range(3):
+        for x in range(3):
+            img[0, y, x] = [10 * y + x + 1, -(10 * y + x + 1)]
+    X = oracle.im2col(img, oracle.F32, 3, 3, 1, 1)
+    centre = X[4].reshape(3, 3, 2)  # output pixel (1, 1): the whole image
+    np.testing.assert_array_equal(centre, img[0])
+    corner = X[0].reshape(3, 3, 2)  # output pixel (0, 0): taps (dy, dx) read (dy - 1, dx - 1)
+    assert np.all(corner[0] == 0) and np.all(corner[:, 0] == 0)
+    np.testing.assert_array_equal(corner[1:, 1:], img[0, :2, :2])
+
+
+def test_conv2d_identity_kernel():
+    """A kernel with one 1 at the centre tap for co = c (B = kh·kw·C, k = 1 per row) reproduces the input
+    (stride 1, pad 1)."""
+    C, kh, kw = 4, 3, 3
+    Kc = kh * kw * C
+    Wm = np.zeros((C, Kc), dtype=np.float32)
+    for c in range(C):
+        Wm[c, (1 * kw + 1) * C + c] = 1.0
+    vals, idx = oracle.prune(Wm, oracle.F32, Kc, 1)
+    inp = synth.to_numpy(synth.vector(1 * 5 * 6 * C, "f32", seed=113)).reshape(1, 5, 6, C)
+    Y, _ = oracle.conv2d(vals, idx, oracle.F32, C, Kc, 1, inp, kh, kw, 1, 1)
+    np.testing.assert_array_equal(Y, inp.reshape(-1, C).astype(np.float64))
