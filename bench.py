@@ -246,12 +246,35 @@ def main():
     mats = [A] + [bs.BSMatrix(A.M, A.K, A.block, A.k, A.dtype, A.layout, A.packed.clone()) for _ in range(C - 1)]
     y_loc = torch.zeros(-(-M // world), dtype=tdt, device=dev)
     y_full = torch.empty(y_loc.numel() * world, dtype=tdt, device=dev)
+    exchange = {}
+    fused = None
     if world > 1:
+        from paper_1811_00206_b200.dist import FusedRowShardedBS, measure_allgather_us, should_shard
         layer = RowShardedBS(A, M)
+        y_ref = layer.forward(x, y_local_buf=y_loc, y_full_buf=y_full).clone()
+        try:  # NEXT-1: the all-gather fused into the SpMV over peer-mapped NVLink buffers
+            fused = FusedRowShardedBS(A, M, tdt, dev)
+            ok = torch.equal(fused(x), y_ref)
+            okt = torch.tensor([1 if ok else 0], device=dev)
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+            if int(okt.item()) != 1:
+                exchange["fused_note"] = "fused y differs from the NCCL y on some rank: not used"
+                fused = None
+        except Exception as e:  # no P2P mapping: the NCCL path is the step
+            exchange["fused_note"] = f"unavailable: {type(e).__name__}: {str(e)[:120]}"
+            fused = None
+        exchange["fused_bit_identical_to_nccl"] = fused is not None
+        t_ag = measure_allgather_us(y_loc.numel() * es, device=dev)
+        exchange["allgather_us"] = round(t_ag, 2)
 
-        def step(i):
-            layer.local = mats[i % C]
-            layer.forward(x, y_local_buf=y_loc, y_full_buf=y_full)
+        if fused is not None:
+            def step(i):
+                fused.local = mats[i % C]
+                fused.forward(x)
+        else:
+            def step(i):
+                layer.local = mats[i % C]
+                layer.forward(x, y_local_buf=y_loc, y_full_buf=y_full)
     else:
         def step(i):
             bs.spmv(mats[i % C], x, out=y_loc[:Ml])
@@ -271,7 +294,13 @@ def main():
     with ClockSampler(local) as clk:
         t0.record(stream)
         for i in range(a.steps):
-            if world > 1:
+            if world > 1 and fused is not None:
+                kstart[i].record(stream)
+                fused.local = mats[i % C]
+                fused.launch(x)
+                kend[i].record(stream)
+                fused.wait()
+            elif world > 1:
                 kstart[i].record(stream)
                 bs.spmv(mats[i % C], x, out=y_loc[:Ml])
                 kend[i].record(stream)
@@ -292,6 +321,21 @@ def main():
     else:
         kern_ms_max = kern_ms
 
+    if world > 1:  # the other exchange variant, for comparison (device-timed, max over ranks)
+        def nccl_step(i):
+            bs.spmv(mats[i % C], x, out=y_loc[:Ml])
+            dist.all_gather_into_tensor(y_full, y_loc)
+        n_cmp = max(20, a.steps // 4)
+        for i in range(3):
+            nccl_step(i)
+        dist.barrier()
+        t_n = time_loop(nccl_step, n_cmp, stream)
+        tt = torch.tensor([t_n], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        exchange["nccl_step_ms"] = round(float(tt[0]), 5)
+        exchange["step_path"] = "fused (bs_spmv_allgather + bs_allgather_wait)" if fused is not None else "NCCL"
+        exchange["spmv_ms"] = round(kern_ms_max, 5)
+        exchange["should_shard"] = should_shard(kern_ms_max * 1e3 * world, world, exchange["allgather_us"])
     full_packed = bs.packed_bytes(M, K, B, k, tdt, "spmv")
     bytes_job = full_packed + world * K * es + M * es          # every rank reads x; y written once in total
     value = bytes_job / (ms * 1e-3) / 1e9
@@ -353,7 +397,9 @@ def main():
         "warmup": a.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
         "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
         "config": {"workload": f"configs[4] {M}x{K} balanced-sparse layer, B={B}, s={a.sparsity} (k={k}, achieved "
-                               f"{1 - k / B:.5f}), batch 1 SpMV, row-sharded x{world}" + (" + NCCL all_gather(y)" if world > 1 else ""),
+                               f"{1 - k / B:.5f}), batch 1 SpMV, row-sharded x{world}"
+                               + ((" + all-gather of y fused into the SpMV (NVLink P2P)" if fused is not None
+                                   else " + NCCL all_gather(y)") if world > 1 else ""),
                    "M": M, "K": K, "block": B, "k": k, "batch": 1, "index_bits": 5 if (B == 32 and es == 2 and K // B >= 256) else (8 if B <= 256 else 16),
                    "packed_bytes_total": full_packed, "packed_bytes_per_rank": A.nbytes,
                    "l2": f"inputs larger than L2: {C} rotating cop{'y' if C == 1 else 'ies'} of a {A.nbytes / 1e6:.0f} MB "
@@ -369,11 +415,15 @@ def main():
         "legs": legs if world == 1 else dict(legs, spmv_ms=round(kern_ms_max, 5),
                                                  allgather_ms=round(max(0.0, ms - kern_ms_max), 5)),
     }
+    if world > 1:
+        out["exchange"] = exchange
     # clocks
     out["clocks"] = clk.summary()
 
     if world == 1 and not a.no_extras:
         out.update(extras(a, bs, W, A, vals, idx, x, k, es, hbm_peak, stream))
+        # the north-star quantity over the sparsity range, inside the key the driver keeps
+        out["roofline"]["sweep_packed_frac"] = {str(r["sparsity"]): r["packed_frac"] for r in out.get("sweep", [])}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -548,7 +598,8 @@ def spmm_rows(a, bs, hbm_peak, l2):
     rows = []
     dev = torch.device("cuda")
     tc_peak = tensor_peak()
-    shapes = [("configs[2] VGG fc6 4096x25088", 4096, 25088, [0.9], [32]),
+    shapes = [("cfgX paper benchmark 16384x8192 (P:240, 8196 read as 8192)", 16384, 8192, [0.9], [1, 8]),
+              ("configs[2] VGG fc6 4096x25088", 4096, 25088, [0.9], [32]),
               ("configs[2] VGG fc7 4096x4096", 4096, 4096, [0.5, 0.9], [32]),
               ("configs[3] CTC W_ih 4096x2048", 4096, 2048, [0.875], [1, 2, 4, 8, 16, 32, 64, 128, 256]),
               ("configs[3] CTC W_hh 4096x1024", 4096, 1024, [0.875], [8, 64, 256])]
@@ -593,6 +644,16 @@ def spmm_rows(a, bs, hbm_peak, l2):
                         row[f"{kn}_tensor_frac"] = round(mma / (tc_peak * (2.0 if kn == "K5" else 1.0)), 4)
                     if best is None or t < best[1]:
                         best = (kn, t)
+                if B != 4 and N <= 32:  # cuSPARSE SpMM (torch.sparse.mm on int32 CSR) on the same W_bs
+                    try:
+                        csr = csr_from_canonical(v, i, M, K, B)
+                        Xt = X.t().contiguous()
+                        row["cusparse_us"] = round(graph_time_us(lambda j: torch.sparse.mm(csr, Xt), 3, reps=3), 2)
+                        del csr
+                    except Exception as e:
+                        row["cusparse_note"] = str(e)[:100]
+                if B == 4 and N >= 16:  # cuSPARSELt 2:4 (torch semi-structured sparsity) on the same W_bs
+                    row.update(cusparselt_time(Wbs, X))
                 row["best"] = best[0]
                 row["speedup_vs_cublas"] = round(td / best[1], 2)
                 row["TFLOPs_nnz"] = round(2.0 * M * (K // B) * ks * N / best[1] / 1e6, 2)
@@ -604,6 +665,165 @@ def spmm_rows(a, bs, hbm_peak, l2):
                                        "against MEASURED_PEAKS hbm_gbs; tensor_frac = issued MMA flops (K6: dense "
                                        f"2MKN on decompressed tiles; K5: 2:4, against 2x) / the measured bf16 peak "
                                        f"{tc_peak} TFLOP/s (sustained; f16 runs at the bf16 rate)"}
+
+
+def cusparselt_time(Wbs, X) -> dict:
+    """cuSPARSELt 2:4 GEMM (torch.sparse.to_sparse_semi_structured, cuSPARSELt backend) on the same W_bs."""
+    try:
+        from torch.sparse import SparseSemiStructuredTensor, to_sparse_semi_structured
+        SparseSemiStructuredTensor._FORCE_CUTLASS = False
+        Ws = to_sparse_semi_structured(Wbs)
+        Xt = X.t().contiguous()
+        t = graph_time_us(lambda j: torch.mm(Ws, Xt), 10, reps=3)
+        return {"cusparselt_us": round(t, 2)}
+    except Exception as e:  # reported, not hidden
+        return {"cusparselt_note": f"{type(e).__name__}: {str(e)[:100]}"}
+
+
+def conv_rows(a, bs, l2):
+    """NEXT-3: VGG-16 conv layers of Table cnn-perf at batch 1, 224x224 input geometry, with
+    the paper's balanced sparsity for each layer, run as im2col + bs_spmm (layout by bs_choose_layout)
+    against cuDNN (torch conv2d, channels_last, f16) on the dense W_bs. CUDA-graph timed."""
+    rows = []
+    dev = torch.device("cuda")
+    for name, C, Cout, HW, s in (("conv3_3", 256, 256, 56, 0.88), ("conv4_2", 512, 512, 28, 0.91),
+                                 ("conv5_2", 512, 512, 14, 0.90), ("conv5_3", 512, 512, 14, 0.95)):
+        Kc = 9 * C
+        Wm = synth.matrix(Cout, Kc, a.dtype, seed=synth.seed_for(6, C + HW), device=dev)
+        ks = bs.k_from_sparsity(a.block, s)
+        v, i, _ = bs.prune(Wm, a.block, k=ks)
+        N = HW * HW
+        lay = bs.choose_layout(Cout, Kc, a.block, ks, Wm.dtype, N)
+        A = bs.pack(v, i, Kc, a.block, layout=lay)
+        inp = synth.vector(HW * HW * C, a.dtype, seed=synth.seed_for(6, 1), device=dev).view(1, HW, HW, C)
+        X = torch.empty((N, Kc), dtype=Wm.dtype, device=dev)
+        Y = torch.empty((N, Cout), dtype=Wm.dtype, device=dev)
+        t_ours = graph_time_us(lambda j: bs.spmm(A, bs.im2col(inp, 3, 3, 1, 1, out=X), out=Y), 20)
+        t_im2col = graph_time_us(lambda j: bs.im2col(inp, 3, 3, 1, 1, out=X), 20)
+        Wd = dense_from_canonical(v, i, Cout, Kc, a.block).view(Cout, 3, 3, C).permute(0, 3, 1, 2)
+        Wd = Wd.contiguous(memory_format=torch.channels_last)
+        xin = inp.permute(0, 3, 1, 2)  # NHWC storage = channels_last NCHW view
+        t_cudnn = graph_time_us(lambda j: torch.nn.functional.conv2d(xin, Wd, padding=1), 20)
+        rows.append({"layer": name, "C": C, "Cout": Cout, "HW": HW, "sparsity": s, "k": ks, "N": N, "layout": lay,
+                     "ours_us": round(t_ours, 2), "im2col_us": round(t_im2col, 2), "cudnn_dense_us": round(t_cudnn, 2),
+                     "speedup_vs_cudnn": round(t_cudnn / t_ours, 2),
+                     "TFLOPs_nnz": round(2.0 * Cout * (Kc // a.block) * ks * N / t_ours / 1e6, 2)})
+        del A, v, i, Wm, Wd, X, Y
+    return {"conv": rows, "conv_note": "ours = bs_im2col + bs_spmm (NHWC, one weight matrix per layer, P:107/P:286); "
+                                       "cudnn = torch conv2d channels_last on the dense W_bs; batch 1"}
+
+
+def lstm_rows(a, bs, l2):
+    """NEXT-2: one LSTM step with balanced-sparse gates (bs_lstm_step: gate SpMV + cell in one kernel) on the
+    PTB layer ([W_ih | W_hh] 6000 x 3000 -> 3008) and a TIMIT direction (hidden 1024, W_hh with
+    W_ih·x_t precomputed), against cuBLAS (addmv on the dense W_bs) + torch's fused LSTM cell kernel."""
+    rows = []
+    dev = torch.device("cuda")
+    for name, H, K, pre in (("PTB [W_ih|W_hh] 6000x3008, 90%", 1500, 3008, False),
+                            ("TIMIT W_hh 4096x1024 + pre, 87.5%", 1024, 1024, True)):
+        s = 0.9 if H == 1500 else 0.875
+        ks = bs.k_from_sparsity(a.block, s)
+        W = synth.matrix(4 * H, K, a.dtype, seed=synth.seed_for(7, H), device=dev)
+        v, i, _ = bs.prune(W, a.block, k=ks)
+        mats = rotating(bs, bs.pack(v, i, K, a.block), l2)
+        C = len(mats)
+        x = synth.vector(K, a.dtype, seed=synth.seed_for(7, 1), device=dev)
+        b = synth.vector(4 * H, a.dtype, seed=synth.seed_for(7, 2), device=dev)
+        u = synth.vector(4 * H, a.dtype, seed=synth.seed_for(7, 3), device=dev) if pre else None
+        c0 = torch.zeros(H, dtype=torch.float32, device=dev)
+        h1, c1 = torch.empty(H, dtype=W.dtype, device=dev), torch.empty(H, dtype=torch.float32, device=dev)
+        n_in = 20 * C if C < 10 else 2 * C
+        t_ours = graph_time_us(lambda j: bs.lstm_step(mats[j % C], x, c0, pre=u, bias=b, h_out=h1, c_out=c1), n_in)
+        Wd = dense_from_canonical(v, i, 4 * H, K, a.block)
+        dens = [Wd] + [Wd.clone() for _ in range(max(1, -(-3 * l2 // (Wd.numel() * 2))) - 1)]
+        Cd = len(dens)
+        cx = torch.zeros(1, H, dtype=W.dtype, device=dev)
+        zero = torch.zeros(1, 4 * H, dtype=W.dtype, device=dev)
+
+        def ref(j):
+            g = torch.addmv(b if u is None else b + u, dens[j % Cd], x).view(1, -1)
+            return torch._thnn_fused_lstm_cell(g, zero, cx)
+        try:
+            t_ref = graph_time_us(ref, 4 * Cd)
+            ref_name = "torch.addmv (cuBLAS) + torch._thnn_fused_lstm_cell"
+        except Exception:
+            def ref2(j):
+                g = torch.addmv(b if u is None else b + u, dens[j % Cd], x).view(4, H)
+                c = torch.sigmoid(g[1]) * cx[0] + torch.sigmoid(g[0]) * torch.tanh(g[2])
+                return torch.sigmoid(g[3]) * torch.tanh(c)
+            t_ref = graph_time_us(ref2, 4 * Cd)
+            ref_name = "torch.addmv (cuBLAS) + torch elementwise cell"
+        rows.append({"layer": name, "sparsity": s, "k": ks, "ours_us": round(t_ours, 2), "cublas_cell_us": round(t_ref, 2),
+                     "speedup": round(t_ref / t_ours, 2), "reference_path": ref_name})
+        del dens, Wd, mats, v, i, W
+    return {"lstm": rows}
+
+
+def f32_rows(a, bs, hbm_peak, l2):
+    """The f32 path (the paper never states its precision; fp32 was the 2018 norm): SpMV GB/s on a 32768^2 f32
+    layer at 90% (5 B per nonzero) and the VGG fc6/fc7 layers at 90% against cuBLAS f32 GEMV on the same W_bs."""
+    rows = []
+    dev = torch.device("cuda")
+    for name, M, K in (("32768x32768 f32", 32768, 32768), ("configs[2] VGG fc6 4096x25088 f32", 4096, 25088),
+                       ("configs[2] VGG fc7 4096x4096 f32", 4096, 4096)):
+        W = synth.matrix(M, K, "f32", seed=synth.seed_for(8, M + K), device=dev)
+        x = synth.vector(K, "f32", seed=synth.seed_for(8, 1), device=dev)
+        y = torch.empty(M, dtype=torch.float32, device=dev)
+        ks = bs.k_from_sparsity(32, 0.9)
+        v, i, _ = bs.prune(W, 32, k=ks)
+        mats = rotating(bs, bs.pack(v, i, K, 32), l2)
+        C = len(mats)
+        t = graph_time_us(lambda j: bs.spmv(mats[j % C], x, out=y), 20 * C if C < 10 else 2 * C)
+        pk = mats[0].nbytes + (K + M) * 4
+        row = {"layer": name, "sparsity": 0.9, "k": ks, "us": round(t, 2), "packed_GBps": round(pk / t / 1e3, 1),
+               "packed_frac": round(pk / t / 1e3 / hbm_peak, 4)}
+        if M * K <= 4096 * 25088:
+            Wd = dense_from_canonical(v, i, M, K, 32)
+            dens = [Wd] + [Wd.clone() for _ in range(max(1, -(-3 * l2 // (Wd.numel() * 4))) - 1)]
+            Cd = len(dens)
+            td = graph_time_us(lambda j: torch.mv(dens[j % Cd], x), 4 * Cd)
+            row["cublas_f32_us"] = round(td, 2)
+            row["speedup_vs_cublas"] = round(td / t, 2)
+            del dens, Wd
+        rows.append(row)
+        del mats, v, i, W
+    return {"f32": rows}
+
+
+def producer_rows(a, bs, W):
+    """The offline producers on the bench layer (65536^2 f16 by default): bs_prune_k (K1) at k = 3 and 16, bs_pack (K2),
+    bs_block_rank, bs_prune_dense (Alg. 1 iteration, prune + decode) and the comparison masks (random,
+    8x8 block) of NEXT-4, as dense-read bandwidth against the HBM peak."""
+    M, K = W.shape
+    dense = M * K * W.element_size()
+    out = {}
+
+    def t_ms(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    for kk in (3, 16):
+        t = t_ms(lambda: bs.prune(W, 32, k=kk))
+        out[f"prune_k{kk}_ms"] = round(t, 3)
+        out[f"prune_k{kk}_TBps_dense_read"] = round(dense / t / 1e9, 2)
+    v, i, _ = bs.prune(W, 32, k=3)
+    out["pack_ms"] = round(t_ms(lambda: bs.pack(v, i, K, 32)), 3)
+    t = t_ms(lambda: bs.block_rank(W, 32))
+    out["block_rank_ms"] = round(t, 3)
+    out["block_rank_TBps"] = round((dense + M * K) / t / 1e9, 2)
+    del v, i
+    Ws = W[:16384].clone()
+    out["random_mask_16384x65536_ms"] = round(t_ms(lambda: bs.random_mask(Ws, 0.9), reps=1), 3)
+    out["block8x8_mask_16384x65536_ms"] = round(t_ms(lambda: bs.block_mask(Ws, 8, 8, 0.9), reps=1), 3)
+    out["prune_dense_16384x65536_ms"] = round(t_ms(lambda: bs.prune_dense(Ws, 32, k=3, out=Ws), reps=1), 3)
+    del Ws
+    return {"producers": out}
 
 
 def tensor_peak() -> float:
@@ -655,6 +875,19 @@ def extras(a, bs, W, A, vals, idx, x, k, es, hbm_peak, stream):
     res.update(layer_rows(a, bs, hbm_peak, l2))
     res.update(epilogue_rows(a, bs, l2))
     res.update(spmm_rows(a, bs, hbm_peak, l2))
+    try:
+        res.update(f32_rows(a, bs, hbm_peak, l2))
+    except Exception as e:
+        res["f32_rows_error"] = f"{type(e).__name__}: {str(e)[:200]}"
+    for fn in (conv_rows, lstm_rows):
+        try:
+            res.update(fn(a, bs, l2))
+        except Exception as e:  # a failing extra is reported, never hidden
+            res[fn.__name__ + "_error"] = f"{type(e).__name__}: {str(e)[:200]}"
+    try:
+        res.update(producer_rows(a, bs, W))
+    except Exception as e:
+        res["producer_rows_error"] = f"{type(e).__name__}: {str(e)[:200]}"
     res["paper_context"] = ("paper: 1.4-3.1x over cuBLAS/cuSPARSE/block-sparse on an unnamed ~2018 GPU (P:8, P:48); "
                             "context only, not a target")
     # oracle on host cores

@@ -77,6 +77,14 @@ size_t bs_packed_bytes(int64_t M, int64_t K, int block, int k, int dt, int layou
  * the data, and every layout gives results within the same tolerance. Returns -1 on invalid arguments. */
 int bs_choose_layout(int64_t M, int64_t K, int block, int k, int dt, int64_t N);
 
+/* Introspection for the bank-conflict model (tests/test_bank_model.py): the byte offset, within the
+ * shared-memory x slots of bs_spmv (nv = 1) or of a bs_spmm pass of nv columns on the SPMV layout
+ * (nv = 2, 4, 8, 16; 16-bit dtypes), of the `part`-th shared-memory load that gathers element
+ * (block b, offset o) of x (part 0, or 0 and 1 for nv = 16: two 16-byte loads). This is the paper's
+ * rearranged x (Fig. 3): the kernel stages and gathers x through the same functions.
+ * Returns -1 on invalid arguments. Host, pure. */
+int64_t bs_x_slot_offset(int64_t K, int block, int dt, int nv, int64_t b, int o, int part);
+
 /* Human-readable status name. */
 const char* bs_status_str(int status);
 
@@ -166,6 +174,20 @@ int bs_block_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int6
                   double sparsity, int criterion, uint8_t* mask, void* workspace, size_t workspace_bytes,
                   void* stream);
 
+/* bs_im2col: convolution as matrix multiplication, "using im2col that converts convolution operation to
+ * matrix-matrix multiplication", so that a conv layer whose kernels form one balanced-sparse
+ * weight matrix runs as bs_spmm (NEXT-3: N = pixels, the large-N regime of the tensor-core paths).
+ * Activations are NHWC (channels last); the weight matrix is Cout × (kh·kw·C) with columns in (dy, dx, c)
+ * order (torch weight.permute(0, 2, 3, 1); reading A23). Then bs_spmm(A, X) = Y [pixels][Cout]
+ * is the NHWC output.
+ *   in  device, [Nimg][H][W][C] of dt;  X  device out, [Nimg·OH·OW] rows of kh·kw·C elements, row stride ldx
+ *   X[(n·OH + oy)·OW + ox][(dy·kw + dx)·C + c] = in[n][oy·stride + dy - pad][ox·stride + dx - pad][c],
+ *   +0 outside the image; OH = (H + 2·pad - kh)/stride + 1, OW likewise. A pure copy (bit-exact).
+ * Errors: BS_ERR_SHAPE for non-positive sizes or a kernel larger than the padded image; BS_ERR_ARG for
+ * NULL pointers or ldx < kh·kw·C. */
+int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw, int pad,
+              int stride, void* X, int64_t ldx, void* stream);
+
 /* bs_pack: permute canonical (vals, idx) into the device layout `layout` and narrow the indices
  * (docs/layout.md). This is a pure permutation, so the output is byte-exact. The paper stores "the
  * same number of non-zero values in each block partition", so the format needs no row
@@ -217,6 +239,69 @@ typedef enum { BS_ACT_NONE = 0, BS_ACT_RELU = 1, BS_ACT_SIGMOID = 2, BS_ACT_TANH
  * Errors: as bs_spmv_ex; BS_ERR_ARG for an unknown act; BS_ERR_UNSUPPORTED for layout SP24. */
 int bs_spmv_fused(const bs_matrix* A, const void* x, const void* bias, int act, void* y, unsigned flags,
                   void* stream);
+
+/* bs_lstm_step: one step of an LSTM layer whose gate weights are balanced-sparse, in ONE kernel: the
+ * gate rows' SpMV with the cell applied in its epilogue. The recurrent workloads of the paper are LSTMs
+ * (PTB "2-layer LSTM ... 1500 hidden units", P:347 = BJ.configs[1]'s 6000 x 3000 [W_ih | W_hh];
+ * TIMIT Bi-LSTM, hidden 1024). The gate pre-activations are Eq. 1 with its +B:
+ *   z = W_bs · x + pre + bias
+ * with A's rows interleaved by unit: row 4j + g is gate g (0 input, 1 forget, 2 cell, 3 output) of
+ * hidden unit j (a row permutation applied before pruning, which is per row, so it commutes with it).
+ * Then, in fp32: i, f, o = sigmoid(z), g = tanh(z_g);  c_out[j] = f·c_prev[j] + i·g;
+ * h_out[j] = o·tanh(c_out[j]), rounded once to A->dt.
+ *   x       device, K elements of A->dt: [x_t ; h_{t-1}] for A = [W_ih | W_hh], or h_{t-1} for A = W_hh
+ *           with pre = W_ih·x_t computed ahead for all steps at once (one bs_spmm with N = T)
+ *   pre     device, M elements of A->dt, or NULL;  bias  device, M elements of A->dt, or NULL
+ *   c_prev  device, M/4 fp32;  c_out  device out, M/4 fp32;  h_out  device out, M/4 of A->dt
+ *   flags   as bs_spmv_ex. No output may alias an input (h_out must not point into x: use two
+ *           buffers and alternate them between steps).
+ * Errors: as bs_spmv_ex; BS_ERR_SHAPE if M mod 4 != 0; BS_ERR_UNSUPPORTED unless layout SPMV. */
+int bs_lstm_step(const bs_matrix* A, const void* x, const void* pre, const void* bias, const float* c_prev,
+                 void* h_out, float* c_out, unsigned flags, void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU: the all-gather fused into the SpMV */
+
+/* A row-sharded layer: rank r owns the rows [row0, row0 + A->M) of the M_total-row W_bs and
+ * every rank needs the whole y. bs_spmv_allgather computes the shard's rows and, in the same kernel,
+ * stores them straight into every rank's full y through peer-mapped pointers (NVLink / NVSwitch P2P);
+ * no separate collective runs (NEXT-1). Protocol per call (epoch e = 1, 2, ...):
+ *   1. each CTA parks its rows in shared memory, stores its contiguous run into y[p] + row0 for every
+ *      rank p, fences at system scope and increments *counter (this rank's, monotonic);
+ *   2. the CTA that brings *counter to e·(its grid size) fences again and stores e (release, system
+ *      scope) into flags[p][rank] on every rank p;
+ *   3. bs_allgather_wait (on each rank's stream) spins, acquire, until flags[rank][q] >= e for all q;
+ *      then the whole y of epoch e is visible to the kernels that follow on that stream.
+ * Buffers: y[p] (M_total elements of the dtype) and flags[p] (nranks uint32, zeroed before epoch 1) live
+ * on rank p and are mapped into every rank (bs_peer_export / bs_peer_import); counter is nranks-local
+ * (one uint32, zeroed before epoch 1). A rank must have consumed y of epoch e before it issues the
+ * SpMV of epoch e + 2 into the same buffer; alternating two y buffers by epoch parity makes that hold
+ * whenever each rank's stream orders its consumption of y_e before its epoch e + 1 wait (the Python
+ * FusedRowShardedBS does this). Epochs run to 2^32 / grid (about 29 million calls at 148 CTAs). */
+typedef struct {
+  int32_t nranks;     /* 1..8 */
+  int32_t rank;
+  int64_t row0;       /* global row of this shard's first row */
+  void* y[8];         /* every rank's full y, mapped into this process */
+  uint32_t* flags[8]; /* every rank's arrival flags (nranks words), mapped into this process */
+  uint32_t* counter;  /* this rank's CTA completion counter */
+  uint32_t epoch;     /* >= 1, incremented by one per call */
+} bs_allgather;
+
+/* y (every rank's, rows row0..row0 + A->M) = A·x, with bias/act as bs_spmv_fused (bias of A->M rows, or
+ * NULL; act a bs_act). Layout SPMV. Errors: as bs_spmv_fused; BS_ERR_ARG for a bad bs_allgather. */
+int bs_spmv_allgather(const bs_matrix* A, const void* x, const void* bias, int act, const bs_allgather* ag,
+                      unsigned flags, void* stream);
+
+/* Enqueues the wait of step 3 on `stream` (one tiny kernel). */
+int bs_allgather_wait(const bs_allgather* ag, void* stream);
+
+/* Peer mapping of a device buffer between processes of one node (CUDA IPC; the plumbing of
+ * bs_allgather). export: a 64-byte handle for the allocation that holds ptr, and ptr's byte offset in it.
+ * import: maps a handle exported by another process and returns the pointer at `offset` in it.
+ * close: unmaps an imported pointer. No device memory is allocated. */
+int bs_peer_export(const void* ptr, void* handle, int64_t* offset);
+int bs_peer_import(const void* handle, int64_t offset, void** ptr);
+int bs_peer_close(void* ptr, int64_t offset);
 
 /* bs_spmv_host: the same product with HOST x and y. The call enqueues H2D(x) -> bs_spmv -> D2H(y) on
  * `stream`, using caller-owned device scratch x_dev (K elements) and y_dev (M elements). x_host and

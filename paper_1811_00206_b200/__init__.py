@@ -30,7 +30,8 @@ LAYOUTS = {"spmv": 1, "spmm": 2, "sp24": 3}
 EXPORTS = ("bs_k_from_sparsity", "bs_packed_bytes", "bs_status_str", "bs_version", "bs_prune", "bs_prune_k",
            "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm", "bs_choose_layout", "bs_block_rank",
            "bs_schedule_sparsity", "bs_keep_count", "bs_decode", "bs_pattern_workspace_bytes", "bs_random_mask",
-           "bs_block_mask")
+           "bs_block_mask", "bs_lstm_step", "bs_im2col", "bs_spmv_allgather", "bs_allgather_wait", "bs_peer_export",
+           "bs_peer_import", "bs_peer_close", "bs_x_slot_offset")
 ACTS = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}  # bs_act (include/bs.h)
 SPMV_PDL, SPMV_W_STATIC = 1, 2  # bs_spmv_ex flags (include/bs.h)
 
@@ -44,6 +45,13 @@ class BSError(RuntimeError):
 class _Matrix(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int64), ("K", ctypes.c_int64), ("block", ctypes.c_int32), ("k", ctypes.c_int32),
                 ("dt", ctypes.c_int32), ("layout", ctypes.c_int32), ("packed", ctypes.c_void_p)]
+
+
+class _AllGather(ctypes.Structure):
+    """bs_allgather (include/bs.h)."""
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("row0", ctypes.c_int64),
+                ("y", ctypes.c_void_p * 8), ("flags", ctypes.c_void_p * 8), ("counter", ctypes.c_void_p),
+                ("epoch", ctypes.c_uint32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -82,7 +90,17 @@ def _load() -> ctypes.CDLL:
     L.bs_pattern_workspace_bytes.restype = ctypes.c_size_t
     L.bs_random_mask.argtypes = [vp, ci, i64, i64, i64, ctypes.c_double, vp, vp, ctypes.c_size_t, vp]
     L.bs_block_mask.argtypes = [vp, ci, i64, i64, i64, i64, i64, ctypes.c_double, ci, vp, vp, ctypes.c_size_t, vp]
-    for f in ("bs_decode", "bs_random_mask", "bs_block_mask"):
+    L.bs_lstm_step.argtypes = [ctypes.POINTER(_Matrix), vp, vp, vp, vp, vp, vp, ctypes.c_uint, vp]
+    L.bs_im2col.argtypes = [vp, ci, i64, i64, i64, i64, ci, ci, ci, ci, vp, i64, vp]
+    L.bs_x_slot_offset.argtypes = [i64, ci, ci, ci, i64, ci, ci]
+    L.bs_x_slot_offset.restype = i64
+    L.bs_spmv_allgather.argtypes = [ctypes.POINTER(_Matrix), vp, vp, ci, ctypes.POINTER(_AllGather), ctypes.c_uint, vp]
+    L.bs_allgather_wait.argtypes = [ctypes.POINTER(_AllGather), vp]
+    L.bs_peer_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_int64)]
+    L.bs_peer_import.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]
+    L.bs_peer_close.argtypes = [vp, ctypes.c_int64]
+    for f in ("bs_decode", "bs_random_mask", "bs_block_mask", "bs_lstm_step", "bs_im2col", "bs_spmv_allgather",
+              "bs_allgather_wait", "bs_peer_export", "bs_peer_import", "bs_peer_close"):
         getattr(L, f).restype = ci
     for f in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm"):
         getattr(L, f).restype = ci
@@ -455,3 +473,135 @@ def vector_mask(W: torch.Tensor, sparsity: float, axis: str = "row") -> torch.Te
     1×K or M×1 tile)."""
     M, K = W.shape
     return block_mask(W, 1, K, sparsity, "mean") if axis == "row" else block_mask(W, M, 1, sparsity, "mean")
+
+
+# ---------------------------------------------------------------- LSTM layers (PTB P:347, TIMIT P:369)
+
+def interleave_gates(W: torch.Tensor) -> torch.Tensor:
+    """PyTorch's gate-block row order (blocks i, f, g, o of H rows each) -> bs_lstm_step's interleaved
+    order (row 4j + g = gate g of unit j). Works for weights [4H, K] and biases [4H]."""
+    H = W.shape[0] // 4
+    return W.reshape(4, H, *W.shape[1:]).transpose(0, 1).reshape(W.shape).contiguous()
+
+
+def lstm_step(A: BSMatrix, x: torch.Tensor, c_prev: torch.Tensor, pre: torch.Tensor | None = None,
+              bias: torch.Tensor | None = None, h_out: torch.Tensor | None = None, c_out: torch.Tensor | None = None,
+              flags: int | None = None):
+    """One LSTM step in one kernel (bs_lstm_step): z = W_bs·x + pre + bias with interleaved gate rows, then
+    c = σ(z_f)·c_prev + σ(z_i)·tanh(z_g), h = σ(z_o)·tanh(c). Returns (h [M/4] of A.dtype, c [M/4] fp32)."""
+    _need_cuda(x, c_prev)
+    if A.M % 4:
+        raise ValueError("an LSTM gate matrix has 4·H rows")
+    H = A.M // 4
+    if x.dtype != A.dtype or x.numel() != A.K or not x.is_contiguous():
+        raise ValueError("x must be a contiguous vector of A.K elements of A.dtype")
+    if c_prev.dtype != torch.float32 or c_prev.numel() != H or not c_prev.is_contiguous():
+        raise ValueError("c_prev must be a contiguous fp32 vector of M/4 elements")
+    for v, name in ((pre, "pre"), (bias, "bias")):
+        if v is not None and (v.dtype != A.dtype or v.numel() != A.M or not v.is_contiguous() or not v.is_cuda):
+            raise ValueError(f"{name} must be a contiguous CUDA vector of A.M elements of A.dtype")
+    _same_device(A, x, c_prev, pre, bias)
+    if h_out is None:
+        h_out = torch.empty(H, dtype=A.dtype, device=x.device)
+    elif h_out.dtype != A.dtype or h_out.numel() != H or not h_out.is_contiguous() or h_out.device != x.device:
+        raise ValueError("h_out must be a contiguous vector of M/4 elements of A.dtype")
+    if c_out is None:
+        c_out = torch.empty(H, dtype=torch.float32, device=x.device)
+    elif c_out.dtype != torch.float32 or c_out.numel() != H or not c_out.is_contiguous() or c_out.device != x.device:
+        raise ValueError("c_out must be a contiguous fp32 vector of M/4 elements")
+    m = A.cstruct()
+    with torch.cuda.device(x.device):
+        st = lib().bs_lstm_step(ctypes.byref(m), x.data_ptr(), pre.data_ptr() if pre is not None else None,
+                                bias.data_ptr() if bias is not None else None, c_prev.data_ptr(), h_out.data_ptr(),
+                                c_out.data_ptr(), bs_flags_default() if flags is None else flags, _stream(x.device))
+    _check(st, "bs_lstm_step")
+    return h_out, c_out
+
+
+def lstm_sequence(A_ih: BSMatrix, A_hh: BSMatrix, X: torch.Tensor, h0: torch.Tensor, c0: torch.Tensor,
+                  bias: torch.Tensor | None = None):
+    """A whole LSTM layer over T steps with balanced-sparse W_ih and W_hh (gate rows interleaved):
+    the input projections of all steps are ONE batched product U = W_ih·X (bs_spmm, N = T; the
+    large-N SpMM of SURVEY NEXT-3), then each step is one bs_lstm_step on W_hh with pre = U[t].
+    X: [T, In]; h0: [H] of the dtype; c0: [H] fp32. Returns (hs [T, H], c_T)."""
+    T = X.shape[0]
+    H = A_hh.M // 4
+    U = spmm(A_ih, X)  # [T, 4H]
+    hs = torch.empty((T, H), dtype=A_hh.dtype, device=X.device)
+    c_bufs = (torch.empty(H, dtype=torch.float32, device=X.device), torch.empty(H, dtype=torch.float32, device=X.device))
+    h, c = h0, c0
+    for t in range(T):
+        c_next = c_bufs[t % 2]
+        lstm_step(A_hh, h, c, pre=U[t], bias=bias, h_out=hs[t], c_out=c_next)
+        h, c = hs[t], c_next
+    return hs, c
+
+
+# ---------------------------------------------------------------- convolution via im2col (P:286)
+
+def conv_weight_matrix(w: torch.Tensor) -> torch.Tensor:
+    """torch conv weight [Cout, C, kh, kw] -> the Cout × (kh·kw·C) matrix with (dy, dx, c) columns that
+    bs_im2col's X multiplies (reading A23). Prune / pack this matrix."""
+    return w.permute(0, 2, 3, 1).reshape(w.shape[0], -1).contiguous()
+
+
+def im2col(inp: torch.Tensor, kh: int, kw: int, pad: int = 0, stride: int = 1, out: torch.Tensor | None = None):
+    """NHWC [Nimg, H, W, C] -> X [Nimg·OH·OW, kh·kw·C] (bs_im2col)."""
+    _need_cuda(inp)
+    if inp.dim() != 4 or not inp.is_contiguous():
+        raise ValueError("inp must be a contiguous NHWC tensor [Nimg, H, W, C]")
+    Nimg, H, W, C = inp.shape
+    OH, OW = (H + 2 * pad - kh) // stride + 1, (W + 2 * pad - kw) // stride + 1
+    if OH < 1 or OW < 1:
+        raise ValueError("kernel larger than the padded image")
+    Kc = kh * kw * C
+    if out is None:
+        out = torch.empty((Nimg * OH * OW, Kc), dtype=inp.dtype, device=inp.device)
+    elif out.dtype != inp.dtype or out.shape[0] != Nimg * OH * OW or out.shape[1] != Kc or out.stride(1) != 1:
+        raise ValueError("out must be [Nimg·OH·OW, kh·kw·C] of inp.dtype with unit column stride")
+    with torch.cuda.device(inp.device):
+        st = lib().bs_im2col(inp.data_ptr(), _dt(inp), Nimg, H, W, C, kh, kw, pad, stride, out.data_ptr(),
+                             out.stride(0), _stream(inp.device))
+    _check(st, "bs_im2col")
+    return out
+
+
+def conv2d(A: BSMatrix, inp: torch.Tensor, kh: int, kw: int, pad: int = 0, stride: int = 1,
+           workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """A conv layer with the balanced-sparse Cout × (kh·kw·C) weight matrix A: im2col then bs_spmm.
+    NHWC in [Nimg, H, W, C], NHWC out [Nimg, OH, OW, Cout]."""
+    Nimg, H, W, C = inp.shape
+    if A.K != kh * kw * C:
+        raise ValueError("A.K must equal kh·kw·C")
+    X = im2col(inp, kh, kw, pad, stride, out=workspace)
+    OH, OW = (H + 2 * pad - kh) // stride + 1, (W + 2 * pad - kw) // stride + 1
+    return spmm(A, X).view(Nimg, OH, OW, A.M)
+
+
+# ---------------------------------------------------------------- multi-GPU: the all-gather fused into the SpMV
+
+def spmv_allgather(A: BSMatrix, x: torch.Tensor, ag: _AllGather, bias: torch.Tensor | None = None,
+                   act: str | None = None, flags: int | None = None):
+    """bs_spmv_allgather: this rank's row shard of y = act(W_bs·x + bias), stored by the kernel into every
+    rank's y (ag.y[p] + ag.row0). Use through dist.FusedRowShardedBS."""
+    _need_cuda(x)
+    if x.dtype != A.dtype or x.numel() != A.K or not x.is_contiguous():
+        raise ValueError("x must be a contiguous vector of A.K elements of A.dtype")
+    if bias is not None and (bias.dtype != A.dtype or bias.numel() != A.M or not bias.is_cuda):
+        raise ValueError("bias must be a CUDA vector of A.M elements of A.dtype")
+    if act not in ACTS:
+        raise ValueError(f"act must be one of {sorted(k for k in ACTS if k)}")
+    _same_device(A, x, bias)
+    m = A.cstruct()
+    with torch.cuda.device(x.device):
+        st = lib().bs_spmv_allgather(ctypes.byref(m), x.data_ptr(), bias.data_ptr() if bias is not None else None,
+                                     ACTS[act], ctypes.byref(ag), bs_flags_default() if flags is None else flags,
+                                     _stream(x.device))
+    _check(st, "bs_spmv_allgather")
+
+
+def allgather_wait(ag: _AllGather, device):
+    """bs_allgather_wait on the current stream of `device`."""
+    with torch.cuda.device(device):
+        st = lib().bs_allgather_wait(ctypes.byref(ag), _stream(device))
+    _check(st, "bs_allgather_wait")

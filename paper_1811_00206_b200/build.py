@@ -26,16 +26,20 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", f"-I{INCLUDE}", f"-I{CSRC}"]
 
-SOURCES = ["bs_api.cu", "prune.cu", "pack.cu", "spmv.cu", "spmv_f16.cu", "spmv_bf16.cu", "spmv_f16_batch.cu", "spmv_bf16_batch.cu", "spmv_f32.cu", "spmm.cu", "spmm24.cu", "patterns.cu"]
+SOURCES = ["bs_api.cu", "prune.cu", "pack.cu", "spmv.cu", "spmv_f16.cu", "spmv_bf16.cu", "spmv_f16_batch.cu", "spmv_bf16_batch.cu", "spmv_f32.cu", "spmm.cu", "spmm24.cu", "patterns.cu", "conv.cu"]
 
 
-def _deps_mtime() -> float:
-    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "bs.h"), __file__]
+def _headers_mtime() -> float:
+    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    files += [os.path.join(INCLUDE, "bs.h"), __file__]
     return max(os.path.getmtime(f) for f in files if os.path.isfile(f))
 
 
-def _compile(src: str, verbose: bool) -> str:
+def _compile(src: str, verbose: bool, force: bool = True) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+    if not force and os.path.exists(obj):  # up to date: newer than its source and every header
+        if os.path.getmtime(obj) >= max(os.path.getmtime(os.path.join(CSRC, src)), _headers_mtime()):
+            return obj
     cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]
@@ -48,11 +52,13 @@ def _compile(src: str, verbose: bool) -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
-        return LIB
+    """Compile the objects that are older than their source or any header (all with force), then relink
+    libbs.so if any object is newer than it."""
     os.makedirs(BUILD, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+        objs = list(ex.map(lambda s: _compile(s, verbose, force), SOURCES))
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
+        return LIB
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

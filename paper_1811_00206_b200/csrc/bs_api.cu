@@ -1,11 +1,14 @@
 // bs_api.cu: the C ABI of libbs.so (include/bs.h). It validates arguments and dispatches to the
 // kernels. It never allocates device memory and never synchronises.
+#include <cuda.h>
 #include <math.h>
+#include <string.h>
 #include <map>
 #include <mutex>
 #include <utility>
 
 #include "bs_common.cuh"
+#include "spmv_impl.cuh"
 
 int64_t bsk_spmv_smem_bytes(const bsk::Geom& g);
 
@@ -224,6 +227,27 @@ int bs_block_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int6
       bsk_launch_block_mask(W, dt, M, K, ldw, bh, bw, sparsity, criterion, mask, workspace, (cudaStream_t)stream));
 }
 
+int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw, int pad,
+              int stride, void* X, int64_t ldx, void* stream) {
+  if (!valid_dt(dt)) return BS_ERR_DTYPE;
+  if (Nimg < 1 || H < 1 || W < 1 || C < 1 || kh < 1 || kw < 1 || pad < 0 || stride < 1) return BS_ERR_SHAPE;
+  const int64_t OH = (H + 2 * pad - kh) / stride + 1, OW = (W + 2 * pad - kw) / stride + 1;
+  if (H + 2 * pad < kh || W + 2 * pad < kw || OH < 1 || OW < 1) return BS_ERR_SHAPE;
+  if (!in || !X || ldx < (int64_t)kh * kw * C) return BS_ERR_ARG;
+  return from_cuda(bsk_launch_im2col(in, dt, Nimg, H, W, C, kh, kw, pad, stride, X, ldx, (cudaStream_t)stream));
+}
+
+int64_t bs_x_slot_offset(int64_t K, int block, int dt, int nv, int64_t b, int o, int part) {
+  bsk::Geom g;
+  if (!bsk::make_geom(1, K, block, 1, dt, BS_LAYOUT_SPMV, &g)) return -1;
+  if (b < 0 || b >= g.NB || o < 0 || o >= block || part < 0 || part > (nv == 16 ? 1 : 0)) return -1;
+  if (!(nv == 1 || ((nv == 2 || nv == 4 || nv == 8 || nv == 16) && g.es == 2))) return -1;
+  const bool pair = g.es == 2 && nv == 1;  // as launch_spmv_nv / the kernel's PAIR
+  return (int64_t)bsk_spmv::x_slot((uint32_t)(b >> 5), (uint32_t)o, (uint32_t)(b & 31), (uint32_t)block,
+                                   (uint32_t)g.es, (uint32_t)nv, pair) +
+         (int64_t)bsk_spmv::x_part_off((uint32_t)(b & 31), (uint32_t)nv, (uint32_t)part);
+}
+
 int bs_spmv_ex(const bs_matrix* A, const void* x, void* y, unsigned flags, void* stream) {
   bsk::Geom g;
   int st = matrix_geom(A, &g);
@@ -247,6 +271,82 @@ int bs_spmv_fused(const bs_matrix* A, const void* x, const void* bias, int act, 
   if (act < BS_ACT_NONE || act > BS_ACT_TANH) return BS_ERR_ARG;
   if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;
   return from_cuda(bsk_launch_spmv(g, A->packed, x, y, flags, (cudaStream_t)stream, bias, act));
+}
+
+int bs_lstm_step(const bs_matrix* A, const void* x, const void* pre, const void* bias, const float* c_prev,
+                 void* h_out, float* c_out, unsigned flags, void* stream) {
+  bsk::Geom g;
+  int st = matrix_geom(A, &g);
+  if (st) return st;
+  if (!x || !c_prev || !h_out || !c_out) return BS_ERR_ARG;
+  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC)) return BS_ERR_ARG;
+  if (g.M % 4 != 0) return BS_ERR_SHAPE;
+  if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;
+  const bsk::LstmIO io{pre, c_prev, c_out, h_out};
+  return from_cuda(bsk_launch_lstm(g, A->packed, x, bias, io, flags, (cudaStream_t)stream));
+}
+
+static bool valid_ag(const bs_allgather* ag) {
+  if (!ag || ag->nranks < 1 || ag->nranks > 8 || ag->rank < 0 || ag->rank >= ag->nranks || ag->row0 < 0) return false;
+  if (!ag->counter || ag->epoch == 0) return false;
+  for (int p = 0; p < ag->nranks; ++p)
+    if (!ag->y[p] || !ag->flags[p]) return false;
+  return true;
+}
+
+int bs_spmv_allgather(const bs_matrix* A, const void* x, const void* bias, int act, const bs_allgather* ag,
+                      unsigned flags, void* stream) {
+  bsk::Geom g;
+  int st = matrix_geom(A, &g);
+  if (st) return st;
+  if (!x || !valid_ag(ag)) return BS_ERR_ARG;
+  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC)) return BS_ERR_ARG;
+  if (act < BS_ACT_NONE || act > BS_ACT_TANH) return BS_ERR_ARG;
+  if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;
+  return from_cuda(bsk_launch_spmv_allgather(g, A->packed, x, *ag, flags, (cudaStream_t)stream, bias, act));
+}
+
+int bs_allgather_wait(const bs_allgather* ag, void* stream) {
+  if (!valid_ag(ag)) return BS_ERR_ARG;
+  return from_cuda(bsk_launch_allgather_wait(*ag, (cudaStream_t)stream));
+}
+
+using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+int bs_peer_export(const void* ptr, void* handle, int64_t* offset) {
+  if (!ptr || !handle || !offset) return BS_ERR_ARG;
+  static AddrRangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return BS_ERR_CUDA;
+    fn = (AddrRangeFn)p;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return BS_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, (void*)base) != cudaSuccess) return BS_ERR_CUDA;
+  memcpy(handle, &h, sizeof(h));
+  *offset = (int64_t)((CUdeviceptr)ptr - base);
+  return BS_OK;
+}
+
+int bs_peer_import(const void* handle, int64_t offset, void** ptr) {
+  if (!handle || !ptr || offset < 0) return BS_ERR_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return BS_ERR_CUDA;
+  *ptr = (char*)base + offset;
+  return BS_OK;
+}
+
+int bs_peer_close(void* ptr, int64_t offset) {
+  if (!ptr || offset < 0) return BS_ERR_ARG;
+  return cudaIpcCloseMemHandle((char*)ptr - offset) == cudaSuccess ? BS_OK : BS_ERR_CUDA;
 }
 
 int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream) {

@@ -131,10 +131,26 @@ cudaError_t bsk_launch_random_mask(const void* W, int dt, int64_t M, int64_t K, 
                                    uint8_t* mask, void* ws, cudaStream_t s);
 cudaError_t bsk_launch_block_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int64_t bh, int64_t bw,
                                   double sparsity, int criterion, uint8_t* mask, void* ws, cudaStream_t s);
+cudaError_t bsk_launch_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw,
+                              int pad, int stride, void* X, int64_t ldx, cudaStream_t s);
 cudaError_t bsk_launch_unpack(const void* packed, const bsk::Geom& g, void* vals, uint16_t* idx,
                               cudaStream_t s);
 cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, unsigned flags,
                             cudaStream_t s, const void* bias = nullptr, int act = 0);
+namespace bsk {
+// Operands of the fused LSTM step (bs_lstm_step).
+struct LstmIO {
+  const void* pre;      // M elements of D or NULL
+  const float* c_prev;  // M/4
+  float* c_out;         // M/4
+  void* h_out;          // M/4 of D
+};
+}  // namespace bsk
+cudaError_t bsk_launch_spmv_allgather(const bsk::Geom& g, const void* packed, const void* x, const bs_allgather& ag,
+                                      unsigned flags, cudaStream_t s, const void* bias, int act);
+cudaError_t bsk_launch_allgather_wait(const bs_allgather& ag, cudaStream_t s);
+cudaError_t bsk_launch_lstm(const bsk::Geom& g, const void* packed, const void* x, const void* bias,
+                            const bsk::LstmIO& io, unsigned flags, cudaStream_t s);
 cudaError_t bsk_launch_spmv_batch(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,
                                   void* Y, int64_t ldy, cudaStream_t s);
 // spmv: the batch-1 product of bs_spmv (CUDA cores, HBM-bound). Otherwise the batched product of bs_spmm,

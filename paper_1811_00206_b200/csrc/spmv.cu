@@ -18,11 +18,38 @@ cudaError_t bsk_spmv_dispatch_f32(const bsk::Geom& g, const SpmvArgs& a, cudaStr
 // (NV = 2, 4, 8 accumulate each column in the same order), i.e. on N.
 static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const void* x, int64_t ldx, void* y,
                                   int64_t ldy, int ncols, int nv, int chunk_nv, unsigned flags, cudaStream_t s,
-                                  const void* bias = nullptr, int act = 0) {
+                                  const void* bias = nullptr, int act = 0, const bsk::LstmIO* lstm = nullptr,
+                                  const bs_allgather* ag = nullptr) {
   SpmvArgs a;
+  a.ag_n = 0;
+  a.ag_rank = 0;
+  a.ag_row0 = 0;
+  a.ag_cnt = nullptr;
+  a.ag_epoch = 0;
+  a.ag_off = 0;
+  for (int p = 0; p < 8; ++p) {
+    a.ag_y[p] = nullptr;
+    a.ag_flag[p] = nullptr;
+  }
+  if (ag && nv == 1) {
+    a.ag_n = ag->nranks;
+    a.ag_rank = ag->rank;
+    a.ag_row0 = ag->row0;
+    a.ag_cnt = ag->counter;
+    a.ag_epoch = ag->epoch;
+    for (int p = 0; p < ag->nranks; ++p) {
+      a.ag_y[p] = ag->y[p];
+      a.ag_flag[p] = ag->flags[p];
+    }
+  }
   a.bias = nv == 1 ? bias : nullptr;
   a.act = nv == 1 ? act : 0;
   a.bias_off = 0;
+  a.lstm = nv == 1 && lstm != nullptr;
+  a.pre = a.lstm ? lstm->pre : nullptr;
+  a.c_prev = a.lstm ? lstm->c_prev : nullptr;
+  a.c_out = a.lstm ? lstm->c_out : nullptr;
+  a.h_out = a.lstm ? lstm->h_out : nullptr;
   a.pdl = (flags & BS_SPMV_PDL) != 0;
   a.w_early = a.pdl && (flags & BS_SPMV_W_STATIC) != 0;
   const uint8_t* base = (const uint8_t*)packed;
@@ -48,8 +75,9 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
   const int64_t group_bytes = (int64_t)g.B * 32 * g.es * nv;  // 32 blocks of x slots
   const int64_t chunk_group = (int64_t)g.B * 32 * g.es * chunk_nv;
   const int64_t tail_groups = (g.NB + 31) / 32 - g.NBf * g.V;
-  // 16-bit SpMV with V >= 2 stores x in group pairs (spmv_impl.cuh stage_x PAIR): round staged groups up to even
-  const bool pair = g.es == 2 && nv == 1 && g.V >= 2;
+  // 16-bit SpMV stores x in group pairs (spmv_impl.cuh stage_x PAIR): round staged groups up to even. With V = 1
+  // unpaired halfword slots put lanes 2m, 2m+1 in one bank with different offsets (2-way conflicts, T2 model)
+  const bool pair = g.es == 2 && nv == 1;
   auto ev = [&](int64_t n) { return pair ? (n + 1) / 2 * 2 : n; };
   if (g.NBf > 0 && g.k > 0) {
     int64_t PC = kXBudget / (chunk_group * g.V);
@@ -88,6 +116,39 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
 cudaError_t bsk_launch_spmv(const bsk::Geom& g, const void* packed, const void* x, void* y, unsigned flags,
                             cudaStream_t s, const void* bias, int act) {
   return launch_spmv_nv(g, packed, x, 0, y, 0, 1, 1, 1, flags, s, bias, act);
+}
+
+// The row shard's SpMV with the all-gather of y fused into its epilogue (spmv_impl.cuh).
+cudaError_t bsk_launch_spmv_allgather(const bsk::Geom& g, const void* packed, const void* x, const bs_allgather& ag,
+                                      unsigned flags, cudaStream_t s, const void* bias, int act) {
+  return launch_spmv_nv(g, packed, x, 0, ag.y[ag.rank], 0, 1, 1, 1, flags, s, bias, act, nullptr, &ag);
+}
+
+namespace {
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Waits until every rank's flag on this rank has reached `epoch` (wrap-safe compare: a faster rank may
+// already have raised the next epoch).
+__global__ void ag_wait_kernel(const uint32_t* flags, int n, uint32_t epoch) {
+  const int i = threadIdx.x;
+  if (i < n)
+    while ((int32_t)(ld_acquire_sys_u32(flags + i) - epoch) < 0) __nanosleep(64);
+  __syncwarp();
+}
+}  // namespace
+
+cudaError_t bsk_launch_allgather_wait(const bs_allgather& ag, cudaStream_t s) {
+  ag_wait_kernel<<<1, 32, 0, s>>>(ag.flags[ag.rank], ag.nranks, ag.epoch);
+  return cudaGetLastError();
+}
+
+// One LSTM step: the gate rows' SpMV with the cell applied in the kernel's epilogue (spmv_impl.cuh).
+cudaError_t bsk_launch_lstm(const bsk::Geom& g, const void* packed, const void* x, const void* bias,
+                            const bsk::LstmIO& io, unsigned flags, cudaStream_t s) {
+  return launch_spmv_nv(g, packed, x, 0, io.h_out, 0, 1, 1, 1, flags, s, bias, 0, &io);
 }
 
 // Batched product on the SPMV layout (16-bit): passes of up to 8 batch columns, each one stream of W;

@@ -82,7 +82,36 @@ struct SpmvArgs {
   const void* bias;  // NV = 1: optional per-row bias (M elements of D), Eq. 1's +B
   int act;           // NV = 1: bs_act applied after the bias (BS_ACT_NONE = 0)
   uint32_t bias_off; // shared-memory byte offset of the CTA's bias rows (fp32)
+  // LSTM cell epilogue (bs_lstm_step; NV = 1): rows are gate rows interleaved 4j + g (i, f, g, o of
+  // unit j). The CTA's row range is a whole number of units; each row's z = W·x + pre + bias is parked
+  // in shared memory (in place of its bias) and, once the CTA's rows are done, one thread per unit
+  // applies the cell: c = sigmoid(z_f)·c_prev + sigmoid(z_i)·tanh(z_g), h = sigmoid(z_o)·tanh(c).
+  int lstm;
+  const void* pre;     // a second per-row addend of D (W_ih·x_t computed ahead), or NULL
+  const float* c_prev; // M/4 fp32
+  float* c_out;        // M/4 fp32
+  void* h_out;         // M/4 of D
+  // Fused all-gather epilogue (bs_spmv_allgather; NV = 1): this launch computes one rank's row shard;
+  // its rows are parked in shared memory and each CTA stores its contiguous run to every rank's full y
+  // (peer-mapped pointers over NVLink), then the last CTA raises this rank's flag on every rank.
+  int ag_n;             // ranks (0: off)
+  int ag_rank;
+  int64_t ag_row0;      // global row of the shard's first row
+  void* ag_y[8];        // every rank's full y (M_total elements of D)
+  uint32_t* ag_flag[8]; // every rank's arrival flags (ag_n words)
+  uint32_t* ag_cnt;     // this rank's CTA completion counter (monotonic)
+  uint32_t ag_epoch;    // call number, >= 1
+  uint32_t ag_off;      // shared-memory byte offset of the parked y rows
 };
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // Layer epilogue y = act(W·x + b) in fp32 before the single rounding to D (bs_spmv_fused).
 __device__ __forceinline__ float apply_act(float v, int act) {
@@ -140,13 +169,33 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
   return b8;
 }
 
+// Byte offset, from the start of a chunk's x slots, of element (block 32·(g0 + gl) + lane, offset o) of
+// the rearranged x (the paper's conflict-free x): ES-byte slots (NV = 1), paired 16-bit
+// groups (PAIR), or 2·NV-byte batch slots (NV > 1). stage_x / stage_xn store through it; the gathers read
+// the same slots (the unit-vector and integer-exact parity tests prove it), and bs_x_slot_offset exports
+// it to the host bank-conflict model (tests/test_bank_model.py).
+__host__ __device__ __forceinline__ uint32_t x_slot(uint32_t gl, uint32_t o, uint32_t lane, uint32_t B, uint32_t ES,
+                                                    uint32_t NV, bool pair) {
+  if (NV > 1) return (gl * B + o) * (32u * 2u * NV) + lane * 2u * NV;
+  if (pair) return ((gl >> 1) * B + o) * 128u + lane * 4u + (gl & 1u) * 2u;
+  return (gl * B + o) * (32u * ES) + lane * ES;
+}
+
+// NV = 16: a slot is 32 bytes (two 16-byte halves, columns 0-7 and 8-15), read by two LDS.128. A 16-byte
+// request is served 8 lanes per wavefront; with the halves in column order, lanes l and l + 4 of a phase
+// would hit the same banks (slot stride 32 B: 2-way conflicts, found by the T2 model). So lane l keeps
+// columns 0-7 in half ((l >> 2) & 1) and columns 8-15 in the other: byte offset of part p in the slot.
+__host__ __device__ __forceinline__ uint32_t x_part_off(uint32_t lane, uint32_t NV, uint32_t part) {
+  return NV == 16 ? 16u * (((lane >> 2) & 1u) ^ part) : 0u;
+}
+
 // Stage the x columns of groups [g0, g1) into slots of ES bytes (halfwords for f16/bf16, words
 // for f32): element (b, o), b = 32·g + l, goes to slot (gl·B + o)·32 + l, gl = g - g0. Lane l always
 // copies block 32·g + l. So for f32 every slot of lane l is in bank l, and for 16-bit x the lanes
 // 2m and 2m+1 share a word. Work items are (group, 16-byte piece of a block); each lane issues up to
 // 8 piece loads before storing them. `after_loads()` runs once, right after the first batch of
 // loads is in flight, so that the caller can queue the W bulk copies behind them.
-// PAIR (16-bit x, V >= 2): groups 2j and 2j+1 share slot words. Element (b, o), b = 32·g + l, goes to
+// PAIR (16-bit x, any V; a single group is paired with an empty one): groups 2j and 2j+1 share slot words. Element (b, o), b = 32·g + l, goes to
 // byte ((g>>1)·B + o)·128 + 4·l + 2·(g&1): lane l's slots are all in bank l, for any offsets (with
 // halfword slots per group, lanes 2m and 2m+1 would share a bank with different offsets: 2-way
 // conflicts). The consumer's group index is compile-time, so the address is still one IMAD.
@@ -184,8 +233,7 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint32_t sx, int64_t 
           const uint32_t q = j - gl * ppb;
           const int64_t b = (g0 + gl) * 32 + lane;
           if (b < a.NB) {
-            const uint32_t col = PAIR ? sx + ((gl >> 1) * B + q * PE) * ROWB + lane * 4 + (gl & 1) * 2
-                                      : sx + (gl * B + q * PE) * ROWB + lane * ES;
+            const uint32_t col = sx + x_slot(gl, q * PE, lane, B, ES, 1, PAIR);
             const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
             for (int e = 0; e < PE; ++e) {
@@ -202,8 +250,7 @@ __device__ __forceinline__ void stage_x(const SpmvArgs& a, uint32_t sx, int64_t 
       const int64_t b = g * 32 + lane;
       if (b >= a.NB) continue;
       const uint32_t gl = (uint32_t)(g - g0);
-      const uint32_t col = PAIR ? sx + (gl >> 1) * (uint32_t)B * ROWB + lane * 4 + (gl & 1) * 2
-                                : sx + gl * (uint32_t)B * ROWB + lane * ES;
+      const uint32_t col = sx + x_slot(gl, 0, lane, B, ES, 1, PAIR);
       for (int o = 0; o < B; ++o) {
         if (ES == 2) bsk::sts_u16(col + o * ROWB, __ldg((const uint16_t*)a.x + b * B + o));
         else bsk::sts_u32(col + o * ROWB, __ldg((const uint32_t*)a.x + b * B + o));
@@ -241,7 +288,7 @@ __device__ __forceinline__ void stage_xn(const SpmvArgs& a, uint32_t sx, int64_t
         hooked = true;
       }
       if (ok) {
-        const uint32_t col = sx + (gl * B + q * 8) * ROWB + lane * SLB;
+        const uint32_t col = sx + x_slot(gl, q * 8, lane, B, 2, NV, false);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           uint32_t h[NV];
@@ -251,8 +298,8 @@ __device__ __forceinline__ void stage_xn(const SpmvArgs& a, uint32_t sx, int64_t
             h[n] = (w >> (16 * (e & 1))) & 0xffffu;
           }
           if constexpr (NV == 16) {
-            bsk::sts_v4(col + e * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
-            bsk::sts_v4(col + e * ROWB + 16, h[8] | (h[9] << 16), h[10] | (h[11] << 16), h[12] | (h[13] << 16), h[14] | (h[15] << 16));
+            bsk::sts_v4(col + e * ROWB + x_part_off(lane, 16, 0), h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+            bsk::sts_v4(col + e * ROWB + x_part_off(lane, 16, 1), h[8] | (h[9] << 16), h[10] | (h[11] << 16), h[12] | (h[13] << 16), h[14] | (h[15] << 16));
           } else if constexpr (NV == 8) bsk::sts_v4(col + e * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
           else if constexpr (NV == 4) asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(col + e * ROWB), "r"(h[0] | (h[1] << 16)), "r"(h[2] | (h[3] << 16)));
           else bsk::sts_u32(col + e * ROWB, h[0] | (h[1] << 16));
@@ -265,14 +312,14 @@ __device__ __forceinline__ void stage_xn(const SpmvArgs& a, uint32_t sx, int64_t
     for (int64_t g = g0 + warp; g < g1; g += nw) {
       const int64_t b = g * 32 + lane;
       if (b >= a.NB) continue;
-      const uint32_t col = sx + (uint32_t)(g - g0) * (uint32_t)B * ROWB + lane * SLB;
+      const uint32_t col = sx + x_slot((uint32_t)(g - g0), 0, lane, B, 2, NV, false);
       for (int o = 0; o < B; ++o) {
         uint32_t h[NV];
 #pragma unroll
         for (int n = 0; n < NV; ++n) h[n] = n < a.ncols ? (uint32_t)__ldg((const uint16_t*)a.x + n * a.ldx + b * B + o) : 0u;
         if constexpr (NV == 16) {
-          bsk::sts_v4(col + o * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
-          bsk::sts_v4(col + o * ROWB + 16, h[8] | (h[9] << 16), h[10] | (h[11] << 16), h[12] | (h[13] << 16), h[14] | (h[15] << 16));
+          bsk::sts_v4(col + o * ROWB + x_part_off(lane, 16, 0), h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+          bsk::sts_v4(col + o * ROWB + x_part_off(lane, 16, 1), h[8] | (h[9] << 16), h[10] | (h[11] << 16), h[12] | (h[13] << 16), h[14] | (h[15] << 16));
         } else if constexpr (NV == 8) bsk::sts_v4(col + o * ROWB, h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
         else if constexpr (NV == 4) asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(col + o * ROWB), "r"(h[0] | (h[1] << 16)), "r"(h[2] | (h[3] << 16)));
         else bsk::sts_u32(col + o * ROWB, h[0] | (h[1] << 16));
@@ -347,15 +394,17 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   const int B = BT > 0 ? BT : a.B;
   constexpr uint32_t SLB = ES * NV;       // bytes per x slot (NV batch columns of one x column)
   constexpr uint32_t ROWB = 32 * SLB;     // bytes per slot row of x (one offset o of 32 blocks)
-  constexpr bool PAIR = ES == 2 && NV == 1 && V >= 2;  // paired groups (stage_x): lane l stays in bank l
+  constexpr bool PAIR = ES == 2 && NV == 1;  // paired groups (stage_x): lane l stays in bank l (tests/test_bank_model.py)
   constexpr uint32_t XROW = PAIR ? 128u : ROWB;         // slot-row stride seen by the gathers
   constexpr uint32_t LSLB = PAIR ? 4u : SLB;            // lane stride of the slots
   constexpr int NA = NV == 1 ? V : NV;    // accumulators: V chains (SpMV) or one per batch column
   const uint32_t GSW = (uint32_t)B * ROWB;  // bytes per group of 32 blocks
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = NT / 32;
-  // balanced row ranges (32-bit arithmetic: M·(grid + 1) < 2^32 is checked on the host)
-  const int64_t rb = blockIdx.x * (uint32_t)a.M / gridDim.x;
-  const int64_t re = (blockIdx.x + 1) * (uint32_t)a.M / gridDim.x;
+  // balanced row ranges (32-bit arithmetic: M·(grid + 1) < 2^32 is checked on the host); the LSTM
+  // epilogue needs whole units (4 gate rows) per CTA
+  const uint32_t RU = (NV == 1 && a.lstm) ? 4u : 1u;
+  const int64_t rb = RU * (blockIdx.x * ((uint32_t)a.M / RU) / gridDim.x);
+  const int64_t re = RU * ((blockIdx.x + 1) * ((uint32_t)a.M / RU) / gridDim.x);
   const uint32_t nr = (uint32_t)(re - rb);
   const int64_t wr0 = rb + warp * nr / nw;
   const int64_t nrows = rb + (warp + 1) * nr / nw - wr0;
@@ -468,8 +517,8 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
       uint32_t xw[NV / 2 > 4 ? NV / 2 : 4];
       const uint32_t ad = base + o * ROWB + v * GSW;
       if constexpr (NV == 16) {
-        bsk::lds_v4(ad, xw[0], xw[1], xw[2], xw[3]);
-        bsk::lds_v4(ad + 16, xw[4], xw[5], xw[6], xw[7]);
+        bsk::lds_v4(ad + x_part_off(lane, 16, 0), xw[0], xw[1], xw[2], xw[3]);
+        bsk::lds_v4(ad + x_part_off(lane, 16, 1), xw[4], xw[5], xw[6], xw[7]);
       } else if constexpr (NV == 8) bsk::lds_v4(ad, xw[0], xw[1], xw[2], xw[3]);
       else if constexpr (NV == 4) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(xw[0]), "=r"(xw[1]) : "r"(ad));
       else xw[0] = bsk::lds_u32(ad);
@@ -494,12 +543,18 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   };
   // the CTA's bias rows are staged into shared memory with the first x staging (their loads go out
   // before the x loads and land while x is staged), so the epilogue adds no global round trip
-  const bool has_bias = NV == 1 && a.bias != nullptr;
+  const bool lstm = NV == 1 && a.lstm;
+  const bool ag = NV == 1 && a.ag_n > 0;
+  const bool has_bias = NV == 1 && (a.bias != nullptr || a.pre != nullptr || lstm);
   float* sbias = (float*)(smem + xoff + a.bias_off);
   // each thread prefetches up to 4 bias rows into registers before the x loads; stored after them
   float bp0 = 0.f, bp1 = 0.f, bp2 = 0.f, bp3 = 0.f;
   bool bias_done = false;
-  auto bias_ld = [&](uint32_t i) { return bsk::to_float<DT>(__ldg((const raw_t*)a.bias + rb + i)); };
+  auto bias_ld = [&](uint32_t i) {
+    float b = a.bias ? bsk::to_float<DT>(__ldg((const raw_t*)a.bias + rb + i)) : 0.f;
+    if (a.pre) b += bsk::to_float<DT>(__ldg((const raw_t*)a.pre + rb + i));
+    return b;
+  };
   auto bias_issue = [&]() {
     if (has_bias && !bias_done) {
       const uint32_t i = threadIdx.x;
@@ -523,7 +578,15 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   auto store_y = [&](int64_t r, int col, float y) {
     if (NV == 1) {
       if (has_bias) y += sbias[r - rb];
+      if (lstm) {  // the gate pre-activation z waits in shared memory for the cell epilogue
+        sbias[r - rb] = y;
+        return;
+      }
       if (a.act) y = apply_act(y, a.act);
+      if (ag) {  // parked for the fused all-gather epilogue
+        ((raw_t*)(smem + xoff + a.ag_off))[r - rb] = (raw_t)bsk::from_float<DT>(y);
+        return;
+      }
       ((raw_t*)a.y)[r] = (raw_t)bsk::from_float<DT>(y);
     }
     else if (col < a.ncols) ((raw_t*)a.y)[col * a.ldy + r] = (raw_t)bsk::from_float<DT>(y);
@@ -734,6 +797,33 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
     __syncwarp();
     for (int64_t i = lane; i < nrows * NV; i += 32) store_y(wr0 + i / NV, (int)(i % NV), part[(wr0 + i / NV) * NV + i % NV]);
   }
+  if (lstm) {  // LSTM cell over the CTA's units, from the gate pre-activations in shared memory
+    __syncthreads();
+    for (uint32_t u = threadIdx.x; u < nr / 4; u += NT) {
+      const float zi = sbias[4 * u], zf = sbias[4 * u + 1], zg = sbias[4 * u + 2], zo = sbias[4 * u + 3];
+      const int64_t j = rb / 4 + u;
+      const float c = apply_act(zf, BS_ACT_SIGMOID) * a.c_prev[j] + apply_act(zi, BS_ACT_SIGMOID) * apply_act(zg, BS_ACT_TANH);
+      a.c_out[j] = c;
+      ((raw_t*)a.h_out)[j] = (raw_t)bsk::from_float<DT>(apply_act(zo, BS_ACT_SIGMOID) * apply_act(c, BS_ACT_TANH));
+    }
+  }
+  if (ag) {  // fused all-gather: the CTA's rows to every rank's y, then the completion protocol
+    __syncthreads();
+    const raw_t* sy = (const raw_t*)(smem + xoff + a.ag_off);
+    for (int p = 0; p < a.ag_n; ++p) {
+      raw_t* dst = (raw_t*)a.ag_y[p] + a.ag_row0 + rb;
+      for (uint32_t i = threadIdx.x; i < nr; i += NT) dst[i] = sy[i];
+    }
+    __syncthreads();  // every thread's peer stores precede thread 0's fence (cumulativity)
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const uint32_t prev = atomicAdd(a.ag_cnt, 1u);
+      if (prev == a.ag_epoch * gridDim.x - 1u) {  // the last CTA: every CTA's stores are fenced
+        __threadfence_system();
+        for (int p = 0; p < a.ag_n; ++p) st_release_sys(a.ag_flag[p] + a.ag_rank, a.ag_epoch);
+      }
+    }
+  }
   BS_MARK(8);
 }
 
@@ -768,16 +858,21 @@ cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   int64_t grid = dp.sms;
   const int64_t need = (a.M + (NT / 32) - 1) / (NT / 32);
   if (grid > need) grid = need;
-  const int64_t scratch = MULTI ? ((a.M + grid - 1) / grid + 1) * 4 * NV : 0;
-  const int64_t bias_bytes = a.bias ? ((a.M + grid - 1) / grid + 1) * 4 : 0;
+  // most rows a CTA owns: ceil(M / grid), plus 4 when the LSTM epilogue rounds row ranges to whole units
+  const int64_t rows_max = (a.M + grid - 1) / grid + (a.lstm ? 4 : 1);
+  const int64_t scratch = MULTI ? rows_max * 4 * NV : 0;
+  const int64_t bias_bytes = (a.bias || a.pre || a.lstm) ? rows_max * 4 : 0;
+  const int64_t ag_bytes = a.ag_n > 0 ? bsk::align_up(rows_max * ES, 16) : 0;
   const int64_t xslack = (IS == 5 && NV == 1) ? 4096 : 0;  // XALIGN in the kernel
-  const int64_t avail = dp.smem_optin - static_smem - a.xbytes - scratch - bias_bytes - xslack;
+  const int64_t avail =
+      dp.smem_optin - static_smem - a.xbytes - scratch - bias_bytes - ag_bytes - xslack - (a.ag_n > 0 ? 16 : 0);
   int NS = (int)(avail / ((NT / 32) * (int64_t)SB));
   if (NS > 4) NS = 4;
   if (NS < (NV == 16 ? 2 : 1)) return cudaErrorInvalidConfiguration;  // NV = 16: the caller falls back to passes of 8
   a.NS = NS;
   a.bias_off = (uint32_t)(a.xbytes + (int64_t)(NT / 32) * NS * SB + scratch);
-  const int64_t smem_all = xslack + a.xbytes + (int64_t)(NT / 32) * NS * SB + scratch + bias_bytes;
+  a.ag_off = (uint32_t)bsk::align_up(a.bias_off + bias_bytes, 16);
+  const int64_t smem_all = xslack + a.ag_off + ag_bytes;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(NT);

@@ -101,3 +101,62 @@ def test_row_range_cover():
             assert spans[0][0] == 0 and spans[-1][1] == Mx
             for a, b in zip(spans, spans[1:]):
                 assert a[1] == b[0]
+
+
+def test_cyclic_chunks_cover_and_gather_order():
+    """Block-cyclic chunks: every row owned once; all ranks' chunk j are the contiguous rows [j·P·R, (j+1)·P·R),
+    so the chunk-j all-gather lands in order (PipelinedRowShardedBS)."""
+    from paper_1811_00206_b200.dist import cyclic_chunks
+    for Mx, P, R in ((37, 2, 5), (65536, 8, 1024), (1000, 3, 64), (7, 4, 4)):
+        owner = np.full(Mx, -1)
+        chunks = [cyclic_chunks(Mx, P, r, R) for r in range(P)]
+        assert len({len(c) for c in chunks}) == 1
+        for r in range(P):
+            for j, (a, b) in enumerate(chunks[r]):
+                assert np.all(owner[a:b] == -1)
+                owner[a:b] = r
+                assert a == min((j * P + r) * R, Mx)
+        assert np.all(owner >= 0)
+
+
+def test_should_shard_policy():
+    """shard iff t1 - t1/P > t_allgather."""
+    from paper_1811_00206_b200.dist import should_shard
+    assert should_shard(231.0, 8, 10.0)          # 65536^2 at 90%: 202 us saved vs ~10 us gather
+    assert not should_shard(1.0, 8, 10.0)        # fc7 at 90%: ~1 us on one GPU
+    assert not should_shard(100.0, 1, 0.0)
+    assert should_shard(20.0, 2, 9.9) and not should_shard(20.0, 2, 10.0)
+
+
+def _pipelined_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1811_00206_b200.dist import PipelinedRowShardedBS, cyclic_chunks
+        R = 6
+        locs = [_Local(a, b) if b > a else None for a, b in cyclic_chunks(M, world, rank, R)]
+        layer = PipelinedRowShardedBS(locs, M, R, local_fn=_spmv_oracle)
+        y = layer(synth.vector(K, "f32", seed=6))
+        q.put((rank, y.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_pipelined_row_sharding_world2():
+    """The block-cyclic pipelined path gathers the same y as the unsharded product (host logic, gloo)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipelined_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    W = synth.to_numpy(synth.matrix(M, K, "f32", seed=5))
+    v, i = oracle.prune(W, oracle.F32, B, k)
+    want, _ = oracle.spmv(v, i, oracle.F32, M, K, B, k, synth.to_numpy(synth.vector(K, "f32", seed=6)))
+    for _, y in out:
+        np.testing.assert_array_equal(y, want.astype(np.float32))

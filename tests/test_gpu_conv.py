@@ -1,0 +1,90 @@
+"""GPU parity of convolution as balanced-sparse SpMM (P:286 im2col, P:107 one weight
+matrix per conv layer): bs_im2col is a pure copy (bit-exact vs orc_im2col), and conv2d = im2col + bs_spmm
+matches the oracle's direct convolution within the north-star tolerance, bit for bit on integer-exact data.
+The shapes are VGG-16 layers of Table cnn-perf at reduced spatial size, and the paper's
+balanced sparsities for them."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DT = {"f32": oracle.F32, "f16": oracle.F16, "bf16": oracle.BF16}
+
+
+@pytest.fixture(scope="module")
+def bs():
+    import paper_1811_00206_b200 as bs
+    return bs
+
+
+def _img(Nimg, H, W, C, dname, seed, family="gaussian"):
+    return synth.vector(Nimg * H * W * C, dname, family=family, seed=seed).reshape(Nimg, H, W, C)
+
+
+@pytest.mark.parametrize("Nimg,H,W,C,kh,kw,pad,stride,dname", [
+    (2, 9, 7, 64, 3, 3, 1, 1, "f16"),     # vector path
+    (1, 14, 14, 32, 3, 3, 1, 2, "bf16"),
+    (3, 5, 6, 3, 3, 3, 1, 1, "f16"),      # C = 3 (conv1_1): scalar path
+    (1, 6, 6, 4, 1, 1, 0, 1, "f32"),
+    (1, 4, 4, 8, 5, 5, 2, 1, "f32"),      # kernel wider than the image core
+])
+def test_im2col_bit_exact(bs, Nimg, H, W, C, kh, kw, pad, stride, dname):
+    inp = _img(Nimg, H, W, C, dname, synth.seed_for(50, C))
+    X = bs.im2col(inp.cuda(), kh, kw, pad, stride)
+    ref = oracle.im2col(synth.to_numpy(inp), DT[dname], kh, kw, pad, stride)
+    got = synth.to_numpy(X)
+    np.testing.assert_array_equal(got.view(np.uint8), ref.view(np.uint8))
+
+
+@pytest.mark.parametrize("layer,Cout,C,HW,s,layout,dname", [
+    ("conv4_2", 512, 512, 7, 0.91, "spmm", "f16"),   # Table cnn-perf: conv4_2 at 91% (28x28 in VGG; 7x7 here)
+    ("conv5_2", 512, 512, 6, 0.90, "spmv", "bf16"),  # the CUDA-core batched path
+    ("conv3_3", 256, 256, 8, 0.88, "spmm", "bf16"),
+    ("conv2_2", 128, 128, 9, 0.5, "sp24", "f16"),    # 2:4 sparse tensor cores (B = 4, 50%)
+])
+def test_conv2d_matches_oracle(bs, layer, Cout, C, HW, s, layout, dname):
+    kh = kw = 3
+    Kc = kh * kw * C
+    B = 4 if layout == "sp24" else 32
+    k = bs.k_from_sparsity(B, s)
+    Wm = synth.matrix(Cout, Kc, dname, seed=synth.seed_for(51, Cout + C))
+    vals, idx, _ = bs.prune(Wm.cuda(), B, k=k)
+    A = bs.pack(vals, idx, Kc, B, layout=layout)
+    inp = _img(1, HW, HW, C, dname, synth.seed_for(51, 7))
+    Y = bs.conv2d(A, inp.cuda(), kh, kw, pad=1, stride=1)
+    assert Y.shape == (1, HW, HW, Cout)
+    ov, oi = oracle.prune(synth.to_numpy(Wm), DT[dname], B, k)
+    Yr, bound = oracle.conv2d(ov, oi, DT[dname], Cout, B, k, synth.to_numpy(inp), kh, kw, 1, 1)
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(Y.reshape(-1, Cout)), DT[dname]), Yr, bound,
+                                       oracle.TAU[DT[dname]])
+    assert ok, f"{layer}: worst |err|/bound {worst}"
+
+
+@pytest.mark.parametrize("layout", ["spmm", "spmv"])
+def test_conv2d_integer_exact(bs, layout):
+    """W, input in {-1, 0, 1}: the conv output equals the oracle's direct convolution bit for bit (stride 2,
+    padding, 2 images)."""
+    Cout, C, kh, kw, B, k = 128, 64, 3, 3, 32, 4
+    Kc = kh * kw * C
+    Wm = synth.matrix(Cout, Kc, "f16", family="intexact", seed=synth.seed_for(52, 0))
+    vals, idx, _ = bs.prune(Wm.cuda(), B, k=k)
+    A = bs.pack(vals, idx, Kc, B, layout=layout)
+    inp = _img(2, 9, 8, C, "f16", synth.seed_for(52, 1), family="intexact")
+    Y = bs.conv2d(A, inp.cuda(), kh, kw, pad=1, stride=2)
+    ov, oi = oracle.prune(synth.to_numpy(Wm), oracle.F16, B, k)
+    Yr, _ = oracle.conv2d(ov, oi, oracle.F16, Cout, B, k, synth.to_numpy(inp), kh, kw, 1, 2)
+    np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(Y.reshape(-1, Cout)), oracle.F16), Yr)
+
+
+def test_conv_weight_matrix_matches_torch(bs):
+    """conv_weight_matrix + im2col + a dense product reproduce torch's conv2d (layout bookkeeping only)."""
+    w = torch.randn(6, 5, 3, 3, dtype=torch.float64)
+    x = torch.randn(1, 5, 7, 7, dtype=torch.float64)
+    ref = torch.nn.functional.conv2d(x, w, padding=1).permute(0, 2, 3, 1).reshape(-1, 6)
+    Wm = bs.conv_weight_matrix(w)
+    X = torch.from_numpy(oracle.im2col(x.permute(0, 2, 3, 1).contiguous().float().numpy(), oracle.F32, 3, 3, 1, 1)).double()
+    assert torch.allclose(X @ Wm.T, ref, atol=1e-5)
