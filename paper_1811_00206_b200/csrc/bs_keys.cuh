@@ -16,7 +16,7 @@ template <>
 struct KeyOf<BS_F32> {
   using raw_t = uint32_t;
   static constexpr int kBits = 31;
-  __device__ static uint32_t key(uint32_t u) {
+  __host__ __device__ static constexpr uint32_t key(uint32_t u) {
     uint32_t a = u & 0x7fffffffu;
     return a > 0x7f800000u ? 0x7f800001u : a;
   }
@@ -25,7 +25,7 @@ template <>
 struct KeyOf<BS_F16> {
   using raw_t = uint16_t;
   static constexpr int kBits = 15;
-  __device__ static uint32_t key(uint32_t u) {
+  __host__ __device__ static constexpr uint32_t key(uint32_t u) {
     uint32_t a = u & 0x7fffu;
     return a > 0x7c00u ? 0x7c01u : a;
   }
@@ -34,7 +34,7 @@ template <>
 struct KeyOf<BS_BF16> {
   using raw_t = uint16_t;
   static constexpr int kBits = 15;
-  __device__ static uint32_t key(uint32_t u) {
+  __host__ __device__ static constexpr uint32_t key(uint32_t u) {
     uint32_t a = u & 0x7fffu;
     return a > 0x7f80u ? 0x7f81u : a;
   }

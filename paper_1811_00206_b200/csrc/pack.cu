@@ -73,6 +73,97 @@ __global__ void pack_kernel(const VT* __restrict__ vals, const uint16_t* __restr
   }
 }
 
+// SPMV layout, one CTA per row (grid-stride): the row's canonical entries (NB·k values and indices,
+// contiguous) are copied into shared memory with coalesced loads, then the row's panel steps (one
+// contiguous run of region A) and its tail entries (regions B and C) are written in order, so both sides
+// of the permutation are coalesced and the index arithmetic is per row, not per entry (the per-entry
+// gather of pack_kernel needs six 64-bit divisions per entry). Used whenever a row fits shared memory.
+template <typename VT>
+__global__ void __launch_bounds__(512) pack_row_kernel(const VT* __restrict__ vals, const uint16_t* __restrict__ idx,
+                                                       PackArgs a, uint8_t* __restrict__ base) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  constexpr int es = sizeof(VT);
+  const int64_t nrow = a.NB * a.k;  // canonical entries per row
+  VT* sv = (VT*)sm;
+  uint16_t* si = (uint16_t*)(sm + bsk::align_up(nrow * es, 16));
+  const int64_t step_bytes = a.P * es + a.ri;
+  const bool five = a.ri != a.P * a.is;
+  const int k = a.k;
+  const int64_t kT = (int64_t)k * a.T;
+  const int64_t steps_row = a.NBf * k;
+  for (int64_t r = blockIdx.x; r < a.M; r += gridDim.x) {
+    // canonical row -> shared memory (16-byte loads when the row start allows it)
+    const uint8_t* gv = (const uint8_t*)(vals + r * nrow);
+    const uint8_t* gi = (const uint8_t*)(idx + r * nrow);
+    auto copy_in = [&](uint8_t* dst, const uint8_t* src, int64_t bytes) {
+      int64_t head = 0;
+      if (((uintptr_t)src & 15) == 0) {
+        const int64_t n16 = bytes / 16;
+        for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) ((uint4*)dst)[i] = __ldcs((const uint4*)src + i);
+        head = n16 * 16;
+      }
+      for (int64_t i = head + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+    };
+    copy_in((uint8_t*)sv, gv, nrow * es);
+    copy_in((uint8_t*)si, gi, nrow * 2);
+    __syncthreads();
+    // region A: steps s = (r·NBf + p)·k + t; P values (position l·V + v = block p·P + v·32 + l) then the
+    // index run
+    uint8_t* rowA = base + a.offA + r * steps_row * step_bytes;
+    // 32-bit index arithmetic inside a row (a row holds < 2^31 entries); P = 32·V is a power of two
+    const uint32_t P = (uint32_t)a.P, lgP = 31u - __clz(P), V = (uint32_t)a.V, lgV = 31u - __clz(V);
+    const uint32_t nvals = five ? 0u : (uint32_t)(steps_row * a.P);  // 5-bit runs: values written below
+    for (uint32_t e = threadIdx.x; e < nvals; e += blockDim.x) {
+      const uint32_t st = e >> lgP;
+      const uint32_t pos = e & (P - 1u);
+      const uint32_t p = st / (uint32_t)k, t = st - p * (uint32_t)k;
+      const uint32_t l = pos >> lgV, v = pos & (V - 1u);
+      const uint32_t b = p * P + v * 32u + l;
+      *(VT*)(rowA + (int64_t)st * step_bytes + pos * es) = sv[b * k + t];
+      if (!five) {
+        uint8_t* idst = rowA + st * step_bytes + a.P * es + pos * a.is;
+        const uint16_t o = si[b * k + t];
+        idst[0] = (uint8_t)(o & 0xff);
+        if (a.is == 2) idst[1] = (uint8_t)(o >> 8);
+      }
+    }
+    if (five) {  // 5-bit runs (B = 32, V = 8, 16-bit values): per (step, lane) the lane's 8 values (one
+                 // 16-byte store) and its 40-bit index field sum_v idx << 5v (a word and a byte)
+      for (uint32_t e = threadIdx.x; e < (uint32_t)steps_row * 32u; e += blockDim.x) {
+        const uint32_t st = e >> 5, l = e & 31u;
+        const uint32_t p = st / (uint32_t)k, t = st - p * (uint32_t)k;
+        uint64_t F = 0;
+        uint32_t vw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint32_t c = (p * P + v * 32u + l) * k + t;
+          F |= (uint64_t)(si[c] & 31u) << (5 * v);
+          vw[v >> 1] |= (uint32_t)(uint16_t)sv[c] << (16 * (v & 1));
+        }
+        *(uint4*)(rowA + (int64_t)st * step_bytes + l * 16u) = make_uint4(vw[0], vw[1], vw[2], vw[3]);
+        uint8_t* run = rowA + (int64_t)st * step_bytes + a.P * es;
+        *(uint32_t*)(run + 4 * l) = (uint32_t)F;
+        run[128 + l] = (uint8_t)(F >> 32);
+      }
+    }
+    // regions B / C: the row's tail, element t·T + q (q = v·32 + l) = block NBf·P + q, entry t
+    if (kT > 0) {
+      VT* tv = (VT*)(base + a.offB) + r * kT;
+      uint8_t* ti = base + a.offC + r * kT * a.is;
+      const uint32_t T = (uint32_t)a.T, b0 = (uint32_t)(a.NBf * a.P);
+      for (uint32_t f = threadIdx.x; f < (uint32_t)kT; f += blockDim.x) {
+        const uint32_t t = f / T, q = f - t * T;
+        const uint32_t c = (b0 + q) * k + t;
+        tv[f] = sv[c];
+        const uint16_t o = si[c];
+        ti[f * a.is] = (uint8_t)(o & 0xff);
+        if (a.is == 2) ti[f * a.is + 1] = (uint8_t)(o >> 8);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // SP24 metadata: byte (r, c) holds blocks b = 2c, 2c+1 of row r as nibbles idx0 | idx1 << 2.
 // 5-bit index runs (docs/layout.md): one thread per (step, lane) builds the 40-bit field
 // F_l = sum_v idx(l, v) << 5v of its 8 indices and writes word l of the u32 plane and byte l of the byte plane.
@@ -200,6 +291,20 @@ cudaError_t run(const bsk::Geom& g, const void* vals, const uint16_t* idx, void*
     if ((err = zero_gap(base, g.offC + nB * g.is, g.total, s))) return err;
   }
   if (nA + nB == 0) return cudaSuccess;
+  if (!unpack) {  // one CTA per row when the row's canonical entries fit shared memory
+    const int64_t smem = bsk::align_up(g.NB * g.k * g.es, 16) + g.NB * g.k * 2;
+    if (smem <= bsk::dev_props().smem_optin - 1024) {
+      cudaError_t perr = cudaSuccess;
+      const void* fn = g.es == 4 ? (const void*)pack_row_kernel<uint32_t> : (const void*)pack_row_kernel<uint16_t>;
+      if (bsk::prepare_func(fn, &perr) < 0) return perr;
+      int64_t grid = g.M < (int64_t)sms * 8 ? g.M : (int64_t)sms * 8;
+      if (g.es == 4)
+        pack_row_kernel<uint32_t><<<(unsigned)grid, 512, (size_t)smem, s>>>((const uint32_t*)vals, idx, a, base);
+      else
+        pack_row_kernel<uint16_t><<<(unsigned)grid, 512, (size_t)smem, s>>>((const uint16_t*)vals, idx, a, base);
+      return cudaGetLastError();
+    }
+  }
   int64_t blocks = (nA + nB + 255) / 256;
   if (blocks > (int64_t)sms * 32) blocks = (int64_t)sms * 32;
   if (g.es == 4) {

@@ -156,6 +156,47 @@ __global__ void __launch_bounds__(256) prune_wide(const typename KeyOf<DT>::raw_
 //     of "smallest kept key, last in offset order", removed), over a 32-bit taken mask;
 //   - otherwise the radix select of prune_narrow on the thread's B keys (kBits counting passes).
 // The kept set is the same as prune_narrow's (the top k under (key desc, offset asc)): bit-exact.
+// Sorting network (bitonic), descending, fully unrolled: B·log2(B)·(log2(B)+1)/4 compare-exchanges of
+// two IMNMX each (240 for B = 32), no data-dependent control flow.
+template <int B>
+__device__ __forceinline__ void sort_desc(uint32_t (&c)[B]) {
+#pragma unroll
+  for (int size = 2; size <= B; size <<= 1)
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1)
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const uint32_t a = c[i], b = c[j];
+          const bool desc = (i & size) == 0;
+          c[i] = desc ? max(a, b) : min(a, b);
+          c[j] = desc ? min(a, b) : max(a, b);
+        }
+      }
+}
+
+// The K largest of B unique composites, in c[0..K) (insertion into a sorted register list: 2K - 1 IMNMX
+// per element).
+template <int K, int B>
+__device__ __forceinline__ void topk_front(uint32_t (&c)[B]) {
+  uint32_t m[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) m[i] = 0u;
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    uint32_t x = c[j];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {  // m[i] = max(m[i], x); x = the value pushed down
+      const uint32_t hi = max(m[i], x);
+      x = min(m[i], x);
+      m[i] = hi;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) c[i] = m[i];
+}
+
 // Block-wide copy of `bytes` from shared to global memory: 16-byte stores where both sides are 16-byte
 // aligned (the destination of a CTA step is, when vals/idx are), then the remaining bytes one by one.
 __device__ __forceinline__ void copy_out(uint8_t* dst, const uint8_t* src, int64_t bytes) {
@@ -168,7 +209,10 @@ __device__ __forceinline__ void copy_out(uint8_t* dst, const uint8_t* src, int64
   for (int64_t i = head + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
 }
 
-template <int DT, int B>
+// KS: 1..4 = the insertion list of that length (k == KS), 0 = the sorting network (any k); chosen at
+// launch so that each instantiation holds one selection path (smaller code: instruction-fetch stalls were
+// a quarter of the samples with the choice inside the loop)
+template <int DT, int B, int KS = 0>
 __global__ void __launch_bounds__(256) prune_thread(const typename KeyOf<DT>::raw_t* __restrict__ W,
                                                     int64_t M, int64_t NB, int64_t ldw, int k,
                                                     typename KeyOf<DT>::raw_t* __restrict__ vals,
@@ -208,23 +252,41 @@ __global__ void __launch_bounds__(256) prune_thread(const typename KeyOf<DT>::ra
       key[j] = KeyOf<DT>::key(raw);
     }
     uint32_t taken = 0;
-    if (k <= 6 && ES == 2) {
-      // 16-bit keys: v_j = (key_j + 1) << 5 | (31 - j) is unique, and its maximum is the largest key,
-      // ties to the lower offset. A pass is a max tree (no serial chain); taken entries become 0.
-      uint32_t v[B];
+    if constexpr (ES == 2) {
+      // 16-bit keys: c_j = key_j << 6 | (31 - j) << 1 | sign_j is unique and orders by magnitude, ties to
+      // the lower offset (the sign bit never decides), so the kept set is the k largest composites: an
+      // insertion list for k <= 4, else a sorting network, then the first k. Each kept composite carries
+      // its offset and its value (key | sign, exact except for a NaN, whose folded key is re-read).
+      uint32_t c[B];
 #pragma unroll
-      for (int j = 0; j < B; ++j) v[j] = ((key[j] + 1u) << 5) | (31u - j);
-      for (int p = 0; p < k; ++p) {
-        uint32_t m[B];
+      for (int j = 0; j < B; ++j) {
+        const uint32_t raw = (w[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+        c[j] = (key[j] << 6) | ((31u - j) << 1) | (raw >> 15);
+      }
+      if constexpr (KS > 0) topk_front<KS, B>(c);
+      else sort_desc<B>(c);
 #pragma unroll
-        for (int j = 0; j < B; ++j) m[j] = v[j];
+      for (int p = 0; p < B; ++p)
+        if (p < k) taken |= 1u << (31u - ((c[p] >> 1) & 31u));
+      // kept entries in offset order: entry p goes to position popc(taken below its offset)
+      if (valid) {
+        const int t0 = threadIdx.x * k;
+        constexpr uint32_t kNanKey = bsk::KeyOf<DT>::key(0x7fffu);
 #pragma unroll
-        for (int h = B / 2; h > 0; h >>= 1)
-#pragma unroll
-          for (int j = 0; j < h; ++j) m[j] = max(m[j], m[j + h]);
-        taken |= 1u << (31u - (m[0] & 31u));
-#pragma unroll
-        for (int j = 0; j < B; ++j) v[j] = v[j] == m[0] ? 0u : v[j];
+        for (int p = 0; p < B; ++p) {
+          if (p < k) {
+            const uint32_t j = 31u - ((c[p] >> 1) & 31u);
+            const int pos = t0 + __popc(taken & ((1u << j) - 1u));
+            const uint32_t key_p = c[p] >> 6;
+            uint32_t raw = key_p | ((c[p] & 1u) << 15);
+            if (key_p == kNanKey) {  // a NaN: copy its own bits
+              const int64_t r = gid / NB, b = gid - r * NB;
+              raw = (uint32_t)W[r * ldw + b * B + j];
+            }
+            sv[pos] = (raw_t)raw;
+            si[pos] = (uint16_t)j;
+          }
+        }
       }
     } else if (k <= 6) {
       for (int p = 0; p < k; ++p) {
@@ -267,7 +329,7 @@ __global__ void __launch_bounds__(256) prune_thread(const typename KeyOf<DT>::ra
     }
     // kept entries in offset order into shared memory, then the CTA writes its contiguous output run
     // with 16-byte stores (per-thread stores at stride k would touch a sector per 2-byte element)
-    if (valid) {
+    if (ES != 2 && valid) {
       int t = threadIdx.x * k;
 #pragma unroll
       for (int j = 0; j < B; ++j) {
@@ -324,12 +386,33 @@ __global__ void __launch_bounds__(256) block_rank_kernel(const typename KeyOf<DT
     uint32_t packed[(B + 3) / 4];
 #pragma unroll
     for (int q = 0; q < (B + 3) / 4; ++q) packed[q] = 0;
+    if constexpr (ES == 2 && B >= 8) {
+      // 16-bit keys: sort the unique composites key << 5 | (31 - j) (a sorting network, 2·240 IMNMX for
+      // B = 32, instead of B^2 comparisons); the element at sorted position p is j = 31 - (c_p & 31),
+      // so rank_j = p, scattered through shared memory (no barrier needed: each thread reads back only its
+      // own bytes). Byte j of thread t lives in word (j / 4)·256 + t, i.e. always in bank t mod 32: the
+      // data-dependent byte stores and the word loads are conflict-free.
+      __shared__ __align__(16) uint32_t srank[(B / 4) * 256];
+      uint32_t c[B];
 #pragma unroll
-    for (int j = 0; j < B; ++j) {
-      int c = 0;
+      for (int j = 0; j < B; ++j) c[j] = (key[j] << 5) | (31u - j);
+      sort_desc<B>(c);
+      uint8_t* my = (uint8_t*)(srank + threadIdx.x);
 #pragma unroll
-      for (int i = 0; i < B; ++i) c += (key[i] > key[j]) || (i < j && key[i] == key[j]);
-      packed[j >> 2] |= (uint32_t)c << (8 * (j & 3));
+      for (int p = 0; p < B; ++p) {
+        const uint32_t j = 31u - (c[p] & 31u);
+        my[(j >> 2) * 1024u + (j & 3u)] = (uint8_t)p;
+      }
+#pragma unroll
+      for (int q = 0; q < B / 4; ++q) packed[q] = srank[q * 256 + threadIdx.x];
+    } else {
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < B; ++i) c += (key[i] > key[j]) || (i < j && key[i] == key[j]);
+        packed[j >> 2] |= (uint32_t)c << (8 * (j & 3));
+      }
     }
     bool wide = false;
     if constexpr (B % 4 == 0) wide = rvec;  // 32-bit stores when `rank` is 4-byte aligned (K, B multiples of 4)
@@ -365,6 +448,22 @@ cudaError_t launch_block_rank_t(const void* W, int64_t M, int64_t K, int64_t ldw
   return cudaGetLastError();
 }
 
+// The prune_thread instantiation for k (16-bit: an insertion list for k <= 4, the sorting network above).
+template <int DT, int B, typename R>
+void sel_k_impl(int k, R&& run) {
+  if constexpr (sizeof(typename KeyOf<DT>::raw_t) == 2) {
+    switch (k) {
+      case 1: run(prune_thread<DT, B, 1>); return;
+      case 2: run(prune_thread<DT, B, 2>); return;
+      case 3: run(prune_thread<DT, B, 3>); return;
+      case 4: run(prune_thread<DT, B, 4>); return;
+      default: run(prune_thread<DT, B, 0>); return;
+    }
+  } else {
+    run(prune_thread<DT, B, 0>);
+  }
+}
+
 template <int DT>
 cudaError_t launch_prune_t(const void* W, int64_t M, int64_t K, int64_t ldw, int B, int k, void* vals,
                            uint16_t* idx, cudaStream_t s) {
@@ -382,9 +481,9 @@ cudaError_t launch_prune_t(const void* W, int64_t M, int64_t K, int64_t ldw, int
       kern<<<(unsigned)blocks, 256, smem, s>>>((const raw_t*)W, M, NB, ldw, k, (raw_t*)vals, idx);
     };
     switch (B) {
-      case 32: run(prune_thread<DT, 32>); break;
-      case 16: run(prune_thread<DT, 16>); break;
-      case 8: run(prune_thread<DT, 8>); break;
+      case 32: sel_k_impl<DT, 32>(k, run); break;
+      case 16: sel_k_impl<DT, 16>(k, run); break;
+      case 8: sel_k_impl<DT, 8>(k, run); break;
       default: if constexpr (sizeof(raw_t) == 4) run(prune_thread<DT, 4>); break;
     }
     return cudaGetLastError();

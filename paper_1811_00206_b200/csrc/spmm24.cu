@@ -81,6 +81,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
+  // PDL: the set-up above (barriers, TMEM allocation) overlapped the previous kernel's tail; every global
+  // access below waits for it (W may have just been packed, X written, Y read)
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = tmem_holder;
 
   if (warp == 0) {
@@ -336,13 +340,15 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)S;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, tA, tX, a);
 }
 

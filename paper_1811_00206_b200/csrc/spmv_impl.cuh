@@ -698,8 +698,13 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   if (a.T > 0 && a.k > 0) {
     const int64_t gt0 = a.NBf * V, gt1 = (a.NB + 31) / 32;
     uint32_t tbase;
+    // paired x slots: the tail starts at a pair boundary plus tpar groups (tpar = 1 only for V = 1 with an
+    // odd number of groups before the tail in the staged chunk)
+    uint32_t tpar = 0;
     if (a.tail_in_last) {
-      tbase = sx + (uint32_t)(gt0 - (int64_t)(a.nchunks - 1) * a.PC * V) * GSW;
+      const uint32_t tg0 = (uint32_t)(gt0 - (int64_t)(a.nchunks - 1) * a.PC * V);
+      tpar = PAIR ? (tg0 & 1u) : 0u;
+      tbase = sx + (tg0 - tpar) * GSW;
     } else {
       __syncthreads();
       bias_issue();
@@ -736,7 +741,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const uint32_t base = tbase + lane * LSLB;
-                const uint32_t ad = PAIR ? base + o[u] * XROW + (uint32_t)(v >> 1) * 2u * GSW + (uint32_t)(v & 1) * 2u
+                const uint32_t ad = PAIR ? base + o[u] * XROW + ((uint32_t)v + tpar) / 2u * 2u * GSW + (((uint32_t)v + tpar) & 1u) * 2u
                                          : base + o[u] * ROWB + v * GSW;
                 xv[u] = lds_x<DT>(ad);
               }
@@ -754,7 +759,12 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
           if (v < Vt && bl < a.T) {
             const uint32_t w = ldv(e0 + bl);
             const uint32_t o = ldi(e0 + bl);
-            gather_fma(tbase + lane * LSLB, o, v, w);
+            if constexpr (PAIR) {
+              const uint32_t g = (uint32_t)v + tpar;
+              bsk::fma_acc<DT>(acc[v], w, lds_x<DT>(tbase + lane * LSLB + o * XROW + g / 2u * 2u * GSW + (g & 1u) * 2u));
+            } else {
+              gather_fma(tbase + lane * LSLB, o, v, w);
+            }
           }
         }
       }
