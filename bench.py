@@ -407,6 +407,8 @@ def main():
                    "parallelism": f"row-shard{world}" + ("+allgather" if world > 1 else "")},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic_from_profile(M, K, B, k, a.dtype, world),
+                     "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                       "ncu --set full capture of this launch (profiles/r2_spmv_65536_s90_ncu.md)",
                      "kernel": "spmv_kernel", "kernel_ms": round(kern_ms_max, 5),
                      "alg_bytes_per_launch": int(alg_l), "packed_bytes_per_launch": packed_l,
                      "packed_frac": round(packed_l / (kern_ms * 1e-3) / 1e9 / hbm_peak, 4), "peak_source": peak_src},
