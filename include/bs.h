@@ -218,8 +218,12 @@ int bs_spmv(const bs_matrix* A, const void* x, void* y, void* stream);
  *   writes A->packed (weights are static, the inference case). The packed W then starts streaming
  *   into shared memory before the wait; x and y still wait. The paper's batch-1 time is dominated by
  *   fixed per-layer costs ("communication inside GPU"; o_time), which this hides. */
+/* BS_SPMV_RING: always use the streaming-ring kernel. By default rows of at most 2 KB of packed bytes
+ *   (the latency-regime layers) take a direct warp-per-row kernel; the two kernels sum in the same
+ *   order, so results are bit-identical either way (this flag exists for tests and A/B timing). */
 #define BS_SPMV_PDL 1u
 #define BS_SPMV_W_STATIC 2u
+#define BS_SPMV_RING 4u
 
 /* bs_spmv_ex: bs_spmv with launch flags (above). flags = BS_SPMV_PDL is bs_spmv; flags = 0 is a
  * plain launch. Errors: as bs_spmv; BS_ERR_ARG for unknown flag bits. Results are bit-identical for

@@ -33,7 +33,7 @@ EXPORTS = ("bs_k_from_sparsity", "bs_packed_bytes", "bs_status_str", "bs_version
            "bs_block_mask", "bs_lstm_step", "bs_im2col", "bs_spmv_allgather", "bs_allgather_wait", "bs_peer_export",
            "bs_peer_import", "bs_peer_close", "bs_x_slot_offset")
 ACTS = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}  # bs_act (include/bs.h)
-SPMV_PDL, SPMV_W_STATIC = 1, 2  # bs_spmv_ex flags (include/bs.h)
+SPMV_PDL, SPMV_W_STATIC, SPMV_RING = 1, 2, 4  # bs_spmv_ex flags (include/bs.h)
 
 
 class BSError(RuntimeError):

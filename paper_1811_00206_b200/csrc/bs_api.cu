@@ -253,7 +253,7 @@ int bs_spmv_ex(const bs_matrix* A, const void* x, void* y, unsigned flags, void*
   int st = matrix_geom(A, &g);
   if (st) return st;
   if (!x || !y) return BS_ERR_ARG;
-  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC)) return BS_ERR_ARG;
+  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC | BS_SPMV_RING)) return BS_ERR_ARG;
   if (g.layout == BS_LAYOUT_SP24)  // 2:4: CUDA-core path with 2-bit metadata
     return from_cuda(bsk_launch_sp24(g, A->packed, x, 1, g.K, y, g.M, (cudaStream_t)stream, true));
   if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;  // SPMM tiles feed bs_spmm
@@ -267,7 +267,7 @@ int bs_spmv_fused(const bs_matrix* A, const void* x, const void* bias, int act, 
   int st = matrix_geom(A, &g);
   if (st) return st;
   if (!x || !y) return BS_ERR_ARG;
-  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC)) return BS_ERR_ARG;
+  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC | BS_SPMV_RING)) return BS_ERR_ARG;
   if (act < BS_ACT_NONE || act > BS_ACT_TANH) return BS_ERR_ARG;
   if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;
   return from_cuda(bsk_launch_spmv(g, A->packed, x, y, flags, (cudaStream_t)stream, bias, act));
@@ -279,7 +279,7 @@ int bs_lstm_step(const bs_matrix* A, const void* x, const void* pre, const void*
   int st = matrix_geom(A, &g);
   if (st) return st;
   if (!x || !c_prev || !h_out || !c_out) return BS_ERR_ARG;
-  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC)) return BS_ERR_ARG;
+  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC | BS_SPMV_RING)) return BS_ERR_ARG;
   if (g.M % 4 != 0) return BS_ERR_SHAPE;
   if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;
   const bsk::LstmIO io{pre, c_prev, c_out, h_out};
@@ -300,7 +300,7 @@ int bs_spmv_allgather(const bs_matrix* A, const void* x, const void* bias, int a
   int st = matrix_geom(A, &g);
   if (st) return st;
   if (!x || !valid_ag(ag)) return BS_ERR_ARG;
-  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC)) return BS_ERR_ARG;
+  if (flags & ~(BS_SPMV_PDL | BS_SPMV_W_STATIC | BS_SPMV_RING)) return BS_ERR_ARG;
   if (act < BS_ACT_NONE || act > BS_ACT_TANH) return BS_ERR_ARG;
   if (g.layout != BS_LAYOUT_SPMV) return BS_ERR_UNSUPPORTED;
   return from_cuda(bsk_launch_spmv_allgather(g, A->packed, x, *ag, flags, (cudaStream_t)stream, bias, act));

@@ -79,6 +79,7 @@ struct SpmvArgs {
   int ncols;         // valid batch columns in this pass (NV > 1)
   int w_early;       // PDL: W may be streamed before griddepcontrol.wait (BS_SPMV_W_STATIC)
   int pdl;           // host: launch with programmatic stream serialization (BS_SPMV_PDL)
+  int direct;        // host: short rows take spmv_rows_kernel (NV = 1, one x chunk; see below)
   const void* bias;  // NV = 1: optional per-row bias (M elements of D), Eq. 1's +B
   int act;           // NV = 1: bs_act applied after the bias (BS_ACT_NONE = 0)
   uint32_t bias_off; // shared-memory byte offset of the CTA's bias rows (fp32)
@@ -837,6 +838,143 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   BS_MARK(8);
 }
 
+// Short rows (the latency-regime layers: PTB, fc7, CTC): a warp per row reads the row's packed bytes
+// straight from global memory (a group of up to 4 steps issued before any is used; with W_STATIC before
+// the PDL wait) and gathers x from the L1 cache: no x staging, ring or CTA barrier, so a row costs
+// tens of instructions per lane instead of the ring kernel's per-row stage bookkeeping (74 lane
+// instructions per nonzero on PTB in round 1's ncu). Its arithmetic is exactly the ring kernel's: acc[v]
+// over the panel steps in order; with a tail, the panel total and the tail total (tail entries in t
+// order) are reduced separately and added; the same FHFMA. So both kernels give bit-identical rows, and
+// the choice (host: per-row bytes, never M) keeps row sharding bit-identical.
+template <int DT, int V, int IS>
+__global__ void __launch_bounds__(256) spmv_rows_kernel(SpmvArgs a) {
+  using raw_t = typename bsk::DTraits<DT>::raw_t;
+  constexpr int ES = bsk::DTraits<DT>::kBytes;
+  constexpr int P = 32 * V;
+  constexpr int ISt = IS == 5 ? 1 : IS;
+  constexpr uint32_t RI = IS == 5 ? 160u : (uint32_t)P * IS;
+  constexpr uint32_t STEPB = (uint32_t)P * ES + RI;
+  constexpr int G = 4;                                   // steps per load group
+  constexpr int WW = (V * ES + 3) / 4;                   // value words per lane and step
+  constexpr int IW = IS == 5 ? 2 : (V * IS + 3) / 4;     // index words per lane and step
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  pdl_launch_dependents();
+  bool waited = !a.w_early;
+  if (waited) pdl_wait();
+  const raw_t* __restrict__ x = (const raw_t*)a.x;
+  const int64_t B = a.B;
+  const int k = a.k;
+  const int64_t S = a.NBf * k;
+  const int64_t kT = (int64_t)k * a.T;
+  for (int64_t r = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); r < a.M; r += nwarps) {
+    float acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = 0.f;
+    const uint8_t* rowA = a.A + r * S * STEPB;
+    for (int64_t s0 = 0; s0 < S; s0 += G) {
+      uint32_t wv[G][WW], iv[G][IW];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (s0 + g < S) {
+          const uint8_t* st = rowA + (s0 + g) * STEPB;
+          bsk::Vec<V * ES> vv;
+          vv.load(st + lane * (V * ES));
+#pragma unroll
+          for (int q = 0; q < WW; ++q) wv[g][q] = vv.w[q];
+          if constexpr (IS == 5) {
+            bsk::Vec<4> i0;
+            bsk::Vec<1> i1;
+            i0.load(st + P * ES + 4 * lane);
+            i1.load(st + P * ES + 128 + lane);
+            iv[g][0] = i0.w[0];
+            iv[g][1] = i1.w[0];
+          } else {
+            bsk::Vec<V * IS> ii;
+            ii.load(st + P * ES + lane * (V * IS));
+#pragma unroll
+            for (int q = 0; q < IW; ++q) iv[g][q] = ii.w[q];
+          }
+        }
+      }
+      if (!waited) {  // W was static: its loads went out before the dependency wait, x waits for it
+        pdl_wait();
+        waited = true;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (s0 + g < S) {
+          const int64_t p = (s0 + g) / k;
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const uint32_t w = ES == 2 ? (wv[g][v >> 1] >> (16 * (v & 1))) & 0xffffu : wv[g][v];
+            uint32_t o;
+            if constexpr (IS == 5) o = (v < 7 ? __funnelshift_r(iv[g][0], iv[g][1], 5 * v) : iv[g][1] >> 3) & 31u;
+            else if constexpr (IS == 1) o = byte_of(iv[g][v >> 2], v & 3);
+            else o = (iv[g][v >> 1] >> (16 * (v & 1))) & 0xffffu;
+            const int64_t b = p * P + v * 32 + lane;
+            bsk::fma_acc<DT>(acc[v], w, (uint32_t)__ldg(x + b * B + o));
+          }
+        }
+      }
+    }
+    if (!waited) {
+      pdl_wait();
+      waited = true;
+    }
+    float y;
+    if (a.T > 0 && k > 0) {
+      const float panel = S > 0 ? warp_total<V>(acc) : 0.f;  // (zeroes acc)
+      const int Vt = (int)((a.T + 31) / 32);
+      const raw_t* tv = (const raw_t*)a.Bt + r * kT;
+      const uint8_t* ti = a.Ct + r * kT * ISt;
+      for (int tt = 0; tt < k; ++tt) {
+        const int64_t e0 = (int64_t)tt * a.T;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int bl = v * 32 + lane;
+          if (v < Vt && bl < a.T) {
+            const uint32_t w = (uint32_t)__ldg(tv + e0 + bl);
+            const uint32_t o = ISt == 1 ? (uint32_t)__ldg(ti + e0 + bl) : (uint32_t)__ldg((const uint16_t*)ti + e0 + bl);
+            const int64_t b = a.NBf * P + bl;
+            bsk::fma_acc<DT>(acc[v], w, (uint32_t)__ldg(x + b * B + o));
+          }
+        }
+      }
+      const float tail = warp_total<V>(acc);
+      y = S > 0 ? panel + tail : tail;
+    } else {
+      y = warp_total<V>(acc);  // k == 0: 0
+    }
+    if (lane == 0) {
+      if (a.bias) y += bsk::to_float<DT>(__ldg((const raw_t*)a.bias + r));
+      if (a.act) y = apply_act(y, a.act);
+      ((raw_t*)a.y)[r] = (raw_t)bsk::from_float<DT>(y);
+    }
+  }
+  if (!waited) pdl_wait();
+}
+
+template <int DT, int V, int IS>
+cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
+  SpmvArgs a = a0;
+  if (!a.pdl) a.w_early = 0;
+  const auto& dp = bsk::dev_props();
+  int64_t warps = a.M < (int64_t)dp.sms * 64 ? a.M : (int64_t)dp.sms * 64;
+  const int64_t grid = (warps + 7) / 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS>, a);
+}
+
 template <int V, int ES>
 struct StageSteps {
   // Q, steps per ring stage: at most 4. The stage loop is unrolled (twice: full and partial stages), so
@@ -928,6 +1066,18 @@ cudaError_t launch_t(const SpmvArgs& a, cudaStream_t s) {
 
 template <int DT, int IS, int NV>
 cudaError_t dispatch_v(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
+  if constexpr (NV == 1) {
+    if (a.direct) {
+      switch (g.V) {
+        case 1: return launch_rows<DT, 1, IS>(a, s);
+        case 2: return launch_rows<DT, 2, IS>(a, s);
+        case 4: return launch_rows<DT, 4, IS>(a, s);
+        default:
+          if constexpr (DT != BS_F32) return launch_rows<DT, 8, IS>(a, s);
+          return cudaErrorInvalidValue;
+      }
+    }
+  }
   switch (g.V) {
     case 1: return launch_t<DT, 1, IS, NV>(a, s);
     case 2: return launch_t<DT, 2, IS, NV>(a, s);
@@ -941,7 +1091,11 @@ cudaError_t dispatch_v(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
 template <int DT, int NV>
 cudaError_t dispatch_is(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
   if constexpr (DT != BS_F32)
-    if (g.ri != g.P * g.is) return launch_t<DT, 8, 5, NV>(a, s);  // 5-bit index runs
+    if (g.ri != g.P * g.is) {  // 5-bit index runs
+      if constexpr (NV == 1)
+        if (a.direct) return launch_rows<DT, 8, 5>(a, s);
+      return launch_t<DT, 8, 5, NV>(a, s);
+    }
   return g.is == 1 ? dispatch_v<DT, 1, NV>(g, a, s) : dispatch_v<DT, 2, NV>(g, a, s);
 }
 

@@ -178,7 +178,7 @@ def test_spmv_launch_modes_and_dependencies(bs):
         A = bs.pack(v, i, K, B)
         assert torch.equal(bs.spmv(A, x0), ref)
     with pytest.raises(bs.BSError):
-        bs.spmv(mats[0], x0, flags=4)
+        bs.spmv(mats[0], x0, flags=8)
 
 
 @pytest.mark.parametrize("act", ["none", "relu", "sigmoid", "tanh"])

@@ -234,3 +234,44 @@ def test_block_rank_errors_and_alignment(bs):
                                 ctypes.c_void_p(buf.data_ptr() + 1), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert st == 0
     assert torch.equal(buf[1:].view(M, K).cpu(), ref)
+
+
+# ---------------------------------------------------------------- direct (short-row) SpMV kernel vs the ring kernel
+
+@pytest.mark.parametrize("M,K,B,k,dname", [
+    (6000, 3008, 32, 3, "f16"),    # PTB (panel + tail): direct by default
+    (4096, 4096, 32, 3, "bf16"),   # fc7 90 %
+    (4096, 2048, 32, 4, "f16"),    # CTC W_ih
+    (4096, 1024, 32, 4, "bf16"),   # CTC W_hh (V = 1)
+    (777, 25088, 32, 1, "f16"),    # fc6 at 97 %: 5-bit runs, V = 8
+    (300, 640, 20, 6, "f32"),      # tail only, odd B, f32
+    (129, 96, 4, 2, "f16"),
+    (64, 640, 32, 0, "f16"),       # k = 0
+])
+def test_direct_kernel_matches_ring(bs, M, K, B, k, dname):
+    """Short rows take the direct warp-per-row kernel unless BS_SPMV_RING; both sum in the same order, so
+    y is bit-identical (and therefore row sharding stays bit-identical whichever kernel a shard takes),
+    with and without the fused bias + activation, and matches the oracle."""
+    W = synth.matrix(M, K, dname, seed=synth.seed_for(28, M + K))
+    vals, idx, k2 = bs.prune(W.cuda(), B, k=k)
+    A = bs.pack(vals, idx, K, B)
+    x = synth.vector(K, dname, seed=synth.seed_for(28, 1)).cuda()
+    bias = synth.vector(M, dname, seed=synth.seed_for(28, 2)).cuda()
+    for fl in (bs.SPMV_PDL, bs.SPMV_PDL | bs.SPMV_W_STATIC, 0):
+        y_d = bs.spmv(A, x, flags=fl)
+        y_r = bs.spmv(A, x, flags=fl | bs.SPMV_RING)
+        assert torch.equal(y_d, y_r), fl
+    assert torch.equal(bs.spmv(A, x, bias=bias, act="tanh"), bs.spmv(A, x, bias=bias, act="tanh", flags=bs.SPMV_PDL | bs.SPMV_RING))
+    ov, oi = oracle.prune(synth.to_numpy(W), DT[dname], B, k)
+    yr, bound = oracle.spmv(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(x.cpu()))
+    ok, worst = oracle.check_tolerance(oracle.to_double(synth.to_numpy(y_d), DT[dname]), yr, bound, oracle.TAU[DT[dname]])
+    assert ok, worst
+
+
+def test_direct_kernel_integer_exact(bs):
+    M, K, B, k = 1000, 3008, 32, 5
+    A, ov, oi = _setup(bs, M, K, B, k, "bf16", synth.seed_for(29, 0), "spmv")
+    x = synth.vector(K, "bf16", family="intexact", seed=synth.seed_for(29, 1))
+    y = bs.spmv(A, x.cuda())
+    yr, _ = oracle.spmv(ov, oi, oracle.BF16, M, K, B, k, synth.to_numpy(x))
+    np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(y), oracle.BF16), yr)
