@@ -55,6 +55,20 @@ int prepare_func(const void* func, cudaError_t* err) {
   return (int)fa.sharedSizeBytes;
 }
 
+int resident_ctas(const void* func, int threads) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({func, dev});
+  if (it != done.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, func, threads, 0) != cudaSuccess) n = 0;
+  done[{func, dev}] = n;
+  return n;
+}
+
 }  // namespace bsk
 
 namespace {

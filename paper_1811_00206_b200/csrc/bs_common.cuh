@@ -104,6 +104,10 @@ const DevProps& dev_props();
 // Returns a negative value (and leaves *err set) on failure.
 int prepare_func(const void* func, cudaError_t* err);
 
+// Resident CTAs per SM of `func` at `threads` threads and no dynamic shared memory (occupancy query,
+// cached per function and device). 0 on error.
+int resident_ctas(const void* func, int threads);
+
 // Split-K of the tensor-core SpMM kernels: at least this many K chunks per CTA (measured defaults:
 // K6 3, K5 6; BS_SPLITK_MIN_CHUNKS overrides both for tuning). It depends on nothing but the
 // environment, so the split (and the summation order) stays a function of M and K only.

@@ -846,8 +846,8 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
 // over the panel steps in order; with a tail, the panel total and the tail total (tail entries in t
 // order) are reduced separately and added; the same FHFMA. So both kernels give bit-identical rows, and
 // the choice (host: per-row bytes, never M) keeps row sharding bit-identical.
-template <int DT, int V, int IS>
-__global__ void __launch_bounds__(256) spmv_rows_kernel(SpmvArgs a) {
+template <int DT, int V, int IS, bool TP>
+__global__ void __launch_bounds__(256, (V <= 4 ? 4 : 1)) spmv_rows_kernel(SpmvArgs a) {
   using raw_t = typename bsk::DTraits<DT>::raw_t;
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int P = 32 * V;
@@ -867,11 +867,38 @@ __global__ void __launch_bounds__(256) spmv_rows_kernel(SpmvArgs a) {
   const int k = a.k;
   const int64_t S = a.NBf * k;
   const int64_t kT = (int64_t)k * a.T;
+  const int Vt = (int)((a.T + 31) / 32);
+  // TP (chosen at launch: a tail with k·V <= 8): the row's tail entries are held in registers, issued with
+  // the panel loads (one memory round trip per row); a separate instantiation keeps the registers of the
+  // layers without a tail. 16-bit values: value | index << 16 in one register per entry.
+  constexpr int TM = TP ? 8 : 1;
+  constexpr int TO = ES == 2 ? 1 : TM;
   for (int64_t r = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); r < a.M; r += nwarps) {
     float acc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[v] = 0.f;
     const uint8_t* rowA = a.A + r * S * STEPB;
+    uint32_t tw[TM], to[TO];
+    if constexpr (TP) {
+      const raw_t* tv = (const raw_t*)a.Bt + r * kT;
+      const uint8_t* ti = a.Ct + r * kT * ISt;
+#pragma unroll
+      for (int q = 0; q < TM; ++q) {
+        const int tt = q / V, v = q - (q / V) * V;  // entry q = (tt, v)
+        const int bl = v * 32 + lane;
+        tw[q] = 0u;
+        if constexpr (ES != 2) to[q] = 0u;
+        if (tt < k && v < Vt && bl < a.T) {
+          const int64_t e = (int64_t)tt * a.T + bl;
+          const uint32_t o = ISt == 1 ? (uint32_t)__ldg(ti + e) : (uint32_t)__ldg((const uint16_t*)ti + e);
+          if constexpr (ES == 2) tw[q] = (uint32_t)__ldg(tv + e) | (o << 16);
+          else {
+            tw[q] = (uint32_t)__ldg(tv + e);
+            to[q] = o;
+          }
+        }
+      }
+    }
     for (int64_t s0 = 0; s0 < S; s0 += G) {
       uint32_t wv[G][WW], iv[G][IW];
 #pragma unroll
@@ -925,10 +952,22 @@ __global__ void __launch_bounds__(256) spmv_rows_kernel(SpmvArgs a) {
     float y;
     if (a.T > 0 && k > 0) {
       const float panel = S > 0 ? warp_total<V>(acc) : 0.f;  // (zeroes acc)
-      const int Vt = (int)((a.T + 31) / 32);
       const raw_t* tv = (const raw_t*)a.Bt + r * kT;
       const uint8_t* ti = a.Ct + r * kT * ISt;
-      for (int tt = 0; tt < k; ++tt) {
+      if constexpr (TP) {  // the same (tt, v) order as the loop below
+#pragma unroll
+        for (int q = 0; q < TM; ++q) {
+          const int tt = q / V, v = q - (q / V) * V;
+          const int bl = v * 32 + lane;
+          if (tt < k && v < Vt && bl < a.T) {
+            const int64_t b = a.NBf * P + bl;
+            const uint32_t w = ES == 2 ? (tw[q] & 0xffffu) : tw[q];
+            const uint32_t o = ES == 2 ? (tw[q] >> 16) : to[q < TO ? q : 0];
+            bsk::fma_acc<DT>(acc[v], w, (uint32_t)__ldg(x + b * B + o));
+          }
+        }
+      }
+      for (int tt = TP ? k : 0; tt < k; ++tt) {
         const int64_t e0 = (int64_t)tt * a.T;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -972,7 +1011,19 @@ cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = a.pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS>, a);
+  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, true>, a);
+  return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, false>, a);
+}
+
+// The direct kernel pays off while every row gets its own resident warp (one wave): a second wave adds
+// a whole row latency (PTB, 6000 rows: 7.0 us direct vs 6.8 us ring; fc7 and CTC, 4096 rows: 1.15-1.35x
+// faster direct). Both kernels give bit-identical rows, so the choice may depend on M.
+template <int DT, int V, int IS>
+bool rows_fit(const SpmvArgs& a) {
+  const bool tp = a.T > 0 && a.k > 0 && a.k * V <= 8;
+  const void* fn = tp ? (const void*)spmv_rows_kernel<DT, V, IS, true> : (const void*)spmv_rows_kernel<DT, V, IS, false>;
+  const int per_sm = bsk::resident_ctas(fn, 256);
+  return per_sm > 0 && a.M <= (int64_t)per_sm * bsk::dev_props().sms * 8;
 }
 
 template <int V, int ES>
@@ -1069,12 +1120,12 @@ cudaError_t dispatch_v(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
   if constexpr (NV == 1) {
     if (a.direct) {
       switch (g.V) {
-        case 1: return launch_rows<DT, 1, IS>(a, s);
-        case 2: return launch_rows<DT, 2, IS>(a, s);
-        case 4: return launch_rows<DT, 4, IS>(a, s);
+        case 1: if (rows_fit<DT, 1, IS>(a)) return launch_rows<DT, 1, IS>(a, s); break;
+        case 2: if (rows_fit<DT, 2, IS>(a)) return launch_rows<DT, 2, IS>(a, s); break;
+        case 4: if (rows_fit<DT, 4, IS>(a)) return launch_rows<DT, 4, IS>(a, s); break;
         default:
-          if constexpr (DT != BS_F32) return launch_rows<DT, 8, IS>(a, s);
-          return cudaErrorInvalidValue;
+          if constexpr (DT != BS_F32)
+            if (rows_fit<DT, 8, IS>(a)) return launch_rows<DT, 8, IS>(a, s);
       }
     }
   }
@@ -1093,7 +1144,7 @@ cudaError_t dispatch_is(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
   if constexpr (DT != BS_F32)
     if (g.ri != g.P * g.is) {  // 5-bit index runs
       if constexpr (NV == 1)
-        if (a.direct) return launch_rows<DT, 8, 5>(a, s);
+        if (a.direct && rows_fit<DT, 8, 5>(a)) return launch_rows<DT, 8, 5>(a, s);
       return launch_t<DT, 8, 5, NV>(a, s);
     }
   return g.is == 1 ? dispatch_v<DT, 1, NV>(g, a, s) : dispatch_v<DT, 2, NV>(g, a, s);

@@ -81,6 +81,9 @@ def test_lstm_step_launch_modes_and_errors(bs):
     h1, c1 = bs.lstm_step(A, x, c0, flags=0)
     h2, c2 = bs.lstm_step(A, x, c0, flags=bs.SPMV_PDL | bs.SPMV_W_STATIC)
     assert torch.equal(h1, h2) and torch.equal(c1, c2)
+    # the direct warp-per-unit kernel and the streaming-ring kernel (cell in a CTA epilogue) agree bit for bit
+    h3, c3 = bs.lstm_step(A, x, c0, flags=bs.SPMV_PDL | bs.SPMV_RING)
+    assert torch.equal(h1, h3) and torch.equal(c1, c3)
     W3 = synth.matrix(6, K, "f16", seed=44).cuda()
     v3, i3, _ = bs.prune(W3, B, k=k)
     with pytest.raises(ValueError):

@@ -239,7 +239,9 @@ def test_block_rank_errors_and_alignment(bs):
 # ---------------------------------------------------------------- direct (short-row) SpMV kernel vs the ring kernel
 
 @pytest.mark.parametrize("M,K,B,k,dname", [
-    (6000, 3008, 32, 3, "f16"),    # PTB (panel + tail): direct by default
+    (6000, 3008, 32, 3, "f16"),    # PTB (panel + tail): more rows than one wave of the direct kernel: ring
+    (1000, 3008, 32, 3, "bf16"),   # PTB width in one wave: direct with the tail held in registers
+    (2000, 3008, 32, 6, "f16"),    # k·V > 8: direct, tail through the loop
     (4096, 4096, 32, 3, "bf16"),   # fc7 90 %
     (4096, 2048, 32, 4, "f16"),    # CTC W_ih
     (4096, 1024, 32, 4, "bf16"),   # CTC W_hh (V = 1)
