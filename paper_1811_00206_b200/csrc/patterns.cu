@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(256) decode_kernel(const raw_t* __restrict__ v
   for (int64_t job = blockIdx.x; job < M * nseg; job += gridDim.x) {
     const int64_t r = job / nseg, e0 = (job - r * nseg) * kSeg;
     const int64_t E = (K - e0) < kSeg ? (K - e0) : kSeg;
-    for (int64_t i = threadIdx.x; i < E; i += blockDim.x) seg[i] = 0;
+    for (int64_t i = threadIdx.x; i < kSeg * (int64_t)sizeof(raw_t) / 16; i += blockDim.x)
+      ((uint4*)seg)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     const int64_t b0 = e0 / B, b1 = (e0 + E - 1) / B;  // blocks overlapping the segment
     const int64_t t0 = (r * NB + b0) * k, t1 = (r * NB + b1 + 1) * k;

@@ -220,9 +220,11 @@ __global__ void __launch_bounds__(256) prune_thread(const typename KeyOf<DT>::ra
   using raw_t = typename KeyOf<DT>::raw_t;
   constexpr int ES = sizeof(raw_t);
   constexpr int NV = B * ES / 16;  // 16-byte loads per block
-  extern __shared__ __align__(16) uint8_t sm_out[];  // staged outputs: 256·k values, then 256·k indices
+  // staged outputs: 256·k values, then 256·k indices; 16-bit: then the threads' raw blocks (padded rows)
+  extern __shared__ __align__(16) uint8_t sm_out[];
   raw_t* sv = (raw_t*)sm_out;
   uint16_t* si = (uint16_t*)(sm_out + bsk::align_up(256LL * k * ES, 16));
+  const uint32_t raw_off = (uint32_t)(bsk::align_up(256LL * k * ES, 16) + bsk::align_up(256LL * k * 2, 16));
   const int64_t nblocks = M * NB;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // the next block's loads are issued before the current block's selection (register double buffer)
@@ -245,45 +247,45 @@ __global__ void __launch_bounds__(256) prune_thread(const typename KeyOf<DT>::ra
 #pragma unroll
     for (int q = 0; q < B * ES / 4; ++q) w[q] = wn[q];
     if (gid + stride < nblocks) load(gid + stride, wn);
-    uint32_t key[B];
+    uint32_t key[ES == 2 ? 1 : B];
+    if constexpr (ES != 2) {
 #pragma unroll
-    for (int j = 0; j < B; ++j) {
-      const uint32_t raw = ES == 2 ? (w[j >> 1] >> (16 * (j & 1))) & 0xffffu : w[j];
-      key[j] = KeyOf<DT>::key(raw);
+      for (int j = 0; j < B; ++j) key[j] = KeyOf<DT>::key(w[j]);
     }
     uint32_t taken = 0;
     if constexpr (ES == 2) {
-      // 16-bit keys: c_j = key_j << 6 | (31 - j) << 1 | sign_j is unique and orders by magnitude, ties to
-      // the lower offset (the sign bit never decides), so the kept set is the k largest composites: an
-      // insertion list for k <= 4, else a sorting network, then the first k. Each kept composite carries
-      // its offset and its value (key | sign, exact except for a NaN, whose folded key is re-read).
+      // 16-bit keys, two per 32-bit word: |w| is one LOP3 and the NaN fold (every NaN onto the key just
+      // above Inf) one VIMNMX.U16x2 for both halves; c_j = key_j << 17 | (31 - j) << 12 is unique and
+      // orders by magnitude, ties to the lower offset, so the kept set is the k largest composites: an
+      // insertion list for k <= 4, else a sorting network, then the first k. The kept values are copied
+      // bit for bit from this thread's raw words parked in shared memory (padded rows: conflict-free).
+      constexpr uint32_t kNan2 = bsk::KeyOf<DT>::key(0x7fffu) * 0x10001u;  // the folded NaN key, both halves
       uint32_t c[B];
 #pragma unroll
-      for (int j = 0; j < B; ++j) {
-        const uint32_t raw = (w[j >> 1] >> (16 * (j & 1))) & 0xffffu;
-        c[j] = (key[j] << 6) | ((31u - j) << 1) | (raw >> 15);
+      for (int q = 0; q < B / 2; ++q) {
+        const uint32_t a2 = __vminu2(w[q] & 0x7fff7fffu, kNan2);
+        c[2 * q] = (a2 << 17) | ((31u - 2 * q) << 12);
+        c[2 * q + 1] = ((a2 << 1) & 0xfffe0000u) | ((31u - (2 * q + 1)) << 12);
       }
+      uint32_t* rawrow = (uint32_t*)(sm_out + raw_off) + threadIdx.x * (B / 2 + 4);
+#pragma unroll
+      for (int q = 0; q < B / 8; ++q)
+        *(uint4*)(rawrow + 4 * q) = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
       if constexpr (KS > 0) topk_front<KS, B>(c);
       else sort_desc<B>(c);
 #pragma unroll
       for (int p = 0; p < B; ++p)
-        if (p < k) taken |= 1u << (31u - ((c[p] >> 1) & 31u));
+        if (p < k) taken |= 1u << (31u - ((c[p] >> 12) & 31u));
       // kept entries in offset order: entry p goes to position popc(taken below its offset)
       if (valid) {
         const int t0 = threadIdx.x * k;
-        constexpr uint32_t kNanKey = bsk::KeyOf<DT>::key(0x7fffu);
+        const uint16_t* raw16 = (const uint16_t*)rawrow;
 #pragma unroll
         for (int p = 0; p < B; ++p) {
           if (p < k) {
-            const uint32_t j = 31u - ((c[p] >> 1) & 31u);
+            const uint32_t j = 31u - ((c[p] >> 12) & 31u);
             const int pos = t0 + __popc(taken & ((1u << j) - 1u));
-            const uint32_t key_p = c[p] >> 6;
-            uint32_t raw = key_p | ((c[p] & 1u) << 15);
-            if (key_p == kNanKey) {  // a NaN: copy its own bits
-              const int64_t r = gid / NB, b = gid - r * NB;
-              raw = (uint32_t)W[r * ldw + b * B + j];
-            }
-            sv[pos] = (raw_t)raw;
+            sv[pos] = (raw_t)raw16[j];
             si[pos] = (uint16_t)j;
           }
         }
@@ -363,8 +365,21 @@ __global__ void __launch_bounds__(256) block_rank_kernel(const typename KeyOf<DT
     using raw_t = typename KeyOf<DT>::raw_t;
     constexpr int ES = sizeof(raw_t);
     const raw_t* src = W + r * ldw + b * B;
-    uint32_t key[B];
-    if constexpr (B * ES % 16 == 0) {
+    constexpr bool PACK16 = ES == 2 && B >= 8;  // 16-bit, B >= 8: keys from raw words, two per word
+    uint32_t key[PACK16 ? 1 : B];
+    uint32_t wraw[PACK16 ? B / 2 : 1];
+    if constexpr (PACK16) {
+      if (B * ES % 16 == 0 && vec) {  // 16-byte loads (rows 16-byte aligned)
+#pragma unroll
+        for (int q = 0; q < B * ES / 16; ++q) {
+          const uint4 v = __ldcs((const uint4*)src + q);
+          wraw[4 * q] = v.x; wraw[4 * q + 1] = v.y; wraw[4 * q + 2] = v.z; wraw[4 * q + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < B / 2; ++q) wraw[q] = (uint32_t)__ldg(src + 2 * q) | ((uint32_t)__ldg(src + 2 * q + 1) << 16);
+      }
+    } else if constexpr (B * ES % 16 == 0) {
       if (vec) {  // 16-byte loads (rows 16-byte aligned)
         uint32_t w[B * ES / 4];
 #pragma unroll
@@ -394,13 +409,20 @@ __global__ void __launch_bounds__(256) block_rank_kernel(const typename KeyOf<DT
       // data-dependent byte stores and the word loads are conflict-free.
       __shared__ __align__(16) uint32_t srank[(B / 4) * 256];
       uint32_t c[B];
+      {  // two keys per word: |w| one LOP3, the NaN fold one VIMNMX.U16x2 (as bs_prune_k)
+        constexpr uint32_t kNan2 = KeyOf<DT>::key(0x7fffu) * 0x10001u;
 #pragma unroll
-      for (int j = 0; j < B; ++j) c[j] = (key[j] << 5) | (31u - j);
+        for (int q = 0; q < B / 2; ++q) {
+          const uint32_t a2 = __vminu2(wraw[q] & 0x7fff7fffu, kNan2);
+          c[2 * q] = (a2 << 17) | ((31u - 2 * q) << 12);
+          c[2 * q + 1] = ((a2 << 1) & 0xfffe0000u) | ((31u - (2 * q + 1)) << 12);
+        }
+      }
       sort_desc<B>(c);
       uint8_t* my = (uint8_t*)(srank + threadIdx.x);
 #pragma unroll
       for (int p = 0; p < B; ++p) {
-        const uint32_t j = 31u - (c[p] & 31u);
+        const uint32_t j = 31u - ((c[p] >> 12) & 31u);
         my[(j >> 2) * 1024u + (j & 3u)] = (uint8_t)p;
       }
 #pragma unroll
@@ -475,7 +497,8 @@ cudaError_t launch_prune_t(const void* W, int64_t M, int64_t K, int64_t ldw, int
   if (aligned16 && k > 0 && (B == 32 || B == 16 || B == 8 || (B == 4 && sizeof(raw_t) == 4))) {
     int64_t blocks = (M * NB + 255) / 256;
     blocks = blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8;
-    const size_t smem = (size_t)bsk::align_up(256LL * k * sizeof(raw_t), 16) + 256 * (size_t)k * 2;
+    const size_t smem = (size_t)bsk::align_up(256LL * k * sizeof(raw_t), 16) + (size_t)bsk::align_up(256LL * k * 2, 16) +
+                        (sizeof(raw_t) == 2 ? 256 * (size_t)(B * 2 + 16) : 0);
     auto run = [&](auto kern) {
       if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kern<<<(unsigned)blocks, 256, smem, s>>>((const raw_t*)W, M, NB, ldw, k, (raw_t*)vals, idx);

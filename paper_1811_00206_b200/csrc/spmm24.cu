@@ -294,7 +294,12 @@ template <int DT>
 cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
                         int64_t ldy, cudaStream_t s) {
   int BN = (int)((N + 15) / 16 * 16);
-  if (BN > 128) BN = 128;  // keeps a 4-stage ring (BN = 256 would leave 2 stages, measured slower)
+  static const int bn_max = [] {  // BS_K5_BN_MAX: tuning knob (128 or 256); BN only partitions columns
+    const char* e = getenv("BS_K5_BN_MAX");
+    const int v = e && e[0] ? atoi(e) : 128;
+    return v >= 256 ? 256 : 128;
+  }();
+  if (BN > bn_max) BN = bn_max;  // 128 keeps a 4-stage ring; 256 leaves 2 stages
   CUtensorMap tA, tX;
   const uint8_t* base = (const uint8_t*)packed;
   if (!bsk_make_map_2d(&tA, DT, base + g.offA, g.K / 2, g.M, g.K / 2, 64, BM)) return cudaErrorNotSupported;
