@@ -792,6 +792,59 @@ def f32_rows(a, bs, hbm_peak, l2):
     return {"f32": rows}
 
 
+def vgg_head_rows(a, bs, l2):
+    """NEXT-2 (o_time): VGG-16's classifier head fc6 -> fc7 -> fc8 with bias + ReLU at Table
+    cnn-perf's balanced sparsities (93 %, 93 %, 75 % -> k = 2, 2, 8 of 32), batch 1: eager launches vs one
+    CUDA graph (bs.LayerStack) vs cuBLAS addmv + ReLU on the dense W_bs (also one graph)."""
+    dev = torch.device("cuda")
+    dims = [(4096, 25088, 0.93, "relu"), (4096, 4096, 0.93, "relu"), (1000, 4096, 0.75, None)]
+    layers, dense = [], []
+    for j, (M, K, s, act) in enumerate(dims):
+        W = synth.matrix(M, K, a.dtype, seed=synth.seed_for(9, j), device=dev)
+        ks = bs.k_from_sparsity(a.block, s)
+        v, i, _ = bs.prune(W, a.block, k=ks)
+        b = synth.vector(M, a.dtype, seed=synth.seed_for(9, 10 + j), device=dev)
+        layers.append((bs.pack(v, i, K, a.block), b, act))
+        dense.append((dense_from_canonical(v, i, M, K, a.block), b, act))
+        del W
+    x = synth.vector(25088, a.dtype, seed=synth.seed_for(9, 99), device=dev)
+    stack = bs.LayerStack(layers)
+    # eager: the same launches without a graph, device-timed per call
+    for _ in range(3):
+        stack(x)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(50):
+        stack(x)
+    e1.record()
+    torch.cuda.synchronize()
+    t_eager = e0.elapsed_time(e1) * 1e3 / 50
+    stack.capture()
+    for _ in range(3):
+        stack.graph.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(50):
+        stack.graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    t_graph = e0.elapsed_time(e1) * 1e3 / 50
+
+    def dense_chain(j):
+        cur = x
+        for Wd, b, act in dense:
+            cur = torch.addmv(b, Wd, cur)
+            if act == "relu":
+                cur = torch.relu(cur)
+        return cur
+    t_dense = graph_time_us(dense_chain, 20)
+    return {"vgg_head": {"layers": "fc6 4096x25088 k=2, fc7 4096x4096 k=2, fc8 1000x4096 k=8 (+bias, ReLU, ReLU)",
+                         "eager_us": round(t_eager, 2), "graph_us": round(t_graph, 2),
+                         "cublas_graph_us": round(t_dense, 2), "speedup_vs_cublas": round(t_dense / t_graph, 2),
+                         "paper_context_us": "Table cnn-perf balanced: fc6 231.1 + fc7 70.3 + fc8 58.9 (another GPU)"}}
+
+
 def producer_rows(a, bs, W):
     """The offline producers on the bench layer (65536^2 f16 by default): bs_prune_k (K1) at k = 3 and 16, bs_pack (K2),
     bs_block_rank, bs_prune_dense (Alg. 1 iteration, prune + decode) and the comparison masks (random,
@@ -881,7 +934,7 @@ def extras(a, bs, W, A, vals, idx, x, k, es, hbm_peak, stream):
         res.update(f32_rows(a, bs, hbm_peak, l2))
     except Exception as e:
         res["f32_rows_error"] = f"{type(e).__name__}: {str(e)[:200]}"
-    for fn in (conv_rows, lstm_rows):
+    for fn in (conv_rows, lstm_rows, vgg_head_rows):
         try:
             res.update(fn(a, bs, l2))
         except Exception as e:  # a failing extra is reported, never hidden

@@ -605,3 +605,55 @@ def allgather_wait(ag: _AllGather, device):
     with torch.cuda.device(device):
         st = lib().bs_allgather_wait(ctypes.byref(ag), _stream(device))
     _check(st, "bs_allgather_wait")
+
+
+# ---------------------------------------------------------------- a stack of layers as one CUDA graph (o_time)
+
+class LayerStack:
+    """A stack of balanced-sparse FC layers y_{i+1} = act_i(W_i·y_i + b_i) (Eq. 1 with its +B) run as
+    one CUDA graph: the per-layer launch cost the paper calls o_time becomes a graph node, and
+    every layer launches with PDL + static weights, so its weight stream starts while the previous layer
+    finishes. ``layers`` is a list of (BSMatrix, bias or None, act or None); each K must equal the previous M.
+    Call with x (device, K of the first layer); returns the last y (a view of a buffer the next call
+    overwrites)."""
+
+    def __init__(self, layers):
+        if not layers:
+            raise ValueError("at least one layer")
+        for (a0, _, _), (a1, _, _) in zip(layers, layers[1:]):
+            if a1.K != a0.M or a1.dtype != a0.dtype:
+                raise ValueError("layer K must equal the previous layer's M (same dtype)")
+        self.layers = layers
+        dev = layers[0][0].packed.device
+        dt = layers[0][0].dtype
+        self.x = torch.zeros(layers[0][0].K, dtype=dt, device=dev)
+        self.ys = [torch.empty(A.M, dtype=dt, device=dev) for A, _, _ in layers]
+        self.graph = None
+
+    def _run(self):
+        cur = self.x
+        fl = SPMV_PDL | SPMV_W_STATIC
+        for (A, b, act), y in zip(self.layers, self.ys):
+            spmv(A, cur, out=y, flags=fl, bias=b, act=act)
+            cur = y
+        return cur
+
+    def capture(self):
+        """Record the stack once (after a warm-up on a side stream, as torch requires)."""
+        s = torch.cuda.Stream(device=self.x.device)
+        s.wait_stream(torch.cuda.current_stream(self.x.device))
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                self._run()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=s):
+                self._run()
+        torch.cuda.current_stream(self.x.device).wait_stream(s)
+        return self
+
+    def __call__(self, x: torch.Tensor) -> torch.Tensor:
+        self.x.copy_(x)
+        if self.graph is None:
+            return self._run()
+        self.graph.replay()
+        return self.ys[-1]

@@ -878,6 +878,19 @@ __global__ void __launch_bounds__(256, (V <= 4 ? 4 : 1)) spmv_rows_kernel(SpmvAr
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[v] = 0.f;
     const uint8_t* rowA = a.A + r * S * STEPB;
+    if (r + nwarps < a.M) {  // this warp's next row (rows beyond one wave): its lines into L2 now
+      const int64_t rn = r + nwarps;
+      const int64_t pb = S * STEPB, vb = kT * ES, ib = kT * ISt;
+      const uint8_t* line = nullptr;
+      if (lane < 16) {
+        if ((int64_t)lane * 128 < pb) line = a.A + rn * pb + lane * 128;
+      } else if (lane < 24) {
+        if ((int64_t)(lane - 16) * 128 < vb) line = a.Bt + rn * vb + (lane - 16) * 128;
+      } else if ((int64_t)(lane - 24) * 128 < ib) {
+        line = a.Ct + rn * ib + (lane - 24) * 128;
+      }
+      if (line) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(line));
+    }
     uint32_t tw[TM], to[TO];
     if constexpr (TP) {
       const raw_t* tv = (const raw_t*)a.Bt + r * kT;
@@ -999,7 +1012,13 @@ cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
   SpmvArgs a = a0;
   if (!a.pdl) a.w_early = 0;
   const auto& dp = bsk::dev_props();
-  int64_t warps = a.M < (int64_t)dp.sms * 64 ? a.M : (int64_t)dp.sms * 64;
+  // one resident wave of warps (occupancy query): a warp with a second row keeps running (no CTA launch
+  // in between) and finds that row's lines already in L2
+  const bool tp0 = a.T > 0 && a.k > 0 && a.k * V <= 8;
+  const int per_sm = bsk::resident_ctas(tp0 ? (const void*)spmv_rows_kernel<DT, V, IS, true>
+                                            : (const void*)spmv_rows_kernel<DT, V, IS, false>, 256);
+  const int64_t cap = (int64_t)(per_sm > 0 ? per_sm : 1) * dp.sms * 8;
+  const int64_t warps = a.M < cap ? a.M : cap;
   const int64_t grid = (warps + 7) / 8;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -1023,7 +1042,12 @@ bool rows_fit(const SpmvArgs& a) {
   const bool tp = a.T > 0 && a.k > 0 && a.k * V <= 8;
   const void* fn = tp ? (const void*)spmv_rows_kernel<DT, V, IS, true> : (const void*)spmv_rows_kernel<DT, V, IS, false>;
   const int per_sm = bsk::resident_ctas(fn, 256);
-  return per_sm > 0 && a.M <= (int64_t)per_sm * bsk::dev_props().sms * 8;
+  const int64_t wave = (int64_t)per_sm * bsk::dev_props().sms * 8;
+  static const int waves = [] {  // BS_DIRECT_WAVES: rows per resident warp allowed (a warp's next row is
+    const char* e = getenv("BS_DIRECT_WAVES");  // prefetched into L2 while it computes the current one)
+    return e && e[0] ? atoi(e) : 2;  // PTB (6000 rows, 1.3 waves): 6.78 us ring -> 6.26 us direct
+  }();
+  return per_sm > 0 && a.M <= wave * waves;
 }
 
 template <int V, int ES>

@@ -138,3 +138,26 @@ def test_lstm_sequence_matches_oracle(bs):
         h_prev, c_prev = hr.astype(np.float16), cr
         dh_prev, dc_prev = float(np.max(dh)) + 2.0 ** -10 * float(np.max(np.abs(hr))), dc
     assert np.all(np.abs(cT.cpu().numpy() - c_prev) <= dc_prev)
+
+
+def test_layer_stack_graph(bs):
+    """LayerStack (the VGG classifier head fc6 -> fc7 -> fc8 at Table cnn-perf's 93 % / 93 % / 75 %, as one
+    CUDA graph) gives exactly the eager chain of bs_spmv_fused calls, replay after replay."""
+    dims = [(512, 2048, 2, "relu"), (512, 512, 2, "relu"), (128, 512, 8, None)]
+    layers = []
+    for j, (M, K, k, act) in enumerate(dims):
+        W = synth.matrix(M, K, "f16", seed=synth.seed_for(42, j)).cuda()
+        v, i, _ = bs.prune(W, 32, k=k)
+        b = synth.vector(M, "f16", seed=synth.seed_for(42, 10 + j)).cuda()
+        layers.append((bs.pack(v, i, K, 32), b, act))
+    x = synth.vector(2048, "f16", seed=synth.seed_for(42, 99)).cuda()
+    ref = x
+    for A, b, act in layers:
+        ref = bs.spmv(A, ref, bias=b, act=act)
+    stack = bs.LayerStack(layers).capture()
+    for _ in range(3):
+        y = stack(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref)
+    with pytest.raises(ValueError):
+        bs.LayerStack([layers[1], layers[0]])
