@@ -846,18 +846,42 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
 // over the panel steps in order; with a tail, the panel total and the tail total (tail entries in t
 // order) are reduced separately and added; the same FHFMA. So both kernels give bit-identical rows, and
 // the choice (host: per-row bytes, never M) keeps row sharding bit-identical.
-template <int DT, int V, int IS, bool TP>
-__global__ void __launch_bounds__(256, (V <= 4 ? 4 : 1)) spmv_rows_kernel(SpmvArgs a) {
+// HW (half-warp rows): 16 lanes per row, so that twice as many rows are resident in one wave (PTB: 6000
+// rows, one wave of warps holds 4736). Lane h plays the ring kernel's lanes h and h + 16 (separate
+// accumulators, acc[j][v] for lane h + 16j); their lane totals are added first, which is exactly the
+// butterfly's xor-16 step, and xor 8, 4, 2, 1 follow within the half: the same sums in the same order.
+template <int V, int NJ>
+__device__ __forceinline__ float row_total(float (&acc)[NJ][V]) {
+  float t = 0.f;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    float s = acc[j][0];
+#pragma unroll
+    for (int v = 1; v < V; ++v) s += acc[j][v];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[j][v] = 0.f;
+    t = j == 0 ? s : t + s;
+  }
+#pragma unroll
+  for (int o = NJ == 2 ? 8 : 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+template <int DT, int V, int IS, bool TP, bool HW>
+__global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 1)) spmv_rows_kernel(SpmvArgs a) {
   using raw_t = typename bsk::DTraits<DT>::raw_t;
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int P = 32 * V;
   constexpr int ISt = IS == 5 ? 1 : IS;
   constexpr uint32_t RI = IS == 5 ? 160u : (uint32_t)P * IS;
   constexpr uint32_t STEPB = (uint32_t)P * ES + RI;
-  constexpr int G = 4;                                   // steps per load group
+  constexpr int G = HW ? 3 : 4;                          // steps per load group (HW: registers for two lanes)
   constexpr int WW = (V * ES + 3) / 4;                   // value words per lane and step
   constexpr int IW = IS == 5 ? 2 : (V * IS + 3) / 4;     // index words per lane and step
+  constexpr int NJ = HW ? 2 : 1;                         // ring-kernel lanes played by one lane
   const int lane = threadIdx.x & 31;
+  const int sub = HW ? (lane >> 4) : 0;                  // HW: which row of the warp's pair
+  const int hl = HW ? (lane & 15) : lane;                // ring-kernel lane of j = 0 (j = 1: hl + 16)
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   pdl_launch_dependents();
   bool waited = !a.w_early;
@@ -873,12 +897,16 @@ __global__ void __launch_bounds__(256, (V <= 4 ? 4 : 1)) spmv_rows_kernel(SpmvAr
   // layers without a tail. 16-bit values: value | index << 16 in one register per entry.
   constexpr int TM = TP ? 8 : 1;
   constexpr int TO = ES == 2 ? 1 : TM;
-  for (int64_t r = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); r < a.M; r += nwarps) {
-    float acc[V];
+  for (int64_t r0 = ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * NJ; r0 < a.M; r0 += nwarps * NJ) {
+    const int64_t r = r0 + sub;
+    const bool live = !HW || r < a.M;  // HW: the warp's second row may not exist (the shuffles still need the lanes)
+    float acc[NJ][V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) acc[v] = 0.f;
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[j][v] = 0.f;
     const uint8_t* rowA = a.A + r * S * STEPB;
-    if (r + nwarps < a.M) {  // this warp's next row (rows beyond one wave): its lines into L2 now
+    if (!HW && r + nwarps < a.M) {  // this warp's next row (rows beyond one wave): its lines into L2 now
       const int64_t rn = r + nwarps;
       const int64_t pb = S * STEPB, vb = kT * ES, ib = kT * ISt;
       const uint8_t* line = nullptr;
@@ -891,49 +919,55 @@ __global__ void __launch_bounds__(256, (V <= 4 ? 4 : 1)) spmv_rows_kernel(SpmvAr
       }
       if (line) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(line));
     }
-    uint32_t tw[TM], to[TO];
+    uint32_t tw[NJ][TM], to[NJ][TO];
     if constexpr (TP) {
       const raw_t* tv = (const raw_t*)a.Bt + r * kT;
       const uint8_t* ti = a.Ct + r * kT * ISt;
 #pragma unroll
-      for (int q = 0; q < TM; ++q) {
-        const int tt = q / V, v = q - (q / V) * V;  // entry q = (tt, v)
-        const int bl = v * 32 + lane;
-        tw[q] = 0u;
-        if constexpr (ES != 2) to[q] = 0u;
-        if (tt < k && v < Vt && bl < a.T) {
-          const int64_t e = (int64_t)tt * a.T + bl;
-          const uint32_t o = ISt == 1 ? (uint32_t)__ldg(ti + e) : (uint32_t)__ldg((const uint16_t*)ti + e);
-          if constexpr (ES == 2) tw[q] = (uint32_t)__ldg(tv + e) | (o << 16);
-          else {
-            tw[q] = (uint32_t)__ldg(tv + e);
-            to[q] = o;
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int q = 0; q < TM; ++q) {
+          const int tt = q / V, v = q - (q / V) * V;  // entry q = (tt, v)
+          const int bl = v * 32 + hl + 16 * j;
+          tw[j][q] = 0u;
+          if constexpr (ES != 2) to[j][q] = 0u;
+          if (live && tt < k && v < Vt && bl < a.T) {
+            const int64_t e = (int64_t)tt * a.T + bl;
+            const uint32_t o = ISt == 1 ? (uint32_t)__ldg(ti + e) : (uint32_t)__ldg((const uint16_t*)ti + e);
+            if constexpr (ES == 2) tw[j][q] = (uint32_t)__ldg(tv + e) | (o << 16);
+            else {
+              tw[j][q] = (uint32_t)__ldg(tv + e);
+              to[j][q] = o;
+            }
           }
         }
-      }
     }
     for (int64_t s0 = 0; s0 < S; s0 += G) {
-      uint32_t wv[G][WW], iv[G][IW];
+      uint32_t wv[G][NJ][WW], iv[G][NJ][IW];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        if (s0 + g < S) {
+        if (live && s0 + g < S) {
           const uint8_t* st = rowA + (s0 + g) * STEPB;
-          bsk::Vec<V * ES> vv;
-          vv.load(st + lane * (V * ES));
 #pragma unroll
-          for (int q = 0; q < WW; ++q) wv[g][q] = vv.w[q];
-          if constexpr (IS == 5) {
-            bsk::Vec<4> i0;
-            bsk::Vec<1> i1;
-            i0.load(st + P * ES + 4 * lane);
-            i1.load(st + P * ES + 128 + lane);
-            iv[g][0] = i0.w[0];
-            iv[g][1] = i1.w[0];
-          } else {
-            bsk::Vec<V * IS> ii;
-            ii.load(st + P * ES + lane * (V * IS));
+          for (int j = 0; j < NJ; ++j) {
+            const int L = hl + 16 * j;
+            bsk::Vec<V * ES> vv;
+            vv.load(st + L * (V * ES));
 #pragma unroll
-            for (int q = 0; q < IW; ++q) iv[g][q] = ii.w[q];
+            for (int q = 0; q < WW; ++q) wv[g][j][q] = vv.w[q];
+            if constexpr (IS == 5) {
+              bsk::Vec<4> i0;
+              bsk::Vec<1> i1;
+              i0.load(st + P * ES + 4 * L);
+              i1.load(st + P * ES + 128 + L);
+              iv[g][j][0] = i0.w[0];
+              iv[g][j][1] = i1.w[0];
+            } else {
+              bsk::Vec<V * IS> ii;
+              ii.load(st + P * ES + L * (V * IS));
+#pragma unroll
+              for (int q = 0; q < IW; ++q) iv[g][j][q] = ii.w[q];
+            }
           }
         }
       }
@@ -943,18 +977,20 @@ __global__ void __launch_bounds__(256, (V <= 4 ? 4 : 1)) spmv_rows_kernel(SpmvAr
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        if (s0 + g < S) {
+        if (live && s0 + g < S) {
           const int64_t p = (s0 + g) / k;
 #pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const uint32_t w = ES == 2 ? (wv[g][v >> 1] >> (16 * (v & 1))) & 0xffffu : wv[g][v];
-            uint32_t o;
-            if constexpr (IS == 5) o = (v < 7 ? __funnelshift_r(iv[g][0], iv[g][1], 5 * v) : iv[g][1] >> 3) & 31u;
-            else if constexpr (IS == 1) o = byte_of(iv[g][v >> 2], v & 3);
-            else o = (iv[g][v >> 1] >> (16 * (v & 1))) & 0xffffu;
-            const int64_t b = p * P + v * 32 + lane;
-            bsk::fma_acc<DT>(acc[v], w, (uint32_t)__ldg(x + b * B + o));
-          }
+          for (int j = 0; j < NJ; ++j)
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const uint32_t w = ES == 2 ? (wv[g][j][v >> 1] >> (16 * (v & 1))) & 0xffffu : wv[g][j][v];
+              uint32_t o;
+              if constexpr (IS == 5) o = (v < 7 ? __funnelshift_r(iv[g][j][0], iv[g][j][1], 5 * v) : iv[g][j][1] >> 3) & 31u;
+              else if constexpr (IS == 1) o = byte_of(iv[g][j][v >> 2], v & 3);
+              else o = (iv[g][j][v >> 1] >> (16 * (v & 1))) & 0xffffu;
+              const int64_t b = p * P + v * 32 + hl + 16 * j;
+              bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + b * B + o));
+            }
         }
       }
     }
@@ -964,41 +1000,45 @@ __global__ void __launch_bounds__(256, (V <= 4 ? 4 : 1)) spmv_rows_kernel(SpmvAr
     }
     float y;
     if (a.T > 0 && k > 0) {
-      const float panel = S > 0 ? warp_total<V>(acc) : 0.f;  // (zeroes acc)
+      const float panel = S > 0 ? row_total<V, NJ>(acc) : 0.f;  // (zeroes acc)
       const raw_t* tv = (const raw_t*)a.Bt + r * kT;
       const uint8_t* ti = a.Ct + r * kT * ISt;
       if constexpr (TP) {  // the same (tt, v) order as the loop below
 #pragma unroll
-        for (int q = 0; q < TM; ++q) {
-          const int tt = q / V, v = q - (q / V) * V;
-          const int bl = v * 32 + lane;
-          if (tt < k && v < Vt && bl < a.T) {
-            const int64_t b = a.NBf * P + bl;
-            const uint32_t w = ES == 2 ? (tw[q] & 0xffffu) : tw[q];
-            const uint32_t o = ES == 2 ? (tw[q] >> 16) : to[q < TO ? q : 0];
-            bsk::fma_acc<DT>(acc[v], w, (uint32_t)__ldg(x + b * B + o));
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int q = 0; q < TM; ++q) {
+            const int tt = q / V, v = q - (q / V) * V;
+            const int bl = v * 32 + hl + 16 * j;
+            if (live && tt < k && v < Vt && bl < a.T) {
+              const int64_t b = a.NBf * P + bl;
+              const uint32_t w = ES == 2 ? (tw[j][q] & 0xffffu) : tw[j][q];
+              const uint32_t o = ES == 2 ? (tw[j][q] >> 16) : to[j][q < TO ? q : 0];
+              bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + b * B + o));
+            }
           }
-        }
       }
       for (int tt = TP ? k : 0; tt < k; ++tt) {
         const int64_t e0 = (int64_t)tt * a.T;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const int bl = v * 32 + lane;
-          if (v < Vt && bl < a.T) {
-            const uint32_t w = (uint32_t)__ldg(tv + e0 + bl);
-            const uint32_t o = ISt == 1 ? (uint32_t)__ldg(ti + e0 + bl) : (uint32_t)__ldg((const uint16_t*)ti + e0 + bl);
-            const int64_t b = a.NBf * P + bl;
-            bsk::fma_acc<DT>(acc[v], w, (uint32_t)__ldg(x + b * B + o));
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const int bl = v * 32 + hl + 16 * j;
+            if (live && v < Vt && bl < a.T) {
+              const uint32_t w = (uint32_t)__ldg(tv + e0 + bl);
+              const uint32_t o = ISt == 1 ? (uint32_t)__ldg(ti + e0 + bl) : (uint32_t)__ldg((const uint16_t*)ti + e0 + bl);
+              const int64_t b = a.NBf * P + bl;
+              bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + b * B + o));
+            }
           }
-        }
       }
-      const float tail = warp_total<V>(acc);
+      const float tail = row_total<V, NJ>(acc);
       y = S > 0 ? panel + tail : tail;
     } else {
-      y = warp_total<V>(acc);  // k == 0: 0
+      y = row_total<V, NJ>(acc);  // k == 0: 0
     }
-    if (lane == 0) {
+    if (hl == 0 && live) {
       if (a.bias) y += bsk::to_float<DT>(__ldg((const raw_t*)a.bias + r));
       if (a.act) y = apply_act(y, a.act);
       ((raw_t*)a.y)[r] = (raw_t)bsk::from_float<DT>(y);
@@ -1007,18 +1047,24 @@ __global__ void __launch_bounds__(256, (V <= 4 ? 4 : 1)) spmv_rows_kernel(SpmvAr
   if (!waited) pdl_wait();
 }
 
-template <int DT, int V, int IS>
+template <int DT, int V, int IS, bool HW>
+const void* rows_fn(const SpmvArgs& a) {
+  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return (const void*)spmv_rows_kernel<DT, V, IS, true, HW>;
+  return (const void*)spmv_rows_kernel<DT, V, IS, false, HW>;
+}
+
+template <int DT, int V, int IS, bool HW>
 cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
   SpmvArgs a = a0;
   if (!a.pdl) a.w_early = 0;
   const auto& dp = bsk::dev_props();
   // one resident wave of warps (occupancy query): a warp with a second row keeps running (no CTA launch
   // in between) and finds that row's lines already in L2
-  const bool tp0 = a.T > 0 && a.k > 0 && a.k * V <= 8;
-  const int per_sm = bsk::resident_ctas(tp0 ? (const void*)spmv_rows_kernel<DT, V, IS, true>
-                                            : (const void*)spmv_rows_kernel<DT, V, IS, false>, 256);
+  constexpr int NJ = HW ? 2 : 1;
+  const int per_sm = bsk::resident_ctas(rows_fn<DT, V, IS, HW>(a), 256);
   const int64_t cap = (int64_t)(per_sm > 0 ? per_sm : 1) * dp.sms * 8;
-  const int64_t warps = a.M < cap ? a.M : cap;
+  const int64_t need = (a.M + NJ - 1) / NJ;
+  const int64_t warps = need < cap ? need : cap;
   const int64_t grid = (warps + 7) / 8;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -1030,24 +1076,49 @@ cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = a.pdl ? 1 : 0;
-  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, true>, a);
-  return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, false>, a);
+  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, true, HW>, a);
+  return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, false, HW>, a);
 }
 
 // The direct kernel pays off while every row gets its own resident warp (one wave): a second wave adds
 // a whole row latency (PTB, 6000 rows: 7.0 us direct vs 6.8 us ring; fc7 and CTC, 4096 rows: 1.15-1.35x
-// faster direct). Both kernels give bit-identical rows, so the choice may depend on M.
+// faster direct). Rows beyond one wave of warps take half-warp rows (V <= 4) while those fit one wave,
+// else (BS_DIRECT_WAVES, default 2) a warp takes a second row. All give bit-identical rows, so the choice
+// may depend on M. Returns 0 (ring kernel), 1 (warp rows) or 2 (half-warp rows).
 template <int DT, int V, int IS>
-bool rows_fit(const SpmvArgs& a) {
-  const bool tp = a.T > 0 && a.k > 0 && a.k * V <= 8;
-  const void* fn = tp ? (const void*)spmv_rows_kernel<DT, V, IS, true> : (const void*)spmv_rows_kernel<DT, V, IS, false>;
-  const int per_sm = bsk::resident_ctas(fn, 256);
+int rows_mode(const SpmvArgs& a) {
+  const int per_sm = bsk::resident_ctas(rows_fn<DT, V, IS, false>(a), 256);
   const int64_t wave = (int64_t)per_sm * bsk::dev_props().sms * 8;
+  if (per_sm > 0 && a.M <= wave) return 1;
+  static const int half = [] {  // BS_DIRECT_HALF=0: no half-warp rows (A/B)
+    const char* e = getenv("BS_DIRECT_HALF");
+    return e && e[0] ? atoi(e) : 1;
+  }();
+  if constexpr (V <= 4) {
+    if (half) {
+      const int ph = bsk::resident_ctas(rows_fn<DT, V, IS, true>(a), 256);
+      if (ph > 0 && a.M <= (int64_t)ph * bsk::dev_props().sms * 16) return 2;
+    }
+  }
   static const int waves = [] {  // BS_DIRECT_WAVES: rows per resident warp allowed (a warp's next row is
     const char* e = getenv("BS_DIRECT_WAVES");  // prefetched into L2 while it computes the current one)
     return e && e[0] ? atoi(e) : 2;  // PTB (6000 rows, 1.3 waves): 6.78 us ring -> 6.26 us direct
   }();
-  return per_sm > 0 && a.M <= wave * waves;
+  return per_sm > 0 && a.M <= wave * waves ? 1 : 0;
+}
+
+template <int DT, int V, int IS>
+bool try_rows(const SpmvArgs& a, cudaStream_t s, cudaError_t* e) {
+  const int m = rows_mode<DT, V, IS>(a);
+  if (m == 0) return false;
+  if constexpr (V <= 4) {
+    if (m == 2) {
+      *e = launch_rows<DT, V, IS, true>(a, s);
+      return true;
+    }
+  }
+  *e = launch_rows<DT, V, IS, false>(a, s);
+  return true;
 }
 
 template <int V, int ES>
@@ -1143,13 +1214,14 @@ template <int DT, int IS, int NV>
 cudaError_t dispatch_v(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
   if constexpr (NV == 1) {
     if (a.direct) {
+      cudaError_t e = cudaSuccess;
       switch (g.V) {
-        case 1: if (rows_fit<DT, 1, IS>(a)) return launch_rows<DT, 1, IS>(a, s); break;
-        case 2: if (rows_fit<DT, 2, IS>(a)) return launch_rows<DT, 2, IS>(a, s); break;
-        case 4: if (rows_fit<DT, 4, IS>(a)) return launch_rows<DT, 4, IS>(a, s); break;
+        case 1: if (try_rows<DT, 1, IS>(a, s, &e)) return e; break;
+        case 2: if (try_rows<DT, 2, IS>(a, s, &e)) return e; break;
+        case 4: if (try_rows<DT, 4, IS>(a, s, &e)) return e; break;
         default:
           if constexpr (DT != BS_F32)
-            if (rows_fit<DT, 8, IS>(a)) return launch_rows<DT, 8, IS>(a, s);
+            if (try_rows<DT, 8, IS>(a, s, &e)) return e;
       }
     }
   }
@@ -1168,7 +1240,10 @@ cudaError_t dispatch_is(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
   if constexpr (DT != BS_F32)
     if (g.ri != g.P * g.is) {  // 5-bit index runs
       if constexpr (NV == 1)
-        if (a.direct && rows_fit<DT, 8, 5>(a)) return launch_rows<DT, 8, 5>(a, s);
+        if (a.direct) {
+          cudaError_t e = cudaSuccess;
+          if (try_rows<DT, 8, 5>(a, s, &e)) return e;
+        }
       return launch_t<DT, 8, 5, NV>(a, s);
     }
   return g.is == 1 ? dispatch_v<DT, 1, NV>(g, a, s) : dispatch_v<DT, 2, NV>(g, a, s);

@@ -239,7 +239,11 @@ def test_block_rank_errors_and_alignment(bs):
 # ---------------------------------------------------------------- direct (short-row) SpMV kernel vs the ring kernel
 
 @pytest.mark.parametrize("M,K,B,k,dname", [
-    (6000, 3008, 32, 3, "f16"),    # PTB (panel + tail): more rows than one wave of the direct kernel: ring
+    (6000, 3008, 32, 3, "f16"),    # PTB (panel + tail): more rows than one wave of warps: half-warp rows
+    (6000, 3008, 32, 6, "bf16"),   # half-warp rows, k·V > 8: tail through the loop
+    (5001, 2048, 32, 4, "f16"),    # half-warp rows, odd M (the last warp's second row does not exist)
+    (5000, 1024, 32, 4, "bf16"),   # half-warp rows, V = 1
+    (9000, 3008, 32, 3, "f16"),    # beyond one wave of half-warp rows: a warp takes a second row
     (1000, 3008, 32, 3, "bf16"),   # PTB width in one wave: direct with the tail held in registers
     (2000, 3008, 32, 6, "f16"),    # k·V > 8: direct, tail through the loop
     (4096, 4096, 32, 3, "bf16"),   # fc7 90 %
