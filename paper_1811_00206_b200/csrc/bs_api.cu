@@ -27,6 +27,7 @@ const DevProps& dev_props() {
     cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&p.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&p.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&p.l2_bytes, cudaDevAttrL2CacheSize, dev);
     if (p.sms <= 0) p.sms = 148;
     props[dev] = p;
     have[dev] = true;

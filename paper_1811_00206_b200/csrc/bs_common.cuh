@@ -95,6 +95,7 @@ struct DevProps {
   int sms;
   int smem_optin;   // max dynamic smem per block (opt-in)
   int smem_per_sm;
+  int l2_bytes;
 };
 const DevProps& dev_props();
 
@@ -117,6 +118,18 @@ inline int splitk_min_chunks(int dflt) {
     return e && e[0] ? atoi(e) : 0;
   }();
   return v >= 1 ? v : dflt;
+}
+
+// Tensor-core SpMM grid order (K5, K6): 1 (default) launches a row tile's column tiles next to each other
+// (grid x = column tile · S + split rank, y = row tile), so that they stream the tile's W from HBM once and
+// share it through L2; 0 (BS_TC_ORDER=0) is round 1's order (x = row tile · S + rank, y = column tile),
+// which streams all of W once per column tile when W exceeds L2.
+inline int tc_cols_fast() {
+  static const int v = [] {
+    const char* e = getenv("BS_TC_ORDER");
+    return e && e[0] ? atoi(e) : 1;
+  }();
+  return v;
 }
 
 }  // namespace bsk

@@ -83,6 +83,26 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t local_addr, uint32_t ra
   return v;
 }
 
+// CTA pairs (cta_group::2): the address of `local_addr` in CTA `rank` of the cluster, and an mbarrier
+// arrive there. Relaxed: a release at cluster scope compiles to a MEMBAR that waits for every load the
+// thread has in flight (the metadata prefetch: ncu showed 46 % membar stalls); the arrive only counts,
+// and the tensor-memory stores it announces are ordered by tcgen05.wait::st + fence::before_thread_sync.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local_addr, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(rank));
+  return ra;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-D tensor copy into this CTA's shared memory that completes on an mbarrier of either CTA of the pair
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+
 }  // namespace bsk_tc
 
 // 2-D tensor map of a row-major [rows][cols] 16-bit matrix (dt f16 / bf16) with row stride `ld`

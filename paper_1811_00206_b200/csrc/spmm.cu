@@ -60,6 +60,7 @@ struct TcArgs {
   int blob_max;       // bytes of a full blob (128 rows, CB blocks)
   uint32_t idesc;
   int tmem_cols, acc_cols;  // allocated columns; columns per accumulator (one per MMA warp)
+  int colfast;        // grid order (bsk::tc_cols_fast)
 };
 
 template <int DT>
@@ -82,10 +83,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
   const int lg_na = NA == 8 ? 3 : 2;
   const int S = a.S;
   const int rank = S > 1 ? (int)cluster_rank() : 0;
-  const int64_t tile = blockIdx.x / S;
+  const int64_t tile = a.colfast ? blockIdx.y : blockIdx.x / S;
   const int64_t m0 = tile * BM;
   const int64_t mt = (a.M - m0) < BM ? (a.M - m0) : BM;
-  const int64_t n0 = (int64_t)blockIdx.y * a.BN;
+  const int64_t n0 = (int64_t)(a.colfast ? blockIdx.x / S : blockIdx.y) * a.BN;
   const int c0 = (int)((int64_t)rank * a.NC / S), c1 = (int)((int64_t)(rank + 1) * a.NC / S);
   const int nloc = c1 - c0;  // >= 1 (S <= NC)
   const uint8_t* tile_base = a.W + tile * a.tile_stride;
@@ -392,7 +393,10 @@ cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int
   CUtensorMap tX;
   if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, KC, (int)BN)) return cudaErrorNotSupported;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(g.P * a.S), (unsigned)((N + BN - 1) / BN));
+  // column tiles adjacent only when W exceeds half of L2 (fc6, 31 MB, ran 10 % slower at N = 128 with them)
+  a.colfast = bsk::tc_cols_fast() && g.P <= 65535 && g.total > (int64_t)bsk::dev_props().l2_bytes / 2;
+  const unsigned nct = (unsigned)((N + BN - 1) / BN);
+  cfg.gridDim = a.colfast ? dim3(nct * (unsigned)a.S, (unsigned)g.P) : dim3((unsigned)(g.P * a.S), nct);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = s;

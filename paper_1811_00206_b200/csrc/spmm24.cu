@@ -23,8 +23,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int KCH = 128;  // original columns per chunk (64 compressed values: one 128-byte swizzle atom)
-constexpr int kMaxStages = 4;  // pipeline stages (runtime NST: 2..4, fewer for BN = 256)
-constexpr int kThreads = 192;
+constexpr int kMaxStages = 4;  // pipeline stages (runtime NST: 2..4, fewer for BN = 256 or RT = 2)
+constexpr int kMetaCols = 16 * 4;  // TMEM metadata columns per row tile: kMaxStages × 4 K-steps × mstride 4
 
 struct Sp24Args {
   const uint8_t* meta;  // M × K/8 bytes
@@ -34,39 +34,44 @@ struct Sp24Args {
   int S;                // split-K cluster size
   int NST;              // pipeline stages
   uint32_t idesc;
-  int tmem_cols, meta_col;
+  int tmem_cols, meta_col, acc_stride;  // allocated TMEM columns; first metadata column; columns per accumulator
   int mstride;          // TMEM columns between the metadata of consecutive K = 32 steps
+  int colfast;          // grid order (bsk::tc_cols_fast)
 };
 
 using namespace bsk_tc;
 
-template <int DT>
-__global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_constant__ CUtensorMap tA,
-                                                             const __grid_constant__ CUtensorMap tX, Sp24Args a) {
+// RT row tiles of 128 rows per CTA (RT = 2: M = 256 per CTA, two accumulators in TMEM that share every
+// X tile, which halves the X traffic from L2 on layers with many row tiles; each row's sum is the same
+// sequence of M = 128 MMAs either way).
+template <int DT, int RT>
+__global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_constant__ CUtensorMap tA,
+                                                                  const __grid_constant__ CUtensorMap tX, Sp24Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bars[3 * kMaxStages + 1];
   using raw_t = uint16_t;
   __shared__ uint32_t tmem_holder;
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t ASZ = BM * 128;                 // compressed A chunk: 128 rows × 128 B
+  const uint32_t ASZ = BM * 128;                 // compressed A chunk of one row tile: 128 rows × 128 B
   const uint32_t BSZ = 2u * (uint32_t)a.BN * 128;  // X chunk: 2 atoms of BN rows × 128 B
   const int NST = a.NST;
-  const uint32_t sA = smem_u32(smem), sB = sA + NST * ASZ;
+  const uint32_t sA = smem_u32(smem), sB = sA + NST * RT * ASZ;
   const uint32_t full = smem_u32(&bars[0]), empty = smem_u32(&bars[kMaxStages]);
   const uint32_t meta_ok = smem_u32(&bars[2 * kMaxStages]), acc_full = smem_u32(&bars[3 * kMaxStages]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.S;
   const int rank = S > 1 ? (int)cluster_rank() : 0;
-  const int64_t m0 = (int64_t)(blockIdx.x / S) * BM;
-  const int64_t mt = (a.M - m0) < BM ? (a.M - m0) : BM;
-  const int64_t n0 = (int64_t)blockIdx.y * a.BN;
+  const int64_t m0 = (int64_t)(a.colfast ? blockIdx.y : blockIdx.x / S) * (BM * RT);
+  const int64_t mrows = (a.M - m0) < BM * RT ? (a.M - m0) : BM * RT;  // rows of this CTA
+  const int rtl = (int)((mrows + BM - 1) / BM);                       // live row tiles (1..RT)
+  const int64_t n0 = (int64_t)(a.colfast ? blockIdx.x / S : blockIdx.y) * a.BN;
   const int c0 = (int)((int64_t)rank * a.NC / S), nloc = (int)((int64_t)(rank + 1) * a.NC / S) - c0;  // >= 1
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(full + 8 * s, 1);
       mbar_init(empty + 8 * s, 1);
-      mbar_init(meta_ok + 8 * s, 128);
+      mbar_init(meta_ok + 8 * s, 4 * RT);  // one arrive per metadata warp
     }
     mbar_init(acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -94,8 +99,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
       for (int i = 0; i < nloc; ++i) {
         const int c = c0 + i;
         if (i >= NST) mbar_wait(empty + 8 * s, ph ^ 1u);
-        mbar_expect_tx(full + 8 * s, ASZ + BSZ);
-        tma_2d(sA + s * ASZ, &tA, c * (KCH / 2), (int)m0, full + 8 * s);
+        mbar_expect_tx(full + 8 * s, (uint32_t)rtl * ASZ + BSZ);
+        for (int t = 0; t < rtl; ++t) tma_2d(sA + (s * RT + t) * ASZ, &tA, c * (KCH / 2), (int)(m0 + t * BM), full + 8 * s);
         tma_2d(sB + s * BSZ, &tX, c * KCH, (int)n0, full + 8 * s);
         tma_2d(sB + s * BSZ + (uint32_t)a.BN * 128, &tX, c * KCH + 64, (int)n0, full + 8 * s);
         if (++s == NST) { s = 0; ph ^= 1u; }
@@ -109,17 +114,22 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
         mbar_wait(full + 8 * s, par);
         mbar_wait(meta_ok + 8 * s, par);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint64_t da = sw128_desc(sA + s * ASZ);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          // A: 16 compressed values (32 B) per K = 32 step; B: 32 columns (64 B) per step, atom j / 2
-          const uint64_t db = sw128_desc(sB + s * BSZ + (uint32_t)(j >> 1) * (uint32_t)a.BN * 128) + (uint64_t)((j & 1) * 4);
-          const uint32_t te = tmem + (uint32_t)a.meta_col + (uint32_t)((s * 4 + j) * a.mstride);
-          const uint32_t acc = (i > 0 || j > 0) ? 1u : 0u;
-          asm volatile(
-              "{ .reg .pred p; setp.ne.b32 p, %5, 0;\n\t"
-              "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, p; }" ::"r"(tmem),
-              "l"(da + (uint64_t)(j * 2)), "l"(db), "r"(te), "r"(a.idesc), "r"(acc));
+        for (int t = 0; t < RT; ++t) {
+          if (t < rtl) {
+            const uint64_t da = sw128_desc(sA + (s * RT + t) * ASZ);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              // A: 16 compressed values (32 B) per K = 32 step; B: 32 columns (64 B) per step, atom j / 2
+              const uint64_t db = sw128_desc(sB + s * BSZ + (uint32_t)(j >> 1) * (uint32_t)a.BN * 128) + (uint64_t)((j & 1) * 4);
+              const uint32_t te = tmem + (uint32_t)(a.meta_col + t * kMetaCols) + (uint32_t)((s * 4 + j) * a.mstride);
+              const uint32_t acc = (i > 0 || j > 0) ? 1u : 0u;
+              asm volatile(
+                  "{ .reg .pred p; setp.ne.b32 p, %5, 0;\n\t"
+                  "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, p; }" ::"r"(tmem + (uint32_t)(t * a.acc_stride)),
+                  "l"(da + (uint64_t)(j * 2)), "l"(db), "r"(te), "r"(a.idesc), "r"(acc));
+            }
+          }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty + 8 * s)
                      : "memory");
@@ -130,12 +140,15 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
     }
   } else {
     // ---- metadata → tensor memory (thread = row); then the epilogue. A row's 16 metadata bytes of a
-    // chunk are loaded two chunks ahead, so the global latency overlaps the MMAs.
-    const int q = warp & 3;  // TMEM lane quarter of this warp: rows 32q .. 32q + 31
-    const int64_t row = 32 * q + lane;
-    const uint8_t* mrow = a.meta + (m0 + row) * (a.K / 8) + (int64_t)c0 * 16;
+    // chunk are loaded two chunks ahead, so the global latency overlaps the MMAs. Warp w >= 2 serves row
+    // tile (w - 2) / 4 and TMEM lane quarter w % 4 (the quarter a warp may access).
+    const int q = warp & 3;  // TMEM lane quarter of this warp: rows 32q .. 32q + 31 of its tile
+    const int t = (warp - 2) >> 2;
+    const int64_t row = 32 * q + lane;  // in the tile
+    const int64_t trow = (int64_t)t * BM + row;  // in the CTA's rows
+    const uint8_t* mrow = a.meta + (m0 + trow) * (a.K / 8) + (int64_t)c0 * 16;
     auto ldm = [&](int i) {
-      return (row < mt && i < nloc) ? __ldg((const uint4*)(mrow + (int64_t)i * 16)) : make_uint4(0u, 0u, 0u, 0u);
+      return (trow < mrows && i < nloc) ? __ldg((const uint4*)(mrow + (int64_t)i * 16)) : make_uint4(0u, 0u, 0u, 0u);
     };
     uint4 m_cur = ldm(0), m_nxt = ldm(1);
     int s = 0;
@@ -145,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
       const uint4 m = m_cur;
       m_cur = m_nxt;
       m_nxt = ldm(i + 2);
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)a.meta_col + (uint32_t)(s * 4 * a.mstride);
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a.meta_col + t * kMetaCols) + (uint32_t)(s * 4 * a.mstride);
       const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -161,26 +174,28 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(meta_ok + 8 * s);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(meta_ok + 8 * s);
       if (++s == NST) { s = 0; ph ^= 1u; }
     }
     mbar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // split-K partial tile [BN][128] fp32 at sA (the rings are idle now)
+    // split-K partial tile [BN][128·RT] fp32 at sA (the rings are idle now)
+    const int64_t mt = mrows - (int64_t)t * BM;  // rows of this warp's tile (may be <= 0)
     for (int nb = 0; nb < a.BN; nb += 8) {
       uint32_t r[8];
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                   : "r"(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)nb));
+                   : "r"(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(t * a.acc_stride + nb)));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (S > 1) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) bsk::sts_u32(sA + (uint32_t)(((nb + e) * BM + row) * 4), r[e]);
+        for (int e = 0; e < 8; ++e) bsk::sts_u32(sA + (uint32_t)(((nb + e) * (BM * RT) + trow) * 4), r[e]);
       } else if (row < mt) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int64_t ng = n0 + nb + e;
-          if (ng < a.N) ((raw_t*)a.Y)[ng * a.ldy + m0 + row] = (raw_t)bsk::from_float<DT>(__uint_as_float(r[e]));
+          if (ng < a.N) ((raw_t*)a.Y)[ng * a.ldy + m0 + trow] = (raw_t)bsk::from_float<DT>(__uint_as_float(r[e]));
         }
       }
     }
@@ -189,23 +204,24 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
     cluster_sync_all();
     if (warp >= 2) {
       const int t = threadIdx.x - 64;
-      const int U = a.BN * BM / 4;
+      constexpr int RW = BM * RT / 4;  // float4 units per partial-tile column
+      const int U = a.BN * RW;
       const int u0 = (int)((int64_t)rank * U / S), u1 = (int)((int64_t)(rank + 1) * U / S);
-      for (int u = u0 + t; u < u1; u += 128) {
+      for (int u = u0 + t; u < u1; u += 128 * RT) {
         const uint32_t la = sA + (uint32_t)u * 16;
         float4 v = ld_cluster_f4(la, 0);
         for (int p = 1; p < S; ++p) {
           const float4 w = ld_cluster_f4(la, (uint32_t)p);
           v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
         }
-        const int n = u >> 5, r4 = (u & 31) * 4;
+        const int n = u / RW, r4 = (u - n * RW) * 4;
         const int64_t ng = n0 + n;
         if (ng < a.N) {
           raw_t* yp = (raw_t*)a.Y + ng * a.ldy + m0 + r4;
           const float f[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (r4 + e < mt) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
+            if (r4 + e < mrows) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
         }
       }
     }
@@ -216,6 +232,160 @@ __global__ void __launch_bounds__(kThreads, 1) spmm24_kernel(const __grid_consta
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
+  }
+}
+
+// CTA pair (cta_group::2, cluster of 2, S = 1): M = 256 rows per pair, 128 per CTA (its compressed A rows
+// and their metadata in its own shared and tensor memory), N_t = BN <= 256 batch columns, BN / 2 X rows per
+// CTA. The leader (rank 0) issues tcgen05.mma.sp.cta_group::2 (M = 256, N = BN, K = 32), which reads both
+// CTAs' operands and accumulates each CTA's 128 rows in its own TMEM. Both CTAs' TMA copies complete on the
+// leader's full barrier; the peer's metadata threads arrive on the leader's meta barrier; the MMA commits
+// multicast to both CTAs' empty / acc barriers. X traffic from L2 is half of the single-CTA M = 128 tile's.
+template <int DT>
+__global__ void __launch_bounds__(192, 1) spmm24_pair_kernel(const __grid_constant__ CUtensorMap tA,
+                                                             const __grid_constant__ CUtensorMap tX, Sp24Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[3 * kMaxStages + 1];
+  using raw_t = uint16_t;
+  __shared__ uint32_t tmem_holder;
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int BNh = a.BN / 2;
+  const uint32_t ASZ = BM * 128;                 // compressed A chunk: 128 rows × 128 B
+  const uint32_t BSZ = 2u * (uint32_t)BNh * 128;  // this CTA's X chunk: 2 atoms of BN/2 rows × 128 B
+  const int NST = a.NST;
+  const uint32_t sA = smem_u32(smem), sB = sA + NST * ASZ;
+  const uint32_t full = smem_u32(&bars[0]), empty = smem_u32(&bars[kMaxStages]);
+  const uint32_t meta_ok = smem_u32(&bars[2 * kMaxStages]), acc_full = smem_u32(&bars[3 * kMaxStages]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_rank();  // 0: leader
+  const int64_t pt = a.colfast ? blockIdx.y : blockIdx.x >> 1;
+  const int64_t ct = a.colfast ? blockIdx.x >> 1 : blockIdx.y;
+  const int64_t m0 = pt * (2 * BM) + rank * BM;  // this CTA's rows
+  const int64_t mt = (a.M - m0) < BM ? (a.M - m0) : BM;  // may be <= 0 (the pair's second half past M)
+  const int64_t n0 = ct * a.BN;
+  const int nloc = a.NC;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full + 8 * s, 2);        // leader: its arrive.expect_tx + the peer's arrive
+      mbar_init(empty + 8 * s, 1);       // one multicast commit
+      mbar_init(meta_ok + 8 * s, 8);     // leader: both CTAs' metadata warps
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tX) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_holder)),
+                 "r"(a.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();  // both CTAs' barriers are initialised before any remote arrive
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const uint32_t tmem = tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs): copies complete on the leader's full barrier
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nloc; ++i) {
+        if (i >= NST) mbar_wait(empty + 8 * s, ph ^ 1u);
+        const uint32_t lf = mapa_u32(full + 8 * s, 0);
+        if (rank == 0) mbar_expect_tx(full + 8 * s, 2u * (ASZ + BSZ));
+        else mbar_arrive_cluster(lf);
+        tma_2d_pair(sA + s * ASZ, &tA, i * (KCH / 2), (int)m0, lf);
+        tma_2d_pair(sB + s * BSZ, &tX, i * KCH, (int)(n0 + rank * BNh), lf);
+        tma_2d_pair(sB + s * BSZ + (uint32_t)BNh * 128, &tX, i * KCH + 64, (int)(n0 + rank * BNh), lf);
+        if (++s == NST) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---- sparse MMA issuer (leader)
+      int s = 0;
+      uint32_t par = 0;
+      for (int i = 0; i < nloc; ++i) {
+        mbar_wait(full + 8 * s, par);
+        mbar_wait(meta_ok + 8 * s, par);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint64_t da = sw128_desc(sA + s * ASZ);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t db = sw128_desc(sB + s * BSZ + (uint32_t)(j >> 1) * (uint32_t)BNh * 128) + (uint64_t)((j & 1) * 4);
+          const uint32_t te = tmem + (uint32_t)a.meta_col + (uint32_t)((s * 4 + j) * a.mstride);
+          const uint32_t acc = (i > 0 || j > 0) ? 1u : 0u;
+          asm volatile(
+              "{ .reg .pred p; setp.ne.b32 p, %5, 0;\n\t"
+              "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%3], %4, p; }" ::"r"(tmem),
+              "l"(da + (uint64_t)(j * 2)), "l"(db), "r"(te), "r"(a.idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(empty + 8 * s),
+                     "h"((uint16_t)3)
+                     : "memory");
+        if (++s == NST) { s = 0; par ^= 1u; }
+      }
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(acc_full),
+                   "h"((uint16_t)3)
+                   : "memory");
+    }
+  } else {
+    // ---- metadata → this CTA's tensor memory (thread = row), as in spmm24_kernel; then the epilogue
+    const int q = warp & 3;
+    const int64_t row = 32 * q + lane;
+    const uint8_t* mrow = a.meta + (m0 + row) * (a.K / 8);
+    auto ldm = [&](int i) {
+      return (row < mt && i < nloc) ? __ldg((const uint4*)(mrow + (int64_t)i * 16)) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    const uint32_t lm = mapa_u32(meta_ok, 0);
+    uint4 m_cur = ldm(0), m_nxt = ldm(1);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nloc; ++i) {
+      if (i >= NST) mbar_wait(empty + 8 * s, ph ^ 1u);
+      const uint4 m = m_cur;
+      m_cur = m_nxt;
+      m_nxt = ldm(i + 2);
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)a.meta_col + (uint32_t)(s * 4 * a.mstride);
+      const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t oth = __shfl_xor_sync(0xffffffffu, mw[j], 8);
+        const uint32_t w = (lane & 8) ? ((oth >> 16) | (mw[j] & 0xFFFF0000u)) : ((mw[j] & 0xFFFFu) | (oth << 16));
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr + (uint32_t)(j * a.mstride)),
+                     "r"(w)
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(lm + 8u * (uint32_t)s);
+      if (++s == NST) { s = 0; ph ^= 1u; }
+    }
+    mbar_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    for (int nb = 0; nb < a.BN; nb += 8) {
+      uint32_t r[8];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)nb));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < mt) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int64_t ng = n0 + nb + e;
+          if (ng < a.N) ((raw_t*)a.Y)[ng * a.ldy + m0 + row] = (raw_t)bsk::from_float<DT>(__uint_as_float(r[e]));
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();  // the leader's MMAs have read the peer's shared memory; both TMEM halves are drained
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
   }
 }
 
@@ -300,61 +470,90 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
     return v >= 256 ? 256 : 128;
   }();
   if (BN > bn_max) BN = bn_max;  // 128 keeps a 4-stage ring; 256 leaves 2 stages
+  const int64_t tiles = (g.M + BM - 1) / BM;
+  // RT = 2 (two row tiles per CTA sharing each X tile) when the layer has enough row tiles and enough
+  // columns that X traffic matters: A/B in DESIGN.md §4 K5. BS_K5_RT forces 1 or 2. BN <= 128 (TMEM:
+  // two accumulators + metadata).
+  static const int rt_env = [] {
+    const char* e = getenv("BS_K5_RT");
+    return e && e[0] ? atoi(e) : 0;
+  }();
+  int RT = rt_env == 1 || rt_env == 2 ? rt_env : ((tiles >= 64 && N > 64) ? 2 : 1);
+  if (RT == 2 && BN > 128) BN = 128;
+  // CTA pairs (M = 256 per pair, BN <= 256) whenever split-K is off (S = 1: >= 75 row tiles on 148 SMs);
+  // bit-identical to the single-CTA kernel (tools/k5_pair_check.py, test_k5_pair_*). BS_K5_PAIR=0: off.
+  static const int pair_env = [] {
+    const char* e = getenv("BS_K5_PAIR");
+    return e && e[0] ? atoi(e) : 1;
+  }();
+  const bool pair = pair_env == 1 && bsk::dev_props().sms / tiles <= 1;
+  if (pair) {
+    RT = 1;
+    BN = (int)((N + 31) / 32 * 32);
+    if (BN > 256) BN = 256;
+  }
   CUtensorMap tA, tX;
   const uint8_t* base = (const uint8_t*)packed;
   if (!bsk_make_map_2d(&tA, DT, base + g.offA, g.K / 2, g.M, g.K / 2, 64, BM)) return cudaErrorNotSupported;
-  if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, 64, BN)) return cudaErrorNotSupported;
+  if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, 64, pair ? BN / 2 : BN)) return cudaErrorNotSupported;
   Sp24Args a;
   a.meta = base + g.offB;
   a.Y = Y;
   a.M = g.M; a.K = g.K; a.N = N; a.ldy = ldy;
   a.BN = BN;
   a.NC = (int)(g.K / KCH);
-  a.idesc = idesc_f16(DT == BS_BF16, BM, BN, true);
+  a.idesc = idesc_f16(DT == BS_BF16, pair ? 2 * BM : BM, BN, true);
   a.mstride = 4;  // the metadata address of each K = 32 step must be 4-column aligned (stride 1 faults)
   int p2 = 32;
   while (p2 < BN) p2 <<= 1;
-  int mcols = 16 * a.mstride;
-  int tot = p2 + mcols;
+  a.acc_stride = p2;
+  const int tot = RT * (p2 + kMetaCols);
   int cols = 32;
   while (cols < tot) cols <<= 1;
-  a.meta_col = p2;
+  a.meta_col = RT * p2;
   a.tmem_cols = cols;
   if (a.tmem_cols > 512) return cudaErrorNotSupported;
-  const int64_t stage = BM * 128 + 2LL * BN * 128;
+  const int64_t stage = (int64_t)RT * BM * 128 + 2LL * (pair ? BN / 2 : BN) * 128;
   int64_t nst = (bsk::dev_props().smem_optin - 2048) / stage;
   if (nst > kMaxStages) nst = kMaxStages;
   if (nst < 2) return cudaErrorNotSupported;
   a.NST = (int)nst;
   const int64_t smem = 1024 + nst * stage;
-  const int64_t tiles = (g.M + BM - 1) / BM;
-  int64_t S = bsk::dev_props().sms / tiles;  // split-K: from M and K only (never N)
+  int64_t S = bsk::dev_props().sms / tiles;  // split-K: from M and K only (never N, never RT)
   if (S > 8) S = 8;
   // 6: a deeper split helped N <= 128 by 7% but cost 60% at N = 256 (A/B on CTC W_ih)
   const int mc = bsk::splitk_min_chunks(6);
   if (S > a.NC / mc) S = a.NC / mc;  // at least mc chunks per CTA: fixed costs stay amortised
   if (S < 1) S = 1;
   a.S = (int)S;
-  auto kern = spmm24_kernel<DT>;
+  if (S > 1 && (int64_t)BN * BM * RT * 4 > nst * stage) return cudaErrorNotSupported;  // partial tile must fit
+  if (pair) a.S = (int)(S = 1);
+  const void* kern = pair ? (const void*)spmm24_pair_kernel<DT>
+                          : RT == 2 ? (const void*)spmm24_kernel<DT, 2> : (const void*)spmm24_kernel<DT, 1>;
   cudaError_t perr = cudaSuccess;
-  const int static_smem = bsk::prepare_func((const void*)kern, &perr);
+  const int static_smem = bsk::prepare_func(kern, &perr);
   if (static_smem < 0) return perr;
   if (smem > bsk::dev_props().smem_optin - static_smem) return cudaErrorNotSupported;
+  const int64_t ctiles = pair ? (g.M + 2 * BM - 1) / (2 * BM) : (g.M + BM * RT - 1) / (BM * RT);
+  const unsigned cl = pair ? 2u : (unsigned)S;  // cluster size along x
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(tiles * S), (unsigned)((N + BN - 1) / BN));
-  cfg.blockDim = dim3(kThreads);
+  a.colfast = bsk::tc_cols_fast() && ctiles <= 65535;
+  const unsigned nct = (unsigned)((N + BN - 1) / BN);
+  cfg.gridDim = a.colfast ? dim3(nct * cl, (unsigned)ctiles) : dim3((unsigned)ctiles * cl, nct);
+  cfg.blockDim = dim3(pair ? 192 : 64 + 128 * RT);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.x = cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, kern, tA, tX, a);
+  void* args[] = {(void*)&tA, (void*)&tX, (void*)&a};
+  return cudaLaunchKernelExC(&cfg, kern, args);
 }
 
 template <int DT>

@@ -157,6 +157,70 @@ def test_sp24_single_column_slices(bs, dname):
         assert torch.equal(bs.spmm(A, X[n0:n1].contiguous()), Y[n0:n1]), (n0, n1)
 
 
+@pytest.mark.parametrize("M,K", [(8192 + 200, 1536),   # RT = 2, split-K S = 2, a partial second row tile
+                                 (8192 + 64, 1024)])   # RT = 2, S = 1, the last CTA has one live row tile
+def test_k5_two_row_tiles_integer_exact(bs, M, K):
+    """Layers with >= 64 row tiles and N > 64 run two row tiles per CTA (RT = 2, sharing each X tile):
+    bit-exact against the oracle on integer-exact data."""
+    A, ov, oi = _setup(bs, M, K, 4, 2, "f16", synth.seed_for(30, M), "sp24")
+    X = synth.vector(K, "f16", family="intexact", seed=synth.seed_for(30, K), n=80)
+    _exact(bs, A, ov, oi, "f16", X)
+
+
+@pytest.mark.parametrize("dname", ["f16", "bf16"])
+def test_k5_two_row_tiles_match_one(bs, dname):
+    """RT = 2 (N > 64) and RT = 1 (N <= 64) sum every row in the same MMA sequence: the first 64 columns of
+    an 80-column product equal the 64-column product bit for bit (Gaussian data), as do one-column slices."""
+    M, K = 8192 + 128, 2048
+    W = synth.matrix(M, K, dname, seed=synth.seed_for(31, 0)).cuda()
+    vals, idx, _ = bs.prune(W, 4, k=2)
+    A = bs.pack(vals, idx, K, 4, layout="sp24")
+    X = synth.vector(K, dname, seed=synth.seed_for(31, 1), n=80).cuda()
+    Y = bs.spmm(A, X)
+    assert torch.equal(bs.spmm(A, X[:64].contiguous()), Y[:64])
+    assert torch.equal(bs.spmm(A, X[79:80].contiguous()), Y[79:80])
+
+
+@pytest.mark.parametrize("M,K,N", [(9600 + 100, 1024, 40),   # CTA pairs, the last pair's second CTA half empty
+                                   (9728, 1536, 200),        # BN = 224 split 112 + 112 between the pair
+                                   (9600, 1024, 1)])
+def test_k5_pair_integer_exact(bs, M, K, N):
+    """>= 75 row tiles (split-K S = 1): K5 runs as CTA pairs (cta_group::2, M = 256). Bit-exact against
+    the oracle on integer-exact data."""
+    A, ov, oi = _setup(bs, M, K, 4, 2, "f16", synth.seed_for(32, M + N), "sp24")
+    X = synth.vector(K, "f16", family="intexact", seed=synth.seed_for(32, K + N), n=N)
+    _exact(bs, A, ov, oi, "f16", X)
+
+
+_PAIR_CHILD = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1811_00206_b200 as bs, synth
+M, K, N = 9728, 2048, 96
+W = synth.matrix(M, K, "bf16", seed=synth.seed_for(33, 0)).cuda()
+v, i, _ = bs.prune(W, 4, k=2)
+A = bs.pack(v, i, K, 4, layout="sp24")
+X = synth.vector(K, "bf16", seed=synth.seed_for(33, 1), n=N).cuda()
+torch.save(bs.spmm(A, X).cpu(), sys.argv[2])
+"""
+
+
+def test_k5_pair_matches_single_cta(tmp_path):
+    """The CTA-pair kernel (M = 256 per pair) and the single-CTA kernel (BS_K5_PAIR=0, M = 128 per CTA)
+    give bit-identical Y on Gaussian data: each row is the same sequence of K = 32 sparse MMAs."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for pair in ("1", "0"):
+        f = str(tmp_path / f"y{pair}.pt")
+        env = dict(os.environ, BS_K5_PAIR=pair)
+        subprocess.run([sys.executable, "-c", _PAIR_CHILD, root, f], env=env, check=True, timeout=300)
+        outs.append(torch.load(f))
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_sp24_integer_exact_single_column(bs):
     M, K = 300, 1024
     A, ov, oi = _setup(bs, M, K, 4, 2, "bf16", synth.seed_for(27, 0), "sp24")
