@@ -600,11 +600,14 @@ def spmm_rows(a, bs, hbm_peak, l2):
     rows = []
     dev = torch.device("cuda")
     tc_peak = tensor_peak()
-    shapes = [("cfgX paper benchmark 16384x8192 (P:240, 8196 read as 8192)", 16384, 8192, [0.9], [1, 8]),
-              ("configs[2] VGG fc6 4096x25088", 4096, 25088, [0.9], [32]),
-              ("configs[2] VGG fc7 4096x4096", 4096, 4096, [0.5, 0.9], [32]),
-              ("configs[3] CTC W_ih 4096x2048", 4096, 2048, [0.875], [1, 2, 4, 8, 16, 32, 64, 128, 256]),
-              ("configs[3] CTC W_hh 4096x1024", 4096, 1024, [0.875], [8, 64, 256])]
+    # (name, M, K, balanced sparsities, batch sizes, batch sizes of the 2:4 variant of the same layer)
+    shapes = [("cfgX paper benchmark 16384x8192 (P:240, 8196 read as 8192)", 16384, 8192, [0.9], [1, 8], [8, 256]),
+              ("configs[2] VGG fc6 4096x25088", 4096, 25088, [0.9], [32], []),
+              ("configs[2] VGG fc7 4096x4096", 4096, 4096, [0.5, 0.9], [32], []),
+              ("configs[3] CTC W_ih 4096x2048", 4096, 2048, [0.875], [1, 2, 4, 8, 16, 32, 64, 128, 256],
+               [1, 2, 4, 8, 16, 32, 64, 128, 256]),
+              ("configs[3] CTC W_hh 4096x1024", 4096, 1024, [0.875], [8, 64, 256], []),
+              ("2:4 at scale 16384x16384 (K5 CTA pairs)", 16384, 16384, [], [], [128, 1024])]
 
     def timed(mats, X, Y):
         C = len(mats)
@@ -615,17 +618,17 @@ def spmm_rows(a, bs, hbm_peak, l2):
         dens = [Wbs] + [Wbs.clone() for _ in range(Cd - 1)]
         return graph_time_us(lambda j: torch.matmul(X, dens[j % Cd].t()), 4 * Cd)
 
-    for name, M, K, sps, Ns in shapes:
+    for name, M, K, sps, Ns, Ns24 in shapes:
         W = synth.matrix(M, K, a.dtype, seed=synth.seed_for(3, M + K), device=dev)
         variants = []
         for s in sps:
             ks = bs.k_from_sparsity(a.block, s)
             v, i, _ = bs.prune(W, a.block, k=ks)
-            variants.append((f"B={a.block} s={s}", a.block, ks, v, i, {"K4": "spmv", "K6": "spmm"}))
-        if "CTC W_ih" in name:  # the 2:4 shape (B = 4, 50%) of the same layer
+            variants.append((f"B={a.block} s={s}", a.block, ks, v, i, {"K4": "spmv", "K6": "spmm"}, Ns))
+        if Ns24:  # the 2:4 shape (B = 4, 50%) of the same layer
             v, i, _ = bs.prune(W, 4, k=2)
-            variants.append(("2:4 (B=4 s=0.5)", 4, 2, v, i, {"K5": "sp24"}))
-        for label, B, ks, v, i, paths in variants:
+            variants.append(("2:4 (B=4 s=0.5)", 4, 2, v, i, {"K5": "sp24"}, Ns24))
+        for label, B, ks, v, i, paths, Ns in variants:
             Wbs = dense_from_canonical(v, i, M, K, B)
             packed = {kn: rotating(bs, bs.pack(v, i, K, B, layout=lay), l2) for kn, lay in paths.items()}
             for N in Ns:

@@ -23,8 +23,7 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int KCH = 128;  // original columns per chunk (64 compressed values: one 128-byte swizzle atom)
-constexpr int kMaxStages = 4;  // pipeline stages (runtime NST: 2..4, fewer for BN = 256 or RT = 2)
-constexpr int kMetaCols = 16 * 4;  // TMEM metadata columns per row tile: kMaxStages × 4 K-steps × mstride 4
+constexpr int kMaxStages = 8;  // pipeline stages (runtime NST: as many as shared memory holds, 2..8)
 
 struct Sp24Args {
   const uint8_t* meta;  // M × K/8 bytes
@@ -35,6 +34,7 @@ struct Sp24Args {
   int NST;              // pipeline stages
   uint32_t idesc;
   int tmem_cols, meta_col, acc_stride;  // allocated TMEM columns; first metadata column; columns per accumulator
+  int meta_cols;        // TMEM metadata columns per row tile: NST stages × 4 K-steps × mstride
   int mstride;          // TMEM columns between the metadata of consecutive K = 32 steps
   int colfast;          // grid order (bsk::tc_cols_fast)
 };
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
             for (int j = 0; j < 4; ++j) {
               // A: 16 compressed values (32 B) per K = 32 step; B: 32 columns (64 B) per step, atom j / 2
               const uint64_t db = sw128_desc(sB + s * BSZ + (uint32_t)(j >> 1) * (uint32_t)a.BN * 128) + (uint64_t)((j & 1) * 4);
-              const uint32_t te = tmem + (uint32_t)(a.meta_col + t * kMetaCols) + (uint32_t)((s * 4 + j) * a.mstride);
+              const uint32_t te = tmem + (uint32_t)(a.meta_col + t * a.meta_cols) + (uint32_t)((s * 4 + j) * a.mstride);
               const uint32_t acc = (i > 0 || j > 0) ? 1u : 0u;
               asm volatile(
                   "{ .reg .pred p; setp.ne.b32 p, %5, 0;\n\t"
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
       const uint4 m = m_cur;
       m_cur = m_nxt;
       m_nxt = ldm(i + 2);
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a.meta_col + t * kMetaCols) + (uint32_t)(s * 4 * a.mstride);
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a.meta_col + t * a.meta_cols) + (uint32_t)(s * 4 * a.mstride);
       const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -507,17 +507,23 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   int p2 = 32;
   while (p2 < BN) p2 <<= 1;
   a.acc_stride = p2;
-  const int tot = RT * (p2 + kMetaCols);
+  const int64_t stage = (int64_t)RT * BM * 128 + 2LL * (pair ? BN / 2 : BN) * 128;
+  int64_t nst = (bsk::dev_props().smem_optin - 2048) / stage;
+  static const int st_env = [] {  // BS_K5_STAGES: cap on the ring depth (A/B)
+    const char* e = getenv("BS_K5_STAGES");
+    return e && e[0] ? atoi(e) : kMaxStages;
+  }();
+  if (nst > st_env) nst = st_env;
+  if (nst > kMaxStages) nst = kMaxStages;
+  if (nst < 2) return cudaErrorNotSupported;
+  a.NST = (int)nst;
+  a.meta_cols = (int)nst * 4 * a.mstride;
+  const int tot = RT * (p2 + a.meta_cols);
   int cols = 32;
   while (cols < tot) cols <<= 1;
   a.meta_col = RT * p2;
   a.tmem_cols = cols;
   if (a.tmem_cols > 512) return cudaErrorNotSupported;
-  const int64_t stage = (int64_t)RT * BM * 128 + 2LL * (pair ? BN / 2 : BN) * 128;
-  int64_t nst = (bsk::dev_props().smem_optin - 2048) / stage;
-  if (nst > kMaxStages) nst = kMaxStages;
-  if (nst < 2) return cudaErrorNotSupported;
-  a.NST = (int)nst;
   const int64_t smem = 1024 + nst * stage;
   int64_t S = bsk::dev_props().sms / tiles;  // split-K: from M and K only (never N, never RT)
   if (S > 8) S = 8;
