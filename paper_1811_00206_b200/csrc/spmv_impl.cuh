@@ -942,12 +942,16 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 1)) spmv_rows_ke
           }
         }
     }
-    for (int64_t s0 = 0; s0 < S; s0 += G) {
+    // 32-bit index math (x has K < 2^31 elements): the gather column of entry (p, v) of ring lane L is
+    // (p·P + 32·v + L)·B + o = p·PB + v·B32 + L·B + o; the panel of step s0 + g follows from one division
+    // per group (round 1's 64-bit division per step made ALU the busiest pipe: ncu, PTB).
+    const uint32_t Bu = (uint32_t)B, B32 = 32u * Bu, PB = (uint32_t)P * Bu;
+    for (int s0 = 0; s0 < (int)S; s0 += G) {
       uint32_t wv[G][NJ][WW], iv[G][NJ][IW];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        if (live && s0 + g < S) {
-          const uint8_t* st = rowA + (s0 + g) * STEPB;
+        if (live && s0 + g < (int)S) {
+          const uint8_t* st = rowA + (int64_t)(s0 + g) * STEPB;
 #pragma unroll
           for (int j = 0; j < NJ; ++j) {
             const int L = hl + 16 * j;
@@ -975,12 +979,13 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 1)) spmv_rows_ke
         pdl_wait();
         waited = true;
       }
+      uint32_t p = (uint32_t)s0 / (uint32_t)k, t = (uint32_t)s0 - p * (uint32_t)k;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        if (live && s0 + g < S) {
-          const int64_t p = (s0 + g) / k;
+        if (live && s0 + g < (int)S) {
 #pragma unroll
-          for (int j = 0; j < NJ; ++j)
+          for (int j = 0; j < NJ; ++j) {
+            const uint32_t cb = p * PB + (uint32_t)(hl + 16 * j) * Bu;
 #pragma unroll
             for (int v = 0; v < V; ++v) {
               const uint32_t w = ES == 2 ? (wv[g][j][v >> 1] >> (16 * (v & 1))) & 0xffffu : wv[g][j][v];
@@ -988,9 +993,13 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 1)) spmv_rows_ke
               if constexpr (IS == 5) o = (v < 7 ? __funnelshift_r(iv[g][j][0], iv[g][j][1], 5 * v) : iv[g][j][1] >> 3) & 31u;
               else if constexpr (IS == 1) o = byte_of(iv[g][j][v >> 2], v & 3);
               else o = (iv[g][j][v >> 1] >> (16 * (v & 1))) & 0xffffu;
-              const int64_t b = p * P + v * 32 + hl + 16 * j;
-              bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + b * B + o));
+              bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + (cb + (uint32_t)v * B32 + o)));
             }
+          }
+        }
+        if (++t == (uint32_t)k) {
+          t = 0;
+          ++p;
         }
       }
     }
@@ -1011,10 +1020,10 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 1)) spmv_rows_ke
             const int tt = q / V, v = q - (q / V) * V;
             const int bl = v * 32 + hl + 16 * j;
             if (live && tt < k && v < Vt && bl < a.T) {
-              const int64_t b = a.NBf * P + bl;
+              const uint32_t cb = ((uint32_t)a.NBf * (uint32_t)P + (uint32_t)bl) * (uint32_t)B;
               const uint32_t w = ES == 2 ? (tw[j][q] & 0xffffu) : tw[j][q];
               const uint32_t o = ES == 2 ? (tw[j][q] >> 16) : to[j][q < TO ? q : 0];
-              bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + b * B + o));
+              bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + (cb + o)));
             }
           }
       }
@@ -1028,8 +1037,8 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 1)) spmv_rows_ke
             if (live && v < Vt && bl < a.T) {
               const uint32_t w = (uint32_t)__ldg(tv + e0 + bl);
               const uint32_t o = ISt == 1 ? (uint32_t)__ldg(ti + e0 + bl) : (uint32_t)__ldg((const uint16_t*)ti + e0 + bl);
-              const int64_t b = a.NBf * P + bl;
-              bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + b * B + o));
+              const uint32_t cb = ((uint32_t)a.NBf * (uint32_t)P + (uint32_t)bl) * (uint32_t)B;
+              bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + (cb + o)));
             }
           }
       }
