@@ -110,7 +110,7 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
   {
     static const int64_t thr = [] {
       const char* e = getenv("BS_DIRECT_ROW_BYTES");
-      return e && e[0] ? (int64_t)atoll(e) : (int64_t)2048;
+      return e && e[0] ? (int64_t)atoll(e) : (int64_t)2304;  // 2304: fc6 at 97 % (2064 B) 7.1 -> 6.4 us
     }();
     const int ist = g.ri == g.P * g.is ? g.is : 1;
     const int64_t row_bytes = g.NBf * g.k * (g.P * g.es + g.ri) + (int64_t)g.k * g.T * (g.es + ist);

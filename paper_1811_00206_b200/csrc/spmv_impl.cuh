@@ -868,7 +868,7 @@ __device__ __forceinline__ float row_total(float (&acc)[NJ][V]) {
 }
 
 template <int DT, int V, int IS, bool TP, bool HW>
-__global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 1)) spmv_rows_kernel(SpmvArgs a) {
+__global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_kernel(SpmvArgs a) {
   using raw_t = typename bsk::DTraits<DT>::raw_t;
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int P = 32 * V;
