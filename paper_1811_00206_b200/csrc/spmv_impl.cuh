@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
 // butterfly's xor-16 step, and xor 8, 4, 2, 1 follow within the half: the same sums in the same order.
 template <int V, int NJ>
 __device__ __forceinline__ float row_total(float (&acc)[NJ][V]) {
-  float t = 0.f;
+  float sj[NJ];
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     float s = acc[j][0];
@@ -860,15 +860,18 @@ __device__ __forceinline__ float row_total(float (&acc)[NJ][V]) {
     for (int v = 1; v < V; ++v) s += acc[j][v];
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[j][v] = 0.f;
-    t = j == 0 ? s : t + s;
+    sj[j] = s;
   }
+  float t = sj[0];
+  if constexpr (NJ == 2) t = sj[0] + sj[1];
 #pragma unroll
-  for (int o = NJ == 2 ? 8 : 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  for (int o = 16 / NJ; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   return t;
 }
 
-template <int DT, int V, int IS, bool TP, bool HW>
-__global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_kernel(SpmvArgs a) {
+template <int DT, int V, int IS, bool TP, int NJ>
+__global__ void __launch_bounds__(256, (V <= 4 ? (NJ == 2 ? 3 : 4) : 2)) spmv_rows_kernel(SpmvArgs a) {
+  constexpr bool HW = NJ > 1;
   using raw_t = typename bsk::DTraits<DT>::raw_t;
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int P = 32 * V;
@@ -878,10 +881,10 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_ke
   constexpr int G = HW ? 3 : 4;                          // steps per load group (HW: registers for two lanes)
   constexpr int WW = (V * ES + 3) / 4;                   // value words per lane and step
   constexpr int IW = IS == 5 ? 2 : (V * IS + 3) / 4;     // index words per lane and step
-  constexpr int NJ = HW ? 2 : 1;                         // ring-kernel lanes played by one lane
   const int lane = threadIdx.x & 31;
-  const int sub = HW ? (lane >> 4) : 0;                  // HW: which row of the warp's pair
-  const int hl = HW ? (lane & 15) : lane;                // ring-kernel lane of j = 0 (j = 1: hl + 16)
+  constexpr int LPR = 32 / NJ;                           // lanes per row; lane hl plays ring lanes hl + LPR·j
+  const int sub = lane / LPR;                            // which row of the warp's NJ rows
+  const int hl = lane % LPR;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   pdl_launch_dependents();
   bool waited = !a.w_early;
@@ -899,7 +902,7 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_ke
   constexpr int TO = ES == 2 ? 1 : TM;
   for (int64_t r0 = ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * NJ; r0 < a.M; r0 += nwarps * NJ) {
     const int64_t r = r0 + sub;
-    const bool live = !HW || r < a.M;  // HW: the warp's second row may not exist (the shuffles still need the lanes)
+    const bool live = !HW || r < a.M;  // NJ > 1: the warp's last rows may not exist (the shuffles still need the lanes)
     float acc[NJ][V];
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
@@ -928,7 +931,7 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_ke
 #pragma unroll
         for (int q = 0; q < TM; ++q) {
           const int tt = q / V, v = q - (q / V) * V;  // entry q = (tt, v)
-          const int bl = v * 32 + hl + 16 * j;
+          const int bl = v * 32 + hl + LPR * j;
           tw[j][q] = 0u;
           if constexpr (ES != 2) to[j][q] = 0u;
           if (live && tt < k && v < Vt && bl < a.T) {
@@ -954,7 +957,7 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_ke
           const uint8_t* st = rowA + (int64_t)(s0 + g) * STEPB;
 #pragma unroll
           for (int j = 0; j < NJ; ++j) {
-            const int L = hl + 16 * j;
+            const int L = hl + LPR * j;
             bsk::Vec<V * ES> vv;
             vv.load(st + L * (V * ES));
 #pragma unroll
@@ -985,7 +988,7 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_ke
         if (live && s0 + g < (int)S) {
 #pragma unroll
           for (int j = 0; j < NJ; ++j) {
-            const uint32_t cb = p * PB + (uint32_t)(hl + 16 * j) * Bu;
+            const uint32_t cb = p * PB + (uint32_t)(hl + LPR * j) * Bu;
 #pragma unroll
             for (int v = 0; v < V; ++v) {
               const uint32_t w = ES == 2 ? (wv[g][j][v >> 1] >> (16 * (v & 1))) & 0xffffu : wv[g][j][v];
@@ -1018,7 +1021,7 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_ke
 #pragma unroll
           for (int q = 0; q < TM; ++q) {
             const int tt = q / V, v = q - (q / V) * V;
-            const int bl = v * 32 + hl + 16 * j;
+            const int bl = v * 32 + hl + LPR * j;
             if (live && tt < k && v < Vt && bl < a.T) {
               const uint32_t cb = ((uint32_t)a.NBf * (uint32_t)P + (uint32_t)bl) * (uint32_t)B;
               const uint32_t w = ES == 2 ? (tw[j][q] & 0xffffu) : tw[j][q];
@@ -1033,7 +1036,7 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_ke
         for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int v = 0; v < V; ++v) {
-            const int bl = v * 32 + hl + 16 * j;
+            const int bl = v * 32 + hl + LPR * j;
             if (live && v < Vt && bl < a.T) {
               const uint32_t w = (uint32_t)__ldg(tv + e0 + bl);
               const uint32_t o = ISt == 1 ? (uint32_t)__ldg(ti + e0 + bl) : (uint32_t)__ldg((const uint16_t*)ti + e0 + bl);
@@ -1056,21 +1059,20 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (HW ? 3 : 4) : 2)) spmv_rows_ke
   if (!waited) pdl_wait();
 }
 
-template <int DT, int V, int IS, bool HW>
+template <int DT, int V, int IS, int NJ>
 const void* rows_fn(const SpmvArgs& a) {
-  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return (const void*)spmv_rows_kernel<DT, V, IS, true, HW>;
-  return (const void*)spmv_rows_kernel<DT, V, IS, false, HW>;
+  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return (const void*)spmv_rows_kernel<DT, V, IS, true, NJ>;
+  return (const void*)spmv_rows_kernel<DT, V, IS, false, NJ>;
 }
 
-template <int DT, int V, int IS, bool HW>
+template <int DT, int V, int IS, int NJ>
 cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
   SpmvArgs a = a0;
   if (!a.pdl) a.w_early = 0;
   const auto& dp = bsk::dev_props();
   // one resident wave of warps (occupancy query): a warp with a second row keeps running (no CTA launch
   // in between) and finds that row's lines already in L2
-  constexpr int NJ = HW ? 2 : 1;
-  const int per_sm = bsk::resident_ctas(rows_fn<DT, V, IS, HW>(a), 256);
+  const int per_sm = bsk::resident_ctas(rows_fn<DT, V, IS, NJ>(a), 256);
   const int64_t cap = (int64_t)(per_sm > 0 ? per_sm : 1) * dp.sms * 8;
   const int64_t need = (a.M + NJ - 1) / NJ;
   const int64_t warps = need < cap ? need : cap;
@@ -1085,8 +1087,8 @@ cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = a.pdl ? 1 : 0;
-  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, true, HW>, a);
-  return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, false, HW>, a);
+  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, true, NJ>, a);
+  return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, false, NJ>, a);
 }
 
 // The direct kernel pays off while every row gets its own resident warp (one wave): a second wave adds
@@ -1096,7 +1098,7 @@ cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
 // may depend on M. Returns 0 (ring kernel), 1 (warp rows) or 2 (half-warp rows).
 template <int DT, int V, int IS>
 int rows_mode(const SpmvArgs& a) {
-  const int per_sm = bsk::resident_ctas(rows_fn<DT, V, IS, false>(a), 256);
+  const int per_sm = bsk::resident_ctas(rows_fn<DT, V, IS, 1>(a), 256);
   const int64_t wave = (int64_t)per_sm * bsk::dev_props().sms * 8;
   if (per_sm > 0 && a.M <= wave) return 1;
   static const int half = [] {  // BS_DIRECT_HALF=0: no half-warp rows (A/B)
@@ -1105,7 +1107,7 @@ int rows_mode(const SpmvArgs& a) {
   }();
   if constexpr (V <= 4) {
     if (half) {
-      const int ph = bsk::resident_ctas(rows_fn<DT, V, IS, true>(a), 256);
+      const int ph = bsk::resident_ctas(rows_fn<DT, V, IS, 2>(a), 256);
       if (ph > 0 && a.M <= (int64_t)ph * bsk::dev_props().sms * 16) return 2;
     }
   }
@@ -1122,11 +1124,11 @@ bool try_rows(const SpmvArgs& a, cudaStream_t s, cudaError_t* e) {
   if (m == 0) return false;
   if constexpr (V <= 4) {
     if (m == 2) {
-      *e = launch_rows<DT, V, IS, true>(a, s);
+      *e = launch_rows<DT, V, IS, 2>(a, s);
       return true;
     }
   }
-  *e = launch_rows<DT, V, IS, false>(a, s);
+  *e = launch_rows<DT, V, IS, 1>(a, s);
   return true;
 }
 
