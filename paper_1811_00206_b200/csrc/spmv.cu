@@ -104,8 +104,8 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
     a.tail_in_last = 0;
     a.xbytes = g.k > 0 ? (int)(ev(tail_groups) * group_bytes) : 0;
   }
-  // Short rows take the direct kernel (spmv_impl.cuh spmv_rows_kernel): plain SpMV / fused bias+act, one
-  // x chunk, at most kDirectRowBytes of packed bytes per row (BS_DIRECT_ROW_BYTES overrides; 0 = off).
+  // Short rows take the direct kernel (spmv_impl.cuh spmv_rows_kernel): plain SpMV / fused bias+act / the
+  // LSTM step (half-warp rows, 4 units per CTA round), one x chunk, at most kDirectRowBytes of packed bytes per row (BS_DIRECT_ROW_BYTES overrides; 0 = off).
   // The choice depends on (K, B, k, dtype) only, never on M, and both kernels sum in the same order.
   {
     static const int64_t thr = [] {
@@ -114,7 +114,7 @@ static cudaError_t launch_spmv_nv(const bsk::Geom& g, const void* packed, const 
     }();
     const int ist = g.ri == g.P * g.is ? g.is : 1;
     const int64_t row_bytes = g.NBf * g.k * (g.P * g.es + g.ri) + (int64_t)g.k * g.T * (g.es + ist);
-    a.direct = nv == 1 && lstm == nullptr && ag == nullptr && a.nchunks <= 1 && row_bytes <= thr &&
+    a.direct = nv == 1 && ag == nullptr && a.nchunks <= 1 && row_bytes <= thr &&
                (flags & BS_SPMV_RING) == 0;
   }
   if (a.xbytes > bsk::dev_props().smem_optin - 16 * 1024) return cudaErrorInvalidConfiguration;

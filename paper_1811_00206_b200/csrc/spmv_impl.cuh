@@ -869,9 +869,13 @@ __device__ __forceinline__ float row_total(float (&acc)[NJ][V]) {
   return t;
 }
 
-template <int DT, int V, int IS, bool TP, int NJ>
+// LS (the LSTM step, NJ = 2): a CTA's 8 warps take 16 consecutive gate rows = 4 units per round (the loop
+// is CTA-uniform); each row's z = W·x + (bias + pre) goes to shared memory and, after a CTA barrier, one
+// thread per unit applies the cell with the ring kernel's expressions (bit-identical, test_gpu_lstm.py).
+template <int DT, int V, int IS, bool TP, int NJ, bool LS = false>
 __global__ void __launch_bounds__(256, (V <= 4 ? (NJ == 2 ? 3 : 4) : 2)) spmv_rows_kernel(SpmvArgs a) {
   constexpr bool HW = NJ > 1;
+  static_assert(!LS || NJ == 2, "the LSTM step takes half-warp rows");
   using raw_t = typename bsk::DTraits<DT>::raw_t;
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int P = 32 * V;
@@ -900,9 +904,20 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (NJ == 2 ? 3 : 4) : 2)) spmv_ro
   // layers without a tail. 16-bit values: value | index << 16 in one register per entry.
   constexpr int TM = TP ? 8 : 1;
   constexpr int TO = ES == 2 ? 1 : TM;
-  for (int64_t r0 = ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * NJ; r0 < a.M; r0 += nwarps * NJ) {
+  __shared__ float zs[LS ? 16 : 1];
+  const int64_t first = LS ? (int64_t)blockIdx.x * 8 * NJ : ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * NJ;
+  for (int64_t base = first; base < a.M; base += nwarps * NJ) {
+    const int64_t r0 = LS ? base + (threadIdx.x >> 5) * NJ : base;
     const int64_t r = r0 + sub;
     const bool live = !HW || r < a.M;  // NJ > 1: the warp's last rows may not exist (the shuffles still need the lanes)
+    float bz = 0.f, cp = 0.f;
+    if constexpr (LS) {  // the row's bias + pre and the unit's c_prev, loaded before the W stream
+      if (hl == 0 && live) {
+        bz = a.bias ? bsk::to_float<DT>(__ldg((const raw_t*)a.bias + r)) : 0.f;
+        if (a.pre) bz += bsk::to_float<DT>(__ldg((const raw_t*)a.pre + r));
+      }
+      if (threadIdx.x < 4 && base + 4 * threadIdx.x < a.M) cp = __ldg(a.c_prev + (base / 4 + threadIdx.x));
+    }
     float acc[NJ][V];
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
@@ -1050,6 +1065,20 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (NJ == 2 ? 3 : 4) : 2)) spmv_ro
     } else {
       y = row_total<V, NJ>(acc);  // k == 0: 0
     }
+    if constexpr (LS) {
+      if (hl == 0 && live) zs[(threadIdx.x >> 5) * NJ + sub] = y + bz;
+      __syncthreads();
+      if (threadIdx.x < 4 && base + 4 * threadIdx.x < a.M) {
+        const int u = threadIdx.x;
+        const float zi = zs[4 * u], zf = zs[4 * u + 1], zg = zs[4 * u + 2], zo = zs[4 * u + 3];
+        const int64_t j = base / 4 + u;
+        const float c = apply_act(zf, BS_ACT_SIGMOID) * cp + apply_act(zi, BS_ACT_SIGMOID) * apply_act(zg, BS_ACT_TANH);
+        a.c_out[j] = c;
+        ((raw_t*)a.h_out)[j] = (raw_t)bsk::from_float<DT>(apply_act(zo, BS_ACT_SIGMOID) * apply_act(c, BS_ACT_TANH));
+      }
+      __syncthreads();
+      continue;
+    }
     if (hl == 0 && live) {
       if (a.bias) y += bsk::to_float<DT>(__ldg((const raw_t*)a.bias + r));
       if (a.act) y = apply_act(y, a.act);
@@ -1059,20 +1088,20 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (NJ == 2 ? 3 : 4) : 2)) spmv_ro
   if (!waited) pdl_wait();
 }
 
-template <int DT, int V, int IS, int NJ>
+template <int DT, int V, int IS, int NJ, bool LS = false>
 const void* rows_fn(const SpmvArgs& a) {
-  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return (const void*)spmv_rows_kernel<DT, V, IS, true, NJ>;
-  return (const void*)spmv_rows_kernel<DT, V, IS, false, NJ>;
+  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return (const void*)spmv_rows_kernel<DT, V, IS, true, NJ, LS>;
+  return (const void*)spmv_rows_kernel<DT, V, IS, false, NJ, LS>;
 }
 
-template <int DT, int V, int IS, int NJ>
+template <int DT, int V, int IS, int NJ, bool LS = false>
 cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
   SpmvArgs a = a0;
   if (!a.pdl) a.w_early = 0;
   const auto& dp = bsk::dev_props();
   // one resident wave of warps (occupancy query): a warp with a second row keeps running (no CTA launch
   // in between) and finds that row's lines already in L2
-  const int per_sm = bsk::resident_ctas(rows_fn<DT, V, IS, NJ>(a), 256);
+  const int per_sm = bsk::resident_ctas(rows_fn<DT, V, IS, NJ, LS>(a), 256);
   const int64_t cap = (int64_t)(per_sm > 0 ? per_sm : 1) * dp.sms * 8;
   const int64_t need = (a.M + NJ - 1) / NJ;
   const int64_t warps = need < cap ? need : cap;
@@ -1087,8 +1116,8 @@ cudaError_t launch_rows(const SpmvArgs& a0, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = a.pdl ? 1 : 0;
-  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, true, NJ>, a);
-  return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, false, NJ>, a);
+  if (a.T > 0 && a.k > 0 && a.k * V <= 8) return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, true, NJ, LS>, a);
+  return cudaLaunchKernelEx(&cfg, spmv_rows_kernel<DT, V, IS, false, NJ, LS>, a);
 }
 
 // The direct kernel pays off while every row gets its own resident warp (one wave): a second wave adds
@@ -1120,6 +1149,13 @@ int rows_mode(const SpmvArgs& a) {
 
 template <int DT, int V, int IS>
 bool try_rows(const SpmvArgs& a, cudaStream_t s, cudaError_t* e) {
+  if (a.lstm) {  // the LSTM step: half-warp rows, 16-bit values, u8 indices, V <= 4; else the ring kernel
+    if constexpr (DT != BS_F32 && IS == 1 && V <= 4) {
+      *e = launch_rows<DT, V, IS, 2, true>(a, s);
+      return true;
+    }
+    return false;
+  }
   const int m = rows_mode<DT, V, IS>(a);
   if (m == 0) return false;
   if constexpr (V <= 4) {

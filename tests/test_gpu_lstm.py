@@ -59,6 +59,10 @@ def test_lstm_step_matches_oracle(bs, H, In, B, k, dname, use_pre):
     vals, idx, _ = bs.prune(W.cuda(), B, k=k)
     A = bs.pack(vals, idx, Kp, B)
     h, c = bs.lstm_step(A, x.cuda(), c_prev.cuda(), pre=pre.cuda() if use_pre else None, bias=bias.cuda())
+    # the direct kernel (half-warp gate rows, the cell after a CTA barrier) and the ring kernel agree bit for bit
+    hR, cR = bs.lstm_step(A, x.cuda(), c_prev.cuda(), pre=pre.cuda() if use_pre else None, bias=bias.cuda(),
+                          flags=bs.SPMV_PDL | bs.SPMV_RING)
+    assert torch.equal(h, hR) and torch.equal(c, cR)
     ov, oi = oracle.prune(synth.to_numpy(W), DT[dname], B, k)
     hr, cr, zb = oracle.lstm_cell(ov, oi, DT[dname], 4 * H, Kp, B, k, synth.to_numpy(x),
                                   synth.to_numpy(pre) if use_pre else None, synth.to_numpy(bias), c_prev.numpy())
