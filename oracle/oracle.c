@@ -341,7 +341,7 @@ static int64_t blob_bytes(int64_t mt, int64_t cb, int k, int es, int is) {
 typedef struct {
   int64_t V, P, NBf, T;
   int es, is;                 /* value bytes, index bytes */
-  int64_t ri;                 /* SPMV: bytes of a step's index run (160 for 5-bit runs, else P*is) */
+  int64_t ri;                 /* SPMV: bytes of a step's index run (160: 5-bit runs, 128: 4-bit runs, else P*is) */
   int64_t offA, offB, offC, total;  /* SP24: offA = values, offB = metadata */
 } orc_geom;
 
@@ -374,8 +374,9 @@ static int geom(int64_t M, int64_t K, int B, int k, int dt, int layout, orc_geom
     g->P = 32 * V;
     g->NBf = NB / g->P;
     g->T = NB - g->NBf * g->P;
-    /* docs/layout.md: 5-bit index runs when B = 32 and V = 8 (two planes: 32 u32 words + 32 bytes) */
-    g->ri = (B == 32 && V == 8) ? 160 : g->P * g->is;
+    /* docs/layout.md: 5-bit index runs when B = 32 and V = 8 (two planes: 32 u32 words + 32 bytes);
+     * 4-bit index runs when B <= 16 and V = 8 (32 u32 words) */
+    g->ri = (B == 32 && V == 8) ? 160 : (B <= 16 && V == 8) ? 128 : g->P * g->is;
     g->offA = 0;
     g->offB = align256(M * g->NBf * k * (g->P * g->es + g->ri));
     g->offC = g->offB + align256(M * k * g->T * g->es);
@@ -445,7 +446,8 @@ int orc_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int B,
     return 0;
   }
   int64_t step_bytes = g.P * g.es + g.ri;
-  int five = g.ri != g.P * g.is; /* 5-bit index runs */
+  int five = g.ri == 160;         /* 5-bit index runs */
+  int four = g.ri == 128 && g.P * g.is != 128; /* 4-bit index runs */
   for (int64_t r = 0; r < M; ++r) {
     /* region A: step (r, p, t) = P values then P indices; entry (l, v) at position l*V + v,
      * holding canonical (r, b = p*P + v*32 + l, t) */
@@ -458,7 +460,14 @@ int orc_pack(const void* vals, const uint16_t* idx, int64_t M, int64_t K, int B,
             int64_t src = (r * NB + b) * k + t;
             int64_t pos = l * g.V + v;
             memcpy(step + pos * g.es, in + src * g.es, g.es);
-            if (!five) put_index(step + g.P * g.es + pos * g.is, g.is, idx[src]);
+            if (!five && !four) put_index(step + g.P * g.es + pos * g.is, g.is, idx[src]);
+          }
+        if (four) /* G_l = sum_v idx(l, v) << 4v: 32 little-endian u32 words */
+          for (int l = 0; l < 32; ++l) {
+            uint32_t G = 0;
+            for (int64_t v = 0; v < 8; ++v) G |= (uint32_t)idx[(r * NB + p * g.P + v * 32 + l) * k + t] << (4 * v);
+            unsigned char* run = step + g.P * g.es;
+            for (int j = 0; j < 4; ++j) run[4 * l + j] = (unsigned char)(G >> (8 * j));
           }
         if (five) /* F_l = sum_v idx(l, v) << 5v: u32 plane (bits 0..31), then byte plane (32..39) */
           for (int l = 0; l < 32; ++l) {

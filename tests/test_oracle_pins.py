@@ -250,6 +250,10 @@ def test_packed_bytes_closed_form():
     assert oracle.packed_bytes(65536, 65536, 32, 3, oracle.F16, oracle.SPMV) == 65536 * 2048 * 3 * 21 // 8 == 1056964608
     # fc7 (NB = 128 -> V = 4): u8 indices, 3 B per nonzero
     assert oracle.packed_bytes(4096, 4096, 32, 3, oracle.F16, oracle.SPMV) == 3 * 4096 * 128 * 3
+    # B <= 16 with NB >= 256 (V = 8) -> 4-bit index runs: 2.5 B per panel nonzero; NB = 128 (V = 4) -> u8
+    assert oracle.packed_bytes(64, 4096, 16, 4, oracle.F16, oracle.SPMV) == 64 * 256 * 4 * 5 // 2
+    assert oracle.packed_bytes(64, 2048, 8, 2, oracle.F16, oracle.SPMV) == 64 * 256 * 2 * 5 // 2
+    assert oracle.packed_bytes(64, 2048, 16, 4, oracle.F16, oracle.SPMV) == 64 * 128 * 4 * 3
     # B > 256 -> u16 indices: 4 B per nnz at f16
     assert oracle.packed_bytes(64, 1024, 512, 8, oracle.F16, oracle.SPMV) == 4 * 64 * 2 * 8
     # SP24: K/2 values + K/8 metadata bytes per row
@@ -285,6 +289,24 @@ def test_pack_spmv_steps_closed_form():
         want = (blk.reshape(4, 32).T.reshape(-1) * 10 + t).astype(np.float32)
         np.testing.assert_array_equal(step[:512].view(np.float32), want)
         np.testing.assert_array_equal(step[512:], np.full(128, t, dtype=np.uint8))
+
+
+def test_pack_spmv_four_bit_runs_closed_form():
+    """B=16, f16, K=4096: NB=256 -> V=8, one panel, k=1. Block b keeps offset (5b+3) mod 16 with value b.
+    The step is 256 values (lane-major transpose), then lane l's 32-bit word sum_v idx(v*32+l) << 4v as
+    32 little-endian u32 words (docs/layout.md), 640 bytes in all, padded to 768."""
+    K, B, NB = 4096, 16, 256
+    blk = np.arange(NB)
+    vals = blk.astype(np.float16).reshape(1, NB, 1)
+    offs = (5 * blk + 3) % 16
+    buf = oracle.pack(vals, offs.astype(np.uint16).reshape(1, NB, 1), 1, K, B, 1, oracle.F16, oracle.SPMV)
+    assert buf.size == 768
+    np.testing.assert_array_equal(buf[:512].view(np.float16), blk.reshape(8, 32).T.reshape(-1).astype(np.float16))
+    words = buf[512:640].view("<u4")
+    for l in range(32):
+        want = sum(int(offs[v * 32 + l]) << (4 * v) for v in range(8))
+        assert int(words[l]) == want, l
+    assert not buf[640:].any()
 
 
 def test_pack_spmv_five_bit_runs_closed_form():
@@ -338,7 +360,9 @@ def test_pack_spmm_blob_closed_form():
 @pytest.mark.parametrize("layout", [oracle.SPMV, oracle.SPMM])
 @pytest.mark.parametrize("M,K,B,k,dt,dname", [(5, 3008, 32, 3, oracle.F16, "f16"), (3, 1024, 16, 8, oracle.F32, "f32"),
                                                (2, 2048, 512, 9, oracle.BF16, "bf16"), (4, 64, 4, 2, oracle.F16, "f16"),
-                                               (3, 8192 + 1024, 32, 3, oracle.BF16, "bf16")])
+                                               (3, 8192 + 1024, 32, 3, oracle.BF16, "bf16"),
+                                               (3, 4096 + 512, 16, 5, oracle.F16, "f16"),     # 4-bit runs + tail
+                                               (2, 2048 + 64, 8, 3, oracle.BF16, "bf16")])    # 4-bit runs, B = 8
 def test_pack_is_a_permutation(layout, M, K, B, k, dt, dname):
     """The packed value+index pairs are exactly the canonical multiset (no entry lost or duplicated)."""
     W = synth.to_numpy(synth.matrix(M, K, dname, seed=21))
@@ -374,7 +398,8 @@ def test_pack_is_a_permutation(layout, M, K, B, k, dt, dname):
     T = NB - (NB // P) * P
     a = lambda x: (x + 255) // 256 * 256
     five = B == 32 and V == 8
-    ri = 160 if five else P * isz                                    # index run bytes per step
+    four = B <= 16 and V == 8
+    ri = 160 if five else 128 if four else P * isz                  # index run bytes per step
     nsteps = nA // P
     A = buf[:nsteps * (P * es + ri)].reshape(-1, P * es + ri)         # steps: P values then the index run
     offB = a(nsteps * (P * es + ri))
@@ -386,6 +411,10 @@ def test_pack_is_a_permutation(layout, M, K, B, k, dt, dname):
     if five:  # 40-bit lane fields: u32 plane + byte plane; index v of lane l is bits 5v..5v+4
         F = A[:, P * es:P * es + 128].copy().view("<u4").astype(np.uint64) | (A[:, P * es + 128:].astype(np.uint64) << 32)
         ia = np.stack([(F >> (5 * v)) & 31 for v in range(8)], axis=-1).reshape(-1)  # (step, lane, v) = position l*V + v
+        pi = np.concatenate([ia, buf[offC:offC + nB].astype(np.uint64)])
+    elif four:  # 32-bit lane words; index v of lane l is bits 4v..4v+3
+        G = A[:, P * es:].copy().view("<u4").astype(np.uint64)
+        ia = np.stack([(G >> (4 * v)) & 15 for v in range(8)], axis=-1).reshape(-1)
         pi = np.concatenate([ia, buf[offC:offC + nB].astype(np.uint64)])
     else:
         iraw = np.concatenate([A[:, P * es:].reshape(-1), buf[offC:offC + nB * isz]])  # tail indices (region C)
