@@ -400,7 +400,7 @@ def main():
                                f"{1 - k / B:.5f}), batch 1 SpMV, row-sharded x{world}"
                                + ((" + all-gather of y fused into the SpMV (NVLink P2P)" if fused is not None
                                    else " + NCCL all_gather(y)") if world > 1 else ""),
-                   "M": M, "K": K, "block": B, "k": k, "batch": 1, "index_bits": 5 if (B == 32 and es == 2 and K // B >= 256) else (8 if B <= 256 else 16),
+                   "M": M, "K": K, "block": B, "k": k, "batch": 1, "index_bits": 5 if (B == 32 and es == 2 and K // B >= 256) else 4 if (B <= 16 and es == 2 and K // B >= 256) else (8 if B <= 256 else 16),
                    "packed_bytes_total": full_packed, "packed_bytes_per_rank": A.nbytes,
                    "l2": f"inputs larger than L2: {C} rotating cop{'y' if C == 1 else 'ies'} of a {A.nbytes / 1e6:.0f} MB "
                          f"packed slice vs {l2 / 1e6:.0f} MB L2",

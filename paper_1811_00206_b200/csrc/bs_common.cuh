@@ -28,7 +28,7 @@ struct Geom {
   int64_t P;    // 32*V blocks per panel
   int64_t NBf;  // full panels per row
   int64_t T;    // tail blocks per row
-  int64_t ri;   // SPMV: bytes of a step's index run (160 = 5-bit runs for B = 32, V = 8; else P·is)
+  int64_t ri;   // SPMV: bytes of a step's index run (160 = 5-bit runs for B = 32, V = 8; 128 = 4-bit runs for B <= 16, V = 8; else P·is)
   int64_t offA, offB, offC, total;  // SPMV/SPMM: panel steps, tail values, tail indices. SP24: values, metadata.
 };
 
@@ -69,8 +69,9 @@ inline bool make_geom(int64_t M, int64_t K, int B, int k, int dt, int layout, Ge
     g->NBf = g->NB / g->P;
     g->T = g->NB - g->NBf * g->P;
     // docs/layout.md: 5-bit index runs (a u32 plane and a byte plane of 40-bit lane fields) when
-    // B = 32 and V = 8; otherwise P indices of `is` bytes
-    g->ri = (B == 32 && V == 8) ? 160 : g->P * g->is;
+    // B = 32 and V = 8; 4-bit index runs (one u32 lane word) when B <= 16 and V = 8; otherwise P indices
+    // of `is` bytes
+    g->ri = (B == 32 && V == 8) ? 160 : (B <= 16 && V == 8) ? 128 : g->P * g->is;
     // region A: M·NBf·k steps of P·es + ri bytes; B / C: tail values / indices (M·k·T each)
     g->offA = 0;
     g->offB = align_up(M * g->NBf * k * (g->P * g->es + g->ri), kAlign);

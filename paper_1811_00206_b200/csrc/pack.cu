@@ -10,7 +10,7 @@ namespace {
 struct PackArgs {
   int64_t M, NB, NBf, T, P;
   int V, k, es, is;
-  int64_t ri;  // index run bytes per step (160: 5-bit runs, written by pack_idx5_kernel)
+  int64_t ri;  // index run bytes per step (160: 5-bit runs, 128: 4-bit runs; both written by pack_idx_runs_kernel)
   int64_t offA, offB, offC;
 };
 
@@ -20,7 +20,7 @@ __global__ void pack_kernel(const VT* __restrict__ vals, const uint16_t* __restr
                             VT* __restrict__ out_vals, uint16_t* __restrict__ out_idx) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t step_bytes = a.P * a.es + a.ri;
-  const bool five = a.ri != a.P * a.is;
+  const bool runs = a.ri != a.P * a.is;
   const int64_t kT = (int64_t)a.k * a.T;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nA + nB; e += stride) {
     int64_t src;
@@ -48,16 +48,18 @@ __global__ void pack_kernel(const VT* __restrict__ vals, const uint16_t* __restr
       vdst = base + a.offB + f * a.es;
       idst = base + a.offC + f * a.is;
     }
-    if (five && e < nA) {  // 5-bit runs: indices are packed per lane by pack_idx5_kernel
+    if (runs && e < nA) {  // 5- or 4-bit runs: indices are packed per lane by pack_idx_runs_kernel
       const int64_t pos = e % a.P;
       const int l = (int)(pos / a.V), v = (int)(pos % a.V);
       if (!unpack) {
         *(VT*)vdst = vals[src];
       } else {
         const uint8_t* run = vdst - pos * a.es + a.P * a.es;
-        const uint64_t F = (uint64_t)(*(const uint32_t*)(run + 4 * l)) | ((uint64_t)run[128 + l] << 32);
+        const int nb = a.ri == 160 ? 5 : 4;
+        uint64_t F = (uint64_t)(*(const uint32_t*)(run + 4 * l));
+        if (nb == 5) F |= (uint64_t)run[128 + l] << 32;
         out_vals[src] = *(const VT*)vdst;
-        out_idx[src] = (uint16_t)((F >> (5 * v)) & 31u);
+        out_idx[src] = (uint16_t)((F >> (nb * v)) & ((1u << nb) - 1u));
       }
       continue;
     }
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(512) pack_row_kernel(const VT* __restrict__ va
   VT* sv = (VT*)sm;
   uint16_t* si = (uint16_t*)(sm + bsk::align_up(nrow * es, 16));
   const int64_t step_bytes = a.P * es + a.ri;
-  const bool five = a.ri != a.P * a.is;
+  const bool runs = a.ri != a.P * a.is;
   const int k = a.k;
   const int64_t kT = (int64_t)k * a.T;
   const int64_t steps_row = a.NBf * k;
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(512) pack_row_kernel(const VT* __restrict__ va
     uint8_t* rowA = base + a.offA + r * steps_row * step_bytes;
     // 32-bit index arithmetic inside a row (a row holds < 2^31 entries); P = 32·V is a power of two
     const uint32_t P = (uint32_t)a.P, lgP = 31u - __clz(P), V = (uint32_t)a.V, lgV = 31u - __clz(V);
-    const uint32_t nvals = five ? 0u : (uint32_t)(steps_row * a.P);  // 5-bit runs: values written below
+    const uint32_t nvals = runs ? 0u : (uint32_t)(steps_row * a.P);  // 5-bit runs: values written below
     for (uint32_t e = threadIdx.x; e < nvals; e += blockDim.x) {
       const uint32_t st = e >> lgP;
       const uint32_t pos = e & (P - 1u);
@@ -120,15 +122,18 @@ __global__ void __launch_bounds__(512) pack_row_kernel(const VT* __restrict__ va
       const uint32_t l = pos >> lgV, v = pos & (V - 1u);
       const uint32_t b = p * P + v * 32u + l;
       *(VT*)(rowA + (int64_t)st * step_bytes + pos * es) = sv[b * k + t];
-      if (!five) {
+      if (!runs) {
         uint8_t* idst = rowA + st * step_bytes + a.P * es + pos * a.is;
         const uint16_t o = si[b * k + t];
         idst[0] = (uint8_t)(o & 0xff);
         if (a.is == 2) idst[1] = (uint8_t)(o >> 8);
       }
     }
-    if (five) {  // 5-bit runs (B = 32, V = 8, 16-bit values): per (step, lane) the lane's 8 values (one
-                 // 16-byte store) and its 40-bit index field sum_v idx << 5v (a word and a byte)
+    if (runs) {  // 5-bit runs (B = 32) or 4-bit runs (B <= 16), V = 8, 16-bit values: per (step, lane) the
+                 // lane's 8 values (one 16-byte store) and its index field sum_v idx << nb·v (a word, and a
+                 // byte for nb = 5)
+      const int nb = a.ri == 160 ? 5 : 4;
+      const uint32_t msk = (1u << nb) - 1u;
       for (uint32_t e = threadIdx.x; e < (uint32_t)steps_row * 32u; e += blockDim.x) {
         const uint32_t st = e >> 5, l = e & 31u;
         const uint32_t p = st / (uint32_t)k, t = st - p * (uint32_t)k;
@@ -137,13 +142,13 @@ __global__ void __launch_bounds__(512) pack_row_kernel(const VT* __restrict__ va
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           const uint32_t c = (p * P + v * 32u + l) * k + t;
-          F |= (uint64_t)(si[c] & 31u) << (5 * v);
+          F |= (uint64_t)(si[c] & msk) << (nb * v);
           vw[v >> 1] |= (uint32_t)(uint16_t)sv[c] << (16 * (v & 1));
         }
         *(uint4*)(rowA + (int64_t)st * step_bytes + l * 16u) = make_uint4(vw[0], vw[1], vw[2], vw[3]);
         uint8_t* run = rowA + (int64_t)st * step_bytes + a.P * es;
         *(uint32_t*)(run + 4 * l) = (uint32_t)F;
-        run[128 + l] = (uint8_t)(F >> 32);
+        if (nb == 5) run[128 + l] = (uint8_t)(F >> 32);
       }
     }
     // regions B / C: the row's tail, element t·T + q (q = v·32 + l) = block NBf·P + q, entry t
@@ -165,11 +170,14 @@ __global__ void __launch_bounds__(512) pack_row_kernel(const VT* __restrict__ va
 }
 
 // SP24 metadata: byte (r, c) holds blocks b = 2c, 2c+1 of row r as nibbles idx0 | idx1 << 2.
-// 5-bit index runs (docs/layout.md): one thread per (step, lane) builds the 40-bit field
-// F_l = sum_v idx(l, v) << 5v of its 8 indices and writes word l of the u32 plane and byte l of the byte plane.
-__global__ void pack_idx5_kernel(const uint16_t* __restrict__ idx, PackArgs a, uint8_t* __restrict__ base, int64_t nsl) {
+// 5-bit / 4-bit index runs (docs/layout.md): one thread per (step, lane) builds the field
+// F_l = sum_v idx(l, v) << nb·v of its 8 indices and writes word l of the u32 plane (and, for nb = 5, byte l of
+// the byte plane).
+__global__ void pack_idx_runs_kernel(const uint16_t* __restrict__ idx, PackArgs a, uint8_t* __restrict__ base, int64_t nsl) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t step_bytes = a.P * a.es + a.ri;
+  const int nb = a.ri == 160 ? 5 : 4;
+  const uint32_t msk = (1u << nb) - 1u;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nsl; e += stride) {
     const int64_t s = e >> 5;
     const int l = (int)(e & 31);
@@ -180,11 +188,11 @@ __global__ void pack_idx5_kernel(const uint16_t* __restrict__ idx, PackArgs a, u
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
       const int64_t b = p * a.P + (int64_t)v * 32 + l;
-      F |= (uint64_t)(idx[(r * a.NB + b) * a.k + t] & 31u) << (5 * v);
+      F |= (uint64_t)(idx[(r * a.NB + b) * a.k + t] & msk) << (nb * v);
     }
     uint8_t* run = base + a.offA + s * step_bytes + a.P * a.es;
     *(uint32_t*)(run + 4 * l) = (uint32_t)F;
-    run[128 + l] = (uint8_t)(F >> 32);
+    if (nb == 5) run[128 + l] = (uint8_t)(F >> 32);
   }
 }
 
@@ -319,7 +327,7 @@ cudaError_t run(const bsk::Geom& g, const void* vals, const uint16_t* idx, void*
     const int64_t nsl = nA / g.P * 32;  // (step, lane) pairs
     int64_t b5 = (nsl + 255) / 256;
     if (b5 > (int64_t)sms * 32) b5 = (int64_t)sms * 32;
-    pack_idx5_kernel<<<(unsigned)b5, 256, 0, s>>>(idx, a, base, nsl);
+    pack_idx_runs_kernel<<<(unsigned)b5, 256, 0, s>>>(idx, a, base, nsl);
   }
   return cudaGetLastError();
 }

@@ -60,6 +60,14 @@ namespace bsk_spmv {
 constexpr int kXBudget = 128 * 1024;  // bytes of x slots per chunk
 constexpr int kMaxChunks = 8;
 
+// IS (index encoding of the panel steps): 1 or 2 index bytes, 5 = 5-bit index runs (B = 32, V = 8), 4 = 4-bit
+// index runs (B <= 16, V = 8); docs/layout.md. Runs: lane l's indices of a step in one u32 word (+ one byte
+// plane for 5-bit). Tail indices (regions B/C) are one byte for the runs.
+template <int V, int IS>
+constexpr uint32_t run_bytes() { return IS == 5 ? 160u : IS == 4 ? 128u : 32u * V * IS; }
+template <int IS>
+constexpr int tail_is() { return (IS == 5 || IS == 4) ? 1 : IS; }
+
 struct SpmvArgs {
   const uint8_t* A;   // panel steps (region A)
   const uint8_t* Bt;  // tail values (region B): element r·k·T + t·T + v·32 + l
@@ -388,8 +396,9 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
   // IS: index bytes (1 or 2), or 5 = 5-bit index runs (B = 32, V = 8; docs/layout.md): per step a
   // plane of 32 u32 words and a plane of 32 bytes, lane l's 40-bit field sum_v idx(l, v) << 5v
   static_assert(IS != 5 || (V == 8 && BT == 32), "5-bit runs need V = 8 and B = 32");
-  constexpr int ISt = IS == 5 ? 1 : IS;                // tail index bytes (regions B/C)
-  constexpr uint32_t RI = IS == 5 ? 160u : P * IS;     // index run bytes per step
+  static_assert(IS != 4 || V == 8, "4-bit runs need V = 8");
+  constexpr int ISt = tail_is<IS>();                   // tail index bytes (regions B/C)
+  constexpr uint32_t RI = run_bytes<V, IS>();          // index run bytes per step
   constexpr uint32_t STEPB = P * ES + RI;              // bytes per step (values then indices)
   constexpr uint32_t SB = Q * STEPB;         // bytes per ring stage
   const int B = BT > 0 ? BT : a.B;
@@ -634,7 +643,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
         auto step = [&](int q) {
           uint32_t wv[(V * ES + 3) / 4], iv[(V * ISt + 3) / 4 > 2 ? (V * ISt + 3) / 4 : 2];
           const uint32_t av = sbase + q * STEPB + lane * (V * ES);
-          const uint32_t ai = sbase + q * STEPB + P * ES + lane * (IS == 5 ? 4 : V * IS);
+          const uint32_t ai = sbase + q * STEPB + P * ES + lane * ((IS == 5 || IS == 4) ? 4 : V * IS);
           if constexpr (V * ES == 16) bsk::lds_v4(av, wv[0], wv[1], wv[2], wv[3]);
           else if constexpr (V * ES == 8) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(wv[0]), "=r"(wv[1]) : "r"(av));
           else if constexpr (V * ES == 4) wv[0] = bsk::lds_u32(av);
@@ -642,6 +651,8 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
           if constexpr (IS == 5) {
             iv[0] = bsk::lds_u32(ai);
             iv[1] = lds_u8(sbase + q * STEPB + P * ES + 128 + lane);
+          } else if constexpr (IS == 4) {
+            iv[0] = bsk::lds_u32(ai);
           } else if constexpr (V * IS == 16) bsk::lds_v4(ai, iv[0], iv[1], iv[2], iv[3]);
           else if constexpr (V * IS == 8) asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(iv[0]), "=r"(iv[1]) : "r"(ai));
           else if constexpr (V * IS == 4) iv[0] = bsk::lds_u32(ai);
@@ -662,6 +673,7 @@ __global__ void __launch_bounds__(NT, 1) spmv_kernel(SpmvArgs a) {
             } else {
               uint32_t o;
               if constexpr (IS == 5) o = (v < 7 ? __funnelshift_r(iv[0], iv[1], 5 * v) : iv[1] >> 3) & 31u;
+              else if constexpr (IS == 4) o = (iv[0] >> (4 * v)) & 15u;
               else if constexpr (IS == 1) o = byte_of(iv[v >> 2], v & 3);
               else o = (iv[v >> 1] >> (16 * (v & 1))) & 0xffffu;
               gather_fma(pb, o, v, w);
@@ -879,12 +891,12 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (NJ == 2 ? 3 : 4) : 2)) spmv_ro
   using raw_t = typename bsk::DTraits<DT>::raw_t;
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int P = 32 * V;
-  constexpr int ISt = IS == 5 ? 1 : IS;
-  constexpr uint32_t RI = IS == 5 ? 160u : (uint32_t)P * IS;
+  constexpr int ISt = tail_is<IS>();
+  constexpr uint32_t RI = run_bytes<V, IS>();
   constexpr uint32_t STEPB = (uint32_t)P * ES + RI;
   constexpr int G = HW ? 3 : 4;                          // steps per load group (HW: registers for two lanes)
   constexpr int WW = (V * ES + 3) / 4;                   // value words per lane and step
-  constexpr int IW = IS == 5 ? 2 : (V * IS + 3) / 4;     // index words per lane and step
+  constexpr int IW = IS == 5 ? 2 : IS == 4 ? 1 : (V * IS + 3) / 4;  // index words per lane and step
   const int lane = threadIdx.x & 31;
   constexpr int LPR = 32 / NJ;                           // lanes per row; lane hl plays ring lanes hl + LPR·j
   const int sub = lane / LPR;                            // which row of the warp's NJ rows
@@ -984,6 +996,10 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (NJ == 2 ? 3 : 4) : 2)) spmv_ro
               i1.load(st + P * ES + 128 + L);
               iv[g][j][0] = i0.w[0];
               iv[g][j][1] = i1.w[0];
+            } else if constexpr (IS == 4) {
+              bsk::Vec<4> i0;
+              i0.load(st + P * ES + 4 * L);
+              iv[g][j][0] = i0.w[0];
             } else {
               bsk::Vec<V * IS> ii;
               ii.load(st + P * ES + L * (V * IS));
@@ -1009,6 +1025,7 @@ __global__ void __launch_bounds__(256, (V <= 4 ? (NJ == 2 ? 3 : 4) : 2)) spmv_ro
               const uint32_t w = ES == 2 ? (wv[g][j][v >> 1] >> (16 * (v & 1))) & 0xffffu : wv[g][j][v];
               uint32_t o;
               if constexpr (IS == 5) o = (v < 7 ? __funnelshift_r(iv[g][j][0], iv[g][j][1], 5 * v) : iv[g][j][1] >> 3) & 31u;
+              else if constexpr (IS == 4) o = (iv[g][j][0] >> (4 * v)) & 15u;
               else if constexpr (IS == 1) o = byte_of(iv[g][j][v >> 2], v & 3);
               else o = (iv[g][j][v >> 1] >> (16 * (v & 1))) & 0xffffu;
               bsk::fma_acc<DT>(acc[j][v], w, (uint32_t)__ldg(x + (cb + (uint32_t)v * B32 + o)));
@@ -1183,7 +1200,7 @@ template <int DT, int V, int IS, int BT, bool MULTI, int NT, int QM, int NV>
 cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   constexpr int ES = bsk::DTraits<DT>::kBytes;
   constexpr int Q = StageSteps<V, ES>::value * QM;
-  constexpr int SB = Q * (32 * V * ES + (IS == 5 ? 160 : 32 * V * IS));
+  constexpr int SB = Q * (32 * V * ES + (int)run_bytes<V, IS>());
   auto kern = spmv_kernel<DT, V, IS, Q, BT, MULTI, NT, NV>;
   const auto& dp = bsk::dev_props();
   cudaError_t perr = cudaSuccess;
@@ -1192,7 +1209,7 @@ cudaError_t launch_cfg(const SpmvArgs& a0, cudaStream_t s) {
   SpmvArgs a = a0;
   a.tail_rows = 0;
   if (a.T > 0 && a.k > 0) {  // whole rows of tail per ring stage (32 bytes of alignment slack)
-    const int64_t per = (int64_t)a.k * a.T * (ES + (IS == 5 ? 1 : IS));
+    const int64_t per = (int64_t)a.k * a.T * (ES + tail_is<IS>());
     const int64_t R = (SB - 64) / per;
     a.tail_rows = R >= 1 ? (int)(R < 64 ? R : 64) : 0;
   }
@@ -1237,8 +1254,8 @@ cudaError_t launch_nt(const SpmvArgs& a, cudaStream_t s) {
   if constexpr (BIG > 1 && MULTI) {  // rows with tails always run the MULTI variant
     // tails stream through the ring a whole row per stage; a row's tail that does not fit a small stage
     // would fall back to per-entry global loads (PTB at 50%: 1.6x slower), so take the big-stage variant
-    constexpr int64_t SBs = (int64_t)StageSteps<V, ES>::value * (32 * V * ES + (IS == 5 ? 160 : 32 * V * IS));
-    const int64_t per = (int64_t)a.k * a.T * (ES + (IS == 5 ? 1 : IS));
+    constexpr int64_t SBs = (int64_t)StageSteps<V, ES>::value * (32 * V * ES + (int)run_bytes<V, IS>());
+    const int64_t per = (int64_t)a.k * a.T * (ES + tail_is<IS>());
     if (a.T > 0 && a.k > 0 && per > SBs - 64) return launch_cfg<DT, V, IS, BT, MULTI, 512, BIG, NV>(a, s);
   }
   return launch_cfg<DT, V, IS, BT, MULTI, 512, 1, NV>(a, s);
@@ -1249,6 +1266,8 @@ cudaError_t launch_t(const SpmvArgs& a, cudaStream_t s) {
   const bool multi = a.nchunks > 1 || a.T > 0;
   if constexpr (IS == 5) {  // B = 32, V = 8 only
     return multi ? launch_nt<DT, V, IS, 32, true, NV>(a, s) : launch_nt<DT, V, IS, 32, false, NV>(a, s);
+  } else if constexpr (IS == 4) {  // B <= 16, V = 8: B at run time
+    return multi ? launch_nt<DT, V, IS, 0, true, NV>(a, s) : launch_nt<DT, V, IS, 0, false, NV>(a, s);
   } else {
     // B = 32 with V = 8 (16-bit) always uses 5-bit runs, so the B = 32 specialisation is for V < 8
     if constexpr (IS == 1 && V < 8)
@@ -1285,13 +1304,20 @@ cudaError_t dispatch_v(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
 template <int DT, int NV>
 cudaError_t dispatch_is(const bsk::Geom& g, const SpmvArgs& a, cudaStream_t s) {
   if constexpr (DT != BS_F32)
-    if (g.ri != g.P * g.is) {  // 5-bit index runs
+    if (g.ri == 160) {  // 5-bit index runs
       if constexpr (NV == 1)
         if (a.direct) {
           cudaError_t e = cudaSuccess;
           if (try_rows<DT, 8, 5>(a, s, &e)) return e;
         }
       return launch_t<DT, 8, 5, NV>(a, s);
+    } else if (g.ri != g.P * g.is) {  // 4-bit index runs
+      if constexpr (NV == 1)
+        if (a.direct) {
+          cudaError_t e = cudaSuccess;
+          if (try_rows<DT, 8, 4>(a, s, &e)) return e;
+        }
+      return launch_t<DT, 8, 4, NV>(a, s);
     }
   return g.is == 1 ? dispatch_v<DT, 1, NV>(g, a, s) : dispatch_v<DT, 2, NV>(g, a, s);
 }

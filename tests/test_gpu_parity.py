@@ -58,6 +58,9 @@ SMALL = [
     (65, 640, 20, 0, "f16", "gaussian"),       # k = 0
     (8, 256, 16, 16, "bf16", "gaussian"),      # k = B (dense)
     (3, 96, 1, 1, "f16", "gaussian"),          # B = 1
+    (40, 4096 + 16 * 40, 16, 4, "f16", "gaussian"),  # 4-bit index runs (B = 16, NB = 296): a panel + a 40-block tail
+    (33, 16 * 512, 16, 3, "bf16", "ties"),     # 4-bit runs, two panels, no tail
+    (20, 8 * 300, 8, 2, "f16", "sameoffset"),  # 4-bit runs, B = 8
 ]
 
 

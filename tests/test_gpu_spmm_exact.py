@@ -52,6 +52,20 @@ def _exact(bs, A, ov, oi, dname, X):
 
 # ---------------------------------------------------------------- K4: SPMV layout, CUDA cores
 
+@pytest.mark.parametrize("N", [1, 3, 8, 13])
+def test_k4_four_bit_runs_integer_exact(bs, N):
+    """B = 16 with NB >= 256: 4-bit index runs (docs/layout.md) through the SpMV (N = 1) and the batched
+    passes, two x chunks worth of panels plus a tail; bit-exact against the oracle."""
+    M, K, B, k = 150, 16 * (512 + 20), 16, 3
+    A, ov, oi = _setup(bs, M, K, B, k, "f16", synth.seed_for(21, N), "spmv")
+    X = synth.vector(K, "f16", family="intexact", seed=synth.seed_for(21, 100 + N), n=N)
+    _exact(bs, A, ov, oi, "f16", X)
+    if N == 1:
+        y = bs.spmv(A, X[0].cuda())
+        Yr, _ = oracle.spmm(ov, oi, DT["f16"], M, K, B, k, synth.to_numpy(X))
+        np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(y), DT["f16"]), Yr[0])
+
+
 @pytest.mark.parametrize("dname", ["f16", "bf16"])
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 8, 13, 24])
 def test_k4_integer_exact(bs, N, dname):
@@ -313,6 +327,8 @@ def test_block_rank_errors_and_alignment(bs):
     (4096, 4096, 32, 3, "bf16"),   # fc7 90 %
     (4096, 2048, 32, 4, "f16"),    # CTC W_ih
     (4096, 1024, 32, 4, "bf16"),   # CTC W_hh (V = 1)
+    (4096, 4096, 16, 2, "f16"),    # 4-bit index runs (B = 16, V = 8)
+    (6000, 4096 + 16 * 8, 16, 1, "bf16"),  # 4-bit runs, more rows than a wave (V = 8), tail held in registers
     (777, 25088, 32, 1, "f16"),    # fc6 at 97 %: 5-bit runs, V = 8
     (300, 640, 20, 6, "f32"),      # tail only, odd B, f32
     (129, 96, 4, 2, "f16"),
