@@ -341,7 +341,7 @@ def main():
     value = bytes_job / (ms * 1e-3) / 1e9
     nnz_l = Ml * (K // B) * k
     alg_l = alg_bytes(nnz_l, B, es, K, Ml)
-    achieved = alg_l / (kern_ms * 1e-3) / 1e9
+    achieved = alg_l / (kern_ms_max * 1e-3) / 1e9  # the slowest rank's launch (max over ranks, as kernel_ms)
     packed_l = A.nbytes + K * es + Ml * es
 
     # ---- e2e: host x (pinned) -> device -> SpMV (-> all-gather) -> host y, every step
@@ -411,7 +411,7 @@ def main():
                                        "ncu --set full capture of this launch (profiles/r2_spmv_65536_s90_ncu.md)",
                      "kernel": "spmv_kernel", "kernel_ms": round(kern_ms_max, 5),
                      "alg_bytes_per_launch": int(alg_l), "packed_bytes_per_launch": packed_l,
-                     "packed_frac": round(packed_l / (kern_ms * 1e-3) / 1e9 / hbm_peak, 4), "peak_source": peak_src},
+                     "packed_frac": round(packed_l / (kern_ms_max * 1e-3) / 1e9 / hbm_peak, 4), "peak_source": peak_src},
         "e2e": e2e,
         "gpu_launches": a.steps,
         "legs": legs if world == 1 else dict(legs, spmv_ms=round(kern_ms_max, 5),
