@@ -33,6 +33,23 @@
 #include "bs_device.cuh"
 #include "bs_tc.cuh"
 
+#ifdef BS_TRACE_K6
+// Debug timeline (tools/k6_trace_probe.py): %globaltimer at phase boundaries, per CTA.
+__device__ unsigned long long g_k6_trace[4096 * 16];
+extern "C" int bs_k6_trace_read(void* host, int n) { return (int)cudaMemcpyFromSymbol(host, g_k6_trace, (size_t)n * 8); }
+#define K6_MARK(i)                                                                                              \
+  do {                                                                                                          \
+    unsigned long long t_;                                                                                      \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                                      \
+    const unsigned cta_ = blockIdx.x + gridDim.x * blockIdx.y;                                                  \
+    if (cta_ < 4096) g_k6_trace[cta_ * 16 + (i)] = t_;                                                          \
+  } while (0)
+#else
+#define K6_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 namespace {
 
 using namespace bsk_tc;
@@ -48,7 +65,10 @@ constexpr int kMmaWarp = kProducers;  // first MMA warp
 constexpr int kMmaWarps = 2;          // MMA issuers (a tcgen05.mma issue costs ~80 cycles: one thread cannot keep up with N <= 32)
 constexpr int kFirstDecomp = 32 * (kProducers + kMmaWarps);
 constexpr int kThreads = kFirstDecomp + kGroups * kDecomp;
-constexpr int kMaxCluster = 8;   // split-K factor (portable cluster size)
+// split-K factor: at most 4 CTAs per cluster. Clusters of 8 CTAs with ~200 KB of shared memory each did not
+// all fit at once (conv4_2: 16 clusters, CTAs starting up to 28 us late, tools/k6_trace_probe.py); S = 4
+// fits and took conv3_3 26.6 -> 14.3 us.
+constexpr int kMaxCluster = 4;
 
 struct TcArgs {
   const uint8_t* W;   // packed SPMM layout
@@ -96,6 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
   };
   const uint32_t blobCB = blob_bytes(a.CB);
 
+  if (threadIdx.x == 0) K6_MARK(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSB; ++s) {
       mbar_init(full + 8 * s, 1);
@@ -121,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem_d = tmem_holder;
+  if (threadIdx.x == 0) K6_MARK(1);
 
   if (warp < kProducers) {
     if (lane == 0) {  // ---- producers: warp w issues chunks i = w, w + 4, ...
@@ -192,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
       const int n_e = (int)mt * cb * k;
       if (i >= NA) mbar_wait(a_empty + 8 * ab, aph ^ 1u);  // MMA done with this A tile
       mbar_wait(full + 8 * s, ph);
+      if (t == 0 && grp == 0 && i == 0) K6_MARK(2);
       // 32-bit shared addresses (a generic pointer here would compile to LD.E with 64-bit math)
       const uint32_t bv = sR + (uint32_t)s * (uint32_t)a.blob_max;
       const uint32_t bi = bv + (((uint32_t)n_e * ES + 15u) & ~15u);
@@ -233,8 +256,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
     }
     // ---- epilogue: TMEM -> registers. Warp w reads lane quarter w % 4 (rows 32·(w % 4) + lane) and
     // column part (w - 2) / 4 of NP parts.
+    if (t == 0 && grp == 0) K6_MARK(3);
     mbar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
+    if (t == 0 && grp == 0) K6_MARK(4);
     const int q = warp & 3, part = (warp - kFirstDecomp / 32) >> 2;
     const int NP = a.BN % 32 == 0 ? 4 : 2;  // parts of BN / NP columns, a multiple of 8
     const int m = 32 * q + lane;
@@ -271,19 +296,26 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
       }
     }
   }
+  if (threadIdx.x == kFirstDecomp) K6_MARK(5);
   if (S > 1) {
     cluster_sync_all();  // every partial tile is parked
+    if (threadIdx.x == kFirstDecomp) K6_MARK(6);
     if (warp >= kFirstDecomp / 32) {
       const int t = threadIdx.x - kFirstDecomp;
       const int U = a.BN * BM / 4;  // float4 units of the tile
       const int u0 = (int)((int64_t)rank * U / S), u1 = (int)((int64_t)(rank + 1) * U / S);
       for (int u = u0 + t; u < u1; u += kGroups * kDecomp) {
         const uint32_t la = sA + (uint32_t)u * 16;
-        float4 v = ld_cluster_f4(la, 0);
-        for (int p = 1; p < S; ++p) {  // fixed rank order: partials over consecutive K ranges
-          const float4 w = ld_cluster_f4(la, (uint32_t)p);
-          v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
-        }
+        // all S remote loads in flight before the first add (a load-add chain was latency-bound: ~4.6 us of
+        // conv4_2's epilogue, tools/k6_trace_probe.py); then the fixed rank order: partials over consecutive K ranges
+        float4 w[kMaxCluster];
+#pragma unroll
+        for (int p = 0; p < kMaxCluster; ++p)
+          if (p < S) w[p] = ld_cluster_f4(la, (uint32_t)p);
+        float4 v = w[0];
+#pragma unroll
+        for (int p = 1; p < kMaxCluster; ++p)
+          if (p < S) { v.x += w[p].x; v.y += w[p].y; v.z += w[p].z; v.w += w[p].w; }
         const int n = u >> 5, row = (u & 31) * 4;
         const int64_t ng = n0 + n;
         if (ng < a.N) {
@@ -295,8 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
         }
       }
     }
+    if (threadIdx.x == kFirstDecomp) K6_MARK(7);
     cluster_sync_all();  // peers' shared memory stays alive until every slice is read
   }
+  if (threadIdx.x == kFirstDecomp) K6_MARK(8);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == kMmaWarp) {

@@ -209,11 +209,14 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
       const int u0 = (int)((int64_t)rank * U / S), u1 = (int)((int64_t)(rank + 1) * U / S);
       for (int u = u0 + t; u < u1; u += 128 * RT) {
         const uint32_t la = sA + (uint32_t)u * 16;
-        float4 v = ld_cluster_f4(la, 0);
-        for (int p = 1; p < S; ++p) {
-          const float4 w = ld_cluster_f4(la, (uint32_t)p);
-          v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
-        }
+        float4 w[8];  // all S remote loads in flight, then the fixed rank order (as K6)
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+          if (p < S) w[p] = ld_cluster_f4(la, (uint32_t)p);
+        float4 v = w[0];
+#pragma unroll
+        for (int p = 1; p < 8; ++p)
+          if (p < S) { v.x += w[p].x; v.y += w[p].y; v.z += w[p].z; v.w += w[p].w; }
         const int n = u / RW, r4 = (u - n * RW) * 4;
         const int64_t ng = n0 + n;
         if (ng < a.N) {

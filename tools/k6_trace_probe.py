@@ -1,0 +1,43 @@
+"""K6 phase timeline (library built with -DBS_TRACE_K6 into probe_bin/libbs_k6trace.so):
+python tools/k6_trace_probe.py M K B k N. Prints, per phase mark, percentiles over CTAs of the time since the
+earliest CTA start (us): 0 entry, 1 set-up done (after the PDL wait), 2 first chunk's stage full (decompress
+group 0), 3 group 0's last chunk, 4 accumulator ready, 5 partial tile parked, 6 after the first cluster
+barrier, 7 slice summed, 8 end."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_1811_00206_b200 as bs  # noqa: E402
+import synth  # noqa: E402
+
+bs.LIB_PATH = os.path.join(ROOT, "probe_bin", "libbs_k6trace.so")
+M, K, B, k, N = (int(v) for v in sys.argv[1:6])
+W = synth.matrix(M, K, "f16", seed=3, device="cuda")
+v, i, _ = bs.prune(W, B, k=k)
+A = bs.pack(v, i, K, B, layout="spmm")
+X = synth.vector(K, "f16", seed=4, n=N, device="cuda")
+Y = torch.empty((N, M), dtype=torch.float16, device="cuda")
+for _ in range(5):
+    bs.spmm(A, X, out=Y)
+torch.cuda.synchronize()
+L = bs.lib()
+L.bs_k6_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
+buf = np.zeros(4096 * 16, dtype=np.uint64)
+L.bs_k6_trace_read(buf.ctypes.data, buf.size)
+T = buf.reshape(4096, 16).astype(np.float64)
+live = T[:, 0] > 0
+T = T[live]
+t0 = T[:, 0].min()
+print(f"M={M} K={K} B={B} k={k} N={N}: {live.sum()} CTAs")
+for m in range(9):
+    col = T[:, m]
+    col = col[col > 0]
+    if col.size:
+        d = (col - t0) / 1e3
+        print(f"  mark {m}: min {d.min():7.2f}  p50 {np.percentile(d, 50):7.2f}  p90 {np.percentile(d, 90):7.2f}  max {d.max():7.2f} us")
