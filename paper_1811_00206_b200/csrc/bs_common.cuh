@@ -133,6 +133,22 @@ inline int tc_cols_fast() {
   return v;
 }
 
+// Tensor-core SpMM column-tile width: when the grid (row tiles × split × column tiles) would occupy at
+// most 1/busy_div of the SMs, narrower column tiles put more CTAs to work. BN only partitions the batch
+// columns, so every column's sum is unchanged. BS_TC_FILL=0 turns it off (A/B).
+inline int64_t fill_bn(int64_t N, int64_t BN, int64_t ctas_per_coltile, int64_t quantum, int64_t busy_div) {
+  static const int on = [] {
+    const char* e = getenv("BS_TC_FILL");
+    return e && e[0] ? atoi(e) : 1;
+  }();
+  const int64_t sms = dev_props().sms;
+  if (!on || ctas_per_coltile <= 0 || ctas_per_coltile * ((N + BN - 1) / BN) * busy_div > sms) return BN;
+  const int64_t want = sms / ctas_per_coltile;  // column tiles that still fit one wave
+  int64_t bn = ((N + want - 1) / want + quantum - 1) / quantum * quantum;
+  if (bn < quantum) bn = quantum;
+  return bn < BN ? bn : BN;
+}
+
 }  // namespace bsk
 
 // Launchers implemented in the kernel translation units. All return cudaError_t of the launch.

@@ -405,6 +405,10 @@ cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int
   if (bn_max < 16) return cudaErrorNotSupported;
   int64_t BN = (N + 15) / 16 * 16;
   if (BN > bn_max) BN = bn_max;
+  // conv5_x: 4 row tiles × S = 4 × 1 column tile left 132 SMs idle (20.6 -> 13.2 us). Only below a quarter
+  // of the SMs: each column tile decompresses its A chunks again, and K6 is shared-memory bound (conv4_2
+  // at 64 -> 144 CTAs: 17.5 -> 23.9 us)
+  BN = bsk::fill_bn(N, BN, g.P * a.S, 16, 4);
   a.BN = (int)BN;
   a.idesc = idesc_f16(DT == BS_BF16, BM, (int)BN, false);
   int cols = 32;

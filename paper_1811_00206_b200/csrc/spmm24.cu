@@ -495,6 +495,14 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
     BN = (int)((N + 31) / 32 * 32);
     if (BN > 256) BN = 256;
   }
+  {  // narrower column tiles when the row tiles × split leave SMs idle (bsk::fill_bn; S as computed below)
+    int64_t Sf = pair ? 1 : bsk::dev_props().sms / tiles;
+    if (Sf > 8) Sf = 8;
+    if (Sf > (g.K / KCH) / bsk::splitk_min_chunks(6)) Sf = (g.K / KCH) / bsk::splitk_min_chunks(6);
+    if (Sf < 1) Sf = 1;
+    const int64_t rows_per_cta = pair ? BM : (int64_t)BM * RT;
+    BN = (int)bsk::fill_bn(N, BN, (g.M + rows_per_cta - 1) / rows_per_cta * Sf, pair ? 32 : 16, 2);  // CTC N = 64: 64 -> 128 CTAs
+  }
   CUtensorMap tA, tX;
   const uint8_t* base = (const uint8_t*)packed;
   if (!bsk_make_map_2d(&tA, DT, base + g.offA, g.K / 2, g.M, g.K / 2, 64, BM)) return cudaErrorNotSupported;

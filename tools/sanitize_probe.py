@@ -1,6 +1,6 @@
 """Every kernel of libbs.so once, on BASELINE configs[0] (64 x 64, f32, B = 16, s = 0.5) and on the VGG fc7
 layer (4096 x 4096, f16, B = 32, s = 0.9), for compute-sanitizer (memcheck / racecheck / synccheck):
-    compute-sanitizer --tool memcheck python tools/sanitize_probe.py [cfg0|fc7]"""
+    compute-sanitizer --tool memcheck python tools/sanitize_probe.py [cfg0|fc7|s3]"""
 import os
 import sys
 
@@ -14,6 +14,28 @@ from paper_1811_00206_b200.dist import FusedRowShardedBS, row_range  # noqa: E40
 
 which = sys.argv[1] if len(sys.argv) > 1 else "fc7"
 dev = torch.device("cuda")
+if which == "s3":  # round 2, session 3's kernels: K5 CTA pairs and RT = 2, half-warp direct rows, the LSTM step
+    # on the direct kernel, 4-bit index runs (SpMV ring + direct, K4 passes)
+    for M, K, N in ((9728, 1024, 40), (8192 + 64, 1536, 80)):  # pairs (S = 1); RT = 2 (S = 2, N > 64)
+        W = synth.matrix(M, K, "f16", seed=11, device=dev)
+        v4, i4, _ = bs.prune(W, 4, k=2)
+        bs.spmm(bs.pack(v4, i4, K, 4, layout="sp24"), synth.vector(K, "f16", seed=12, n=N, device=dev))
+    W = synth.matrix(6000, 3008, "f16", seed=13, device=dev)
+    v, i, k = bs.prune(W, 32, sparsity=0.9)
+    A = bs.pack(v, i, 3008, 32)
+    x = synth.vector(3008, "f16", seed=14, device=dev)
+    bs.spmv(A, x)                                    # half-warp rows
+    bs.lstm_step(A, x, torch.zeros(1500, dtype=torch.float32, device=dev), bias=x[:0].new_zeros(6000))
+    W = synth.matrix(512, 4096 + 128, "bf16", seed=15, device=dev)
+    v, i, k = bs.prune(W, 16, k=3)
+    A = bs.pack(v, i, 4096 + 128, 16)               # 4-bit index runs + tail
+    bs.unpack(A)
+    xb = synth.vector(4096 + 128, "bf16", seed=16, device=dev)
+    bs.spmv(A, xb)                                   # direct kernel
+    bs.spmv(A, xb, flags=bs.SPMV_PDL | bs.SPMV_RING)  # ring kernel
+    bs.spmm(A, synth.vector(4096 + 128, "bf16", seed=17, n=11, device=dev))  # K4 passes
+    torch.cuda.synchronize()
+    sys.exit(0)
 if which == "cfg0":
     M, K, B, s, dt = 64, 64, 16, 0.5, "f32"
 else:
