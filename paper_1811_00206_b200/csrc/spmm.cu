@@ -304,26 +304,34 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
       const int t = threadIdx.x - kFirstDecomp;
       const int U = a.BN * BM / 4;  // float4 units of the tile
       const int u0 = (int)((int64_t)rank * U / S), u1 = (int)((int64_t)(rank + 1) * U / S);
-      for (int u = u0 + t; u < u1; u += kGroups * kDecomp) {
-        const uint32_t la = sA + (uint32_t)u * 16;
-        // all S remote loads in flight before the first add (a load-add chain was latency-bound: ~4.6 us of
-        // conv4_2's epilogue, tools/k6_trace_probe.py); then the fixed rank order: partials over consecutive K ranges
-        float4 w[kMaxCluster];
+      // two units per thread and round with all their S remote loads in flight before the first add (a
+      // load-add chain per unit was latency-bound: ~4.6 us of conv4_2's epilogue, tools/k6_trace_probe.py);
+      // then the fixed rank order: partials over consecutive K ranges
+      constexpr int UU = 2, NTH = kGroups * kDecomp;
+      for (int ub = u0 + t; ub < u1; ub += UU * NTH) {
+        float4 w[UU][kMaxCluster];
 #pragma unroll
-        for (int p = 0; p < kMaxCluster; ++p)
-          if (p < S) w[p] = ld_cluster_f4(la, (uint32_t)p);
-        float4 v = w[0];
+        for (int j = 0; j < UU; ++j)
 #pragma unroll
-        for (int p = 1; p < kMaxCluster; ++p)
-          if (p < S) { v.x += w[p].x; v.y += w[p].y; v.z += w[p].z; v.w += w[p].w; }
-        const int n = u >> 5, row = (u & 31) * 4;
-        const int64_t ng = n0 + n;
-        if (ng < a.N) {
-          raw_t* yp = (raw_t*)a.Y + ng * a.ldy + m0 + row;
-          const float f[4] = {v.x, v.y, v.z, v.w};
+          for (int p = 0; p < kMaxCluster; ++p)
+            if (p < S && ub + j * NTH < u1) w[j][p] = ld_cluster_f4(sA + (uint32_t)(ub + j * NTH) * 16, (uint32_t)p);
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (row + e < mt) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
+        for (int j = 0; j < UU; ++j) {
+          const int u = ub + j * NTH;
+          if (u >= u1) break;
+          float4 v = w[j][0];
+#pragma unroll
+          for (int p = 1; p < kMaxCluster; ++p)
+            if (p < S) { v.x += w[j][p].x; v.y += w[j][p].y; v.z += w[j][p].z; v.w += w[j][p].w; }
+          const int n = u >> 5, row = (u & 31) * 4;
+          const int64_t ng = n0 + n;
+          if (ng < a.N) {
+            raw_t* yp = (raw_t*)a.Y + ng * a.ldy + m0 + row;
+            const float f[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (row + e < mt) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
+          }
         }
       }
     }

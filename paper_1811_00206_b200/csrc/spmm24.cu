@@ -19,11 +19,29 @@
 #include "bs_device.cuh"
 #include "bs_tc.cuh"
 
+#ifdef BS_TRACE_K5
+// Debug timeline (tools/k6_trace_probe.py --k5): %globaltimer at phase boundaries, per CTA.
+__device__ unsigned long long g_k5_trace[4096 * 16];
+extern "C" int bs_k5_trace_read(void* host, int n) { return (int)cudaMemcpyFromSymbol(host, g_k5_trace, (size_t)n * 8); }
+#define K5_MARK(i)                                                                                              \
+  do {                                                                                                          \
+    unsigned long long t_;                                                                                      \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                                      \
+    const unsigned cta_ = blockIdx.x + gridDim.x * blockIdx.y;                                                  \
+    if (cta_ < 4096) g_k5_trace[cta_ * 16 + (i)] = t_;                                                          \
+  } while (0)
+#else
+#define K5_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int BM = 128;
 constexpr int KCH = 128;  // original columns per chunk (64 compressed values: one 128-byte swizzle atom)
 constexpr int kMaxStages = 8;  // pipeline stages (runtime NST: as many as shared memory holds, 2..8)
+constexpr int kMaxSplit = 4;   // split-K cluster size cap (as K6: clusters of 8 large-smem CTAs may not all fit)
 
 struct Sp24Args {
   const uint8_t* meta;  // M × K/8 bytes
@@ -67,6 +85,7 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
   const int64_t n0 = (int64_t)(a.colfast ? blockIdx.x / S : blockIdx.y) * a.BN;
   const int c0 = (int)((int64_t)rank * a.NC / S), nloc = (int)((int64_t)(rank + 1) * a.NC / S) - c0;  // >= 1
 
+  if (threadIdx.x == 0) K5_MARK(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(full + 8 * s, 1);
@@ -91,6 +110,7 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = tmem_holder;
+  if (threadIdx.x == 0) K5_MARK(1);
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
@@ -112,6 +132,7 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
       uint32_t par = 0;
       for (int i = 0; i < nloc; ++i) {
         mbar_wait(full + 8 * s, par);
+        if (i == 0) K5_MARK(2);
         mbar_wait(meta_ok + 8 * s, par);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
@@ -178,8 +199,10 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
       if (lane == 0) mbar_arrive(meta_ok + 8 * s);
       if (++s == NST) { s = 0; ph ^= 1u; }
     }
+    if (threadIdx.x == 64) K5_MARK(3);
     mbar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
+    if (threadIdx.x == 64) K5_MARK(4);
     // split-K partial tile [BN][128·RT] fp32 at sA (the rings are idle now)
     const int64_t mt = mrows - (int64_t)t * BM;  // rows of this warp's tile (may be <= 0)
     for (int nb = 0; nb < a.BN; nb += 8) {
@@ -200,36 +223,50 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
       }
     }
   }
+  if (threadIdx.x == 64) K5_MARK(5);
   if (S > 1) {  // fixed-order sum of the S partial tiles through distributed shared memory
     cluster_sync_all();
+    if (threadIdx.x == 64) K5_MARK(6);
     if (warp >= 2) {
       const int t = threadIdx.x - 64;
       constexpr int RW = BM * RT / 4;  // float4 units per partial-tile column
       const int U = a.BN * RW;
       const int u0 = (int)((int64_t)rank * U / S), u1 = (int)((int64_t)(rank + 1) * U / S);
-      for (int u = u0 + t; u < u1; u += 128 * RT) {
-        const uint32_t la = sA + (uint32_t)u * 16;
-        float4 w[8];  // all S remote loads in flight, then the fixed rank order (as K6)
+      // four units per thread and round, all their S remote loads in flight before the first add: a
+      // load-add chain per unit was latency-bound (CTC N = 256: 4.1 us, tools/k6_trace_probe.py --k5)
+      constexpr int UU = 4;
+      const int NTH = 128 * RT;
+      for (int ub = u0 + t; ub < u1; ub += UU * NTH) {
+        float4 w[UU][kMaxSplit];
 #pragma unroll
-        for (int p = 0; p < 8; ++p)
-          if (p < S) w[p] = ld_cluster_f4(la, (uint32_t)p);
-        float4 v = w[0];
+        for (int j = 0; j < UU; ++j)
 #pragma unroll
-        for (int p = 1; p < 8; ++p)
-          if (p < S) { v.x += w[p].x; v.y += w[p].y; v.z += w[p].z; v.w += w[p].w; }
-        const int n = u / RW, r4 = (u - n * RW) * 4;
-        const int64_t ng = n0 + n;
-        if (ng < a.N) {
-          raw_t* yp = (raw_t*)a.Y + ng * a.ldy + m0 + r4;
-          const float f[4] = {v.x, v.y, v.z, v.w};
+          for (int p = 0; p < kMaxSplit; ++p)
+            if (p < S && ub + j * NTH < u1) w[j][p] = ld_cluster_f4(sA + (uint32_t)(ub + j * NTH) * 16, (uint32_t)p);
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (r4 + e < mrows) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
+        for (int j = 0; j < UU; ++j) {
+          const int u = ub + j * NTH;
+          if (u >= u1) break;
+          float4 v = w[j][0];
+#pragma unroll
+          for (int p = 1; p < kMaxSplit; ++p)  // the fixed rank order (as K6)
+            if (p < S) { v.x += w[j][p].x; v.y += w[j][p].y; v.z += w[j][p].z; v.w += w[j][p].w; }
+          const int n = u / RW, r4 = (u - n * RW) * 4;
+          const int64_t ng = n0 + n;
+          if (ng < a.N) {
+            raw_t* yp = (raw_t*)a.Y + ng * a.ldy + m0 + r4;
+            const float f[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (r4 + e < mrows) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
+          }
         }
       }
     }
+    if (threadIdx.x == 64) K5_MARK(7);
     cluster_sync_all();
   }
+  if (threadIdx.x == 64) K5_MARK(8);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) {
@@ -497,7 +534,7 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   }
   {  // narrower column tiles when the row tiles × split leave SMs idle (bsk::fill_bn; S as computed below)
     int64_t Sf = pair ? 1 : bsk::dev_props().sms / tiles;
-    if (Sf > 8) Sf = 8;
+    if (Sf > kMaxSplit) Sf = kMaxSplit;
     if (Sf > (g.K / KCH) / bsk::splitk_min_chunks(6)) Sf = (g.K / KCH) / bsk::splitk_min_chunks(6);
     if (Sf < 1) Sf = 1;
     const int64_t rows_per_cta = pair ? BM : (int64_t)BM * RT;
@@ -537,7 +574,7 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   if (a.tmem_cols > 512) return cudaErrorNotSupported;
   const int64_t smem = 1024 + nst * stage;
   int64_t S = bsk::dev_props().sms / tiles;  // split-K: from M and K only (never N, never RT)
-  if (S > 8) S = 8;
+  if (S > kMaxSplit) S = kMaxSplit;
   // 6: a deeper split helped N <= 128 by 7% but cost 60% at N = 256 (A/B on CTC W_ih)
   const int mc = bsk::splitk_min_chunks(6);
   if (S > a.NC / mc) S = a.NC / mc;  // at least mc chunks per CTA: fixed costs stay amortised

@@ -16,20 +16,23 @@ import torch  # noqa: E402
 import paper_1811_00206_b200 as bs  # noqa: E402
 import synth  # noqa: E402
 
-bs.LIB_PATH = os.path.join(ROOT, "probe_bin", "libbs_k6trace.so")
-M, K, B, k, N = (int(v) for v in sys.argv[1:6])
+K5 = "--k5" in sys.argv  # the 2:4 kernel (libbs_k5trace.so, -DBS_TRACE_K5): marks 2 = first stage full
+argv = [a for a in sys.argv[1:] if a != "--k5"]
+bs.LIB_PATH = os.path.join(ROOT, "probe_bin", "libbs_k5trace.so" if K5 else "libbs_k6trace.so")
+M, K, B, k, N = (int(v) for v in argv[:5])
 W = synth.matrix(M, K, "f16", seed=3, device="cuda")
 v, i, _ = bs.prune(W, B, k=k)
-A = bs.pack(v, i, K, B, layout="spmm")
+A = bs.pack(v, i, K, B, layout="sp24" if K5 else "spmm")
 X = synth.vector(K, "f16", seed=4, n=N, device="cuda")
 Y = torch.empty((N, M), dtype=torch.float16, device="cuda")
 for _ in range(5):
     bs.spmm(A, X, out=Y)
 torch.cuda.synchronize()
 L = bs.lib()
-L.bs_k6_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
+rd = L.bs_k5_trace_read if K5 else L.bs_k6_trace_read
+rd.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = np.zeros(4096 * 16, dtype=np.uint64)
-L.bs_k6_trace_read(buf.ctypes.data, buf.size)
+rd(buf.ctypes.data, buf.size)
 T = buf.reshape(4096, 16).astype(np.float64)
 live = T[:, 0] > 0
 T = T[live]
