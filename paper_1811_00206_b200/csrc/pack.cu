@@ -80,6 +80,32 @@ __global__ void pack_kernel(const VT* __restrict__ vals, const uint16_t* __restr
 // contiguous run of region A) and its tail entries (regions B and C) are written in order, so both sides
 // of the permutation are coalesced and the index arithmetic is per row, not per entry (the per-entry
 // gather of pack_kernel needs six 64-bit divisions per entry). Used whenever a row fits shared memory.
+// Index runs of one row (docs/layout.md), NB_ = 5 (B = 32) or 4 (B <= 16) bits per index, V = 8, 16-bit
+// values: per (step, lane) the lane's 8 values (one 16-byte store) and its field sum_v idx << NB_·v (a word,
+// and a byte for 5-bit runs). The width is a template parameter: with a run-time shift the round-1 5-bit
+// pack ran 25 % slower (0.72 -> 0.90 ms at 65536^2).
+template <int NB_, typename VT>
+__device__ __forceinline__ void pack_runs(const VT* sv, const uint16_t* si, uint8_t* rowA, int64_t steps_row,
+                                          int64_t step_bytes, uint32_t P, int k, uint32_t run_off) {
+  constexpr uint32_t msk = (1u << NB_) - 1u;
+  for (uint32_t e = threadIdx.x; e < (uint32_t)steps_row * 32u; e += blockDim.x) {
+    const uint32_t st = e >> 5, l = e & 31u;
+    const uint32_t p = st / (uint32_t)k, t = st - p * (uint32_t)k;
+    uint64_t F = 0;
+    uint32_t vw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const uint32_t c = (p * P + v * 32u + l) * k + t;
+      F |= (uint64_t)(si[c] & msk) << (NB_ * v);
+      vw[v >> 1] |= (uint32_t)(uint16_t)sv[c] << (16 * (v & 1));
+    }
+    *(uint4*)(rowA + (int64_t)st * step_bytes + l * 16u) = make_uint4(vw[0], vw[1], vw[2], vw[3]);
+    uint8_t* run = rowA + (int64_t)st * step_bytes + run_off;
+    *(uint32_t*)(run + 4 * l) = (uint32_t)F;
+    if constexpr (NB_ == 5) run[128 + l] = (uint8_t)(F >> 32);
+  }
+}
+
 template <typename VT>
 __global__ void __launch_bounds__(512) pack_row_kernel(const VT* __restrict__ vals, const uint16_t* __restrict__ idx,
                                                        PackArgs a, uint8_t* __restrict__ base) {
@@ -129,27 +155,9 @@ __global__ void __launch_bounds__(512) pack_row_kernel(const VT* __restrict__ va
         if (a.is == 2) idst[1] = (uint8_t)(o >> 8);
       }
     }
-    if (runs) {  // 5-bit runs (B = 32) or 4-bit runs (B <= 16), V = 8, 16-bit values: per (step, lane) the
-                 // lane's 8 values (one 16-byte store) and its index field sum_v idx << nb·v (a word, and a
-                 // byte for nb = 5)
-      const int nb = a.ri == 160 ? 5 : 4;
-      const uint32_t msk = (1u << nb) - 1u;
-      for (uint32_t e = threadIdx.x; e < (uint32_t)steps_row * 32u; e += blockDim.x) {
-        const uint32_t st = e >> 5, l = e & 31u;
-        const uint32_t p = st / (uint32_t)k, t = st - p * (uint32_t)k;
-        uint64_t F = 0;
-        uint32_t vw[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const uint32_t c = (p * P + v * 32u + l) * k + t;
-          F |= (uint64_t)(si[c] & msk) << (nb * v);
-          vw[v >> 1] |= (uint32_t)(uint16_t)sv[c] << (16 * (v & 1));
-        }
-        *(uint4*)(rowA + (int64_t)st * step_bytes + l * 16u) = make_uint4(vw[0], vw[1], vw[2], vw[3]);
-        uint8_t* run = rowA + (int64_t)st * step_bytes + a.P * es;
-        *(uint32_t*)(run + 4 * l) = (uint32_t)F;
-        if (nb == 5) run[128 + l] = (uint8_t)(F >> 32);
-      }
+    if (runs) {  // 5-bit runs (B = 32) or 4-bit runs (B <= 16), V = 8, 16-bit values (pack_runs)
+      if (a.ri == 160) pack_runs<5>(sv, si, rowA, steps_row, step_bytes, P, k, (uint32_t)(a.P * es));
+      else pack_runs<4>(sv, si, rowA, steps_row, step_bytes, P, k, (uint32_t)(a.P * es));
     }
     // regions B / C: the row's tail, element t·T + q (q = v·32 + l) = block NBf·P + q, entry t
     if (kT > 0) {

@@ -9,6 +9,9 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_1811_00206_b200 as bs  # noqa: E402
+
+if os.environ.get("BS_LIB"):  # A/B against another build of the same ABI
+    bs.LIB_PATH = os.environ["BS_LIB"]
 import synth  # noqa: E402
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
