@@ -44,10 +44,21 @@ extern "C" int bs_k6_trace_read(void* host, int n) { return (int)cudaMemcpyFromS
     const unsigned cta_ = blockIdx.x + gridDim.x * blockIdx.y;                                                  \
     if (cta_ < 4096) g_k6_trace[cta_ * 16 + (i)] = t_;                                                          \
   } while (0)
+// cycle accounting of the waits (clock64; globaltimer ticks are too coarse for ~200 ns chunks)
+#define K6_TIC(t) t = clock64()
+#define K6_TOC(acc, t) acc += clock64() - (t)
+#define K6_STORE(i, v)                                                                                          \
+  do {                                                                                                          \
+    const unsigned cta_ = blockIdx.x + gridDim.x * blockIdx.y;                                                  \
+    if (cta_ < 4096) g_k6_trace[cta_ * 16 + (i)] = (unsigned long long)(v);                                     \
+  } while (0)
 #else
 #define K6_MARK(i) \
   do {             \
   } while (0)
+#define K6_TIC(t) (void)0
+#define K6_TOC(acc, t) (void)0
+#define K6_STORE(i, v) (void)0
 #endif
 
 namespace {
@@ -149,9 +160,12 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
       if (warp == 0) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tX) : "memory");
       int s = warp % NSB;
       uint32_t ph = 0;
+      [[maybe_unused]] long long tw_ = 0, c_empty = 0;
       for (int i = warp; i < nloc; i += kProducers) {
         const int c = c0 + i;
+        K6_TIC(tw_);
         if (i >= NSB) mbar_wait(empty + 8 * s, ph ^ 1u);
+        K6_TOC(c_empty, tw_);
         const int64_t cb = (a.NB - (int64_t)a.CB * c) < a.CB ? (a.NB - (int64_t)a.CB * c) : a.CB;
         const uint32_t bytes = blob_bytes(cb);
         mbar_expect_tx(full + 8 * s, bytes + XSZ);
@@ -160,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
         s += kProducers;
         if (s >= NSB) { s -= NSB; ph ^= 1u; }
       }
+      if (warp == 0) K6_STORE(9, c_empty);
     }
   } else if (warp < kFirstDecomp / 32) {
     if (lane == 0) {  // ---- MMA issuers: warp j issues chunks i = j, j + kMmaWarps, ... into accumulator j
@@ -167,10 +182,16 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
       const uint32_t acc_j = tmem_d + (uint32_t)(j * a.acc_cols);
       int s = j % NSB;
       uint32_t ph = 0;
+      [[maybe_unused]] long long tw_ = 0, c_full = 0, c_afull = 0, c_issue = 0;
       for (int i = j; i < nloc; i += kMmaWarps) {
         const int ab = i & (NA - 1);
+        K6_TIC(tw_);
         mbar_wait(full + 8 * s, ph);
+        K6_TOC(c_full, tw_);
+        K6_TIC(tw_);
         mbar_wait(a_full + 8 * ab, (uint32_t)(i >> lg_na) & 1u);
+        K6_TOC(c_afull, tw_);
+        K6_TIC(tw_);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint64_t da = sw128_desc(sA + (uint32_t)ab * BM * 128), db = sw128_desc(sX + (uint32_t)s * XSZ);
 #pragma unroll
@@ -185,8 +206,14 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
                      : "memory");
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(a_empty + 8 * ab)
                      : "memory");
+        K6_TOC(c_issue, tw_);
         s += kMmaWarps;
         if (s >= NSB) { s -= NSB; ph ^= 1u; }
+      }
+      if (j == 0) {
+        K6_STORE(10, c_full);
+        K6_STORE(11, c_afull);
+        K6_STORE(12, c_issue);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(acc_full)
                    : "memory");
@@ -206,14 +233,20 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
     const int cbF = a.CB, cbL = (int)(a.NB - (int64_t)a.CB * (a.NC - 1));
     int s = grp;  // ring stage of chunk i
     uint32_t ph = 0;
+    [[maybe_unused]] long long tw_ = 0, c_aempty = 0, c_dfull = 0, c_work = 0;
     for (int i = grp; i < nloc; i += kGroups) {
       const int ab = i & (NA - 1);
       const uint32_t aph = (uint32_t)(i >> lg_na) & 1u;
       const uint32_t aT = sA + (uint32_t)ab * BM * 128;
       const int cb = i == ilast ? cbL : cbF;
       const int n_e = (int)mt * cb * k;
+      K6_TIC(tw_);
       if (i >= NA) mbar_wait(a_empty + 8 * ab, aph ^ 1u);  // MMA done with this A tile
+      K6_TOC(c_aempty, tw_);
+      K6_TIC(tw_);
       mbar_wait(full + 8 * s, ph);
+      K6_TOC(c_dfull, tw_);
+      K6_TIC(tw_);
       if (t == 0 && grp == 0 && i == 0) K6_MARK(2);
       // 32-bit shared addresses (a generic pointer here would compile to LD.E with 64-bit math)
       const uint32_t bv = sR + (uint32_t)s * (uint32_t)a.blob_max;
@@ -251,8 +284,14 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core
       mbar_arrive(a_full + 8 * ab);
+      K6_TOC(c_work, tw_);
       s += kGroups;
       if (s >= NSB) { s -= NSB; ph ^= 1u; }
+    }
+    if (t == 0 && grp == 0) {
+      K6_STORE(13, c_aempty);
+      K6_STORE(14, c_dfull);
+      K6_STORE(15, c_work);
     }
     // ---- epilogue: TMEM -> registers. Warp w reads lane quarter w % 4 (rows 32·(w % 4) + lane) and
     // column part (w - 2) / 4 of NP parts.

@@ -38,6 +38,14 @@ live = T[:, 0] > 0
 T = T[live]
 t0 = T[:, 0].min()
 print(f"M={M} K={K} B={B} k={k} N={N}: {live.sum()} CTAs")
+names = {9: "producer 0: cycles waiting for empty stages", 10: "MMA warp 0: cycles waiting for full stages",
+         11: "MMA warp 0: cycles waiting for A tiles", 12: "MMA warp 0: cycles issuing (fence, MMAs, commits)",
+         13: "decompress group 0: cycles waiting for free A tiles", 14: "decompress group 0: cycles waiting for stages",
+         15: "decompress group 0: cycles decompressing"}
+if not K5:
+    for m, nm in names.items():
+        col = buf.reshape(4096, 16)[live][:, m].astype(np.float64)
+        print(f"  {nm}: p50 {np.percentile(col, 50):9.0f}  max {col.max():9.0f}")
 for m in range(9):
     col = T[:, m]
     col = col[col > 0]
