@@ -189,7 +189,9 @@ int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_
               int stride, void* X, int64_t ldx, void* stream);
 
 /* bs_pack: permute canonical (vals, idx) into the device layout `layout` and narrow the indices
- * (docs/layout.md). This is a pure permutation, so the output is byte-exact. The paper stores "the
+ * (docs/layout.md: u8 for block <= 256, u16 above; in SPMV panels of 16-bit values with V = 8, 5-bit index
+ * runs for block == 32 and 4-bit runs for block <= 16). This is a pure permutation, so the output is
+ * byte-exact. The paper stores "the
  * same number of non-zero values in each block partition", so the format needs no row
  * pointers. `packed` receives bs_packed_bytes(...) bytes; alignment padding bytes are zeroed.
  * Errors: as bs_prune_k; BS_ERR_UNSUPPORTED for SP24 unless block == 4, k == 2 and K mod 8 == 0. */
