@@ -687,7 +687,7 @@ def cusparselt_time(Wbs, X) -> dict:
 
 def conv_rows(a, bs, l2):
     """NEXT-3: VGG-16 conv layers of Table cnn-perf at batch 1, 224x224 input geometry, with
-    the paper's balanced sparsity for each layer, run as im2col + bs_spmm (layout by bs_choose_layout)
+    the paper's balanced sparsity for each layer, run as bs_conv2d (implicit im2col) or im2col + bs_spmm
     against cuDNN (torch conv2d, channels_last, f16) on the dense W_bs. CUDA-graph timed."""
     rows = []
     dev = torch.device("cuda")
@@ -703,19 +703,25 @@ def conv_rows(a, bs, l2):
         inp = synth.vector(HW * HW * C, a.dtype, seed=synth.seed_for(6, 1), device=dev).view(1, HW, HW, C)
         X = torch.empty((N, Kc), dtype=Wm.dtype, device=dev)
         Y = torch.empty((N, Cout), dtype=Wm.dtype, device=dev)
-        t_ours = graph_time_us(lambda j: bs.spmm(A, bs.im2col(inp, 3, 3, 1, 1, out=X), out=Y), 20)
+        t_explicit = graph_time_us(lambda j: bs.spmm(A, bs.im2col(inp, 3, 3, 1, 1, out=X), out=Y), 20)
         t_im2col = graph_time_us(lambda j: bs.im2col(inp, 3, 3, 1, 1, out=X), 20)
+        implicit = lay == "spmm" and C % 64 == 0
+        t_ours = graph_time_us(lambda j: bs.conv2d(A, inp, 3, 3, pad=1), 20) if implicit else t_explicit
         Wd = dense_from_canonical(v, i, Cout, Kc, a.block).view(Cout, 3, 3, C).permute(0, 3, 1, 2)
         Wd = Wd.contiguous(memory_format=torch.channels_last)
         xin = inp.permute(0, 3, 1, 2)  # NHWC storage = channels_last NCHW view
         t_cudnn = graph_time_us(lambda j: torch.nn.functional.conv2d(xin, Wd, padding=1), 20)
         rows.append({"layer": name, "C": C, "Cout": Cout, "HW": HW, "sparsity": s, "k": ks, "N": N, "layout": lay,
-                     "ours_us": round(t_ours, 2), "im2col_us": round(t_im2col, 2), "cudnn_dense_us": round(t_cudnn, 2),
+                     "ours_us": round(t_ours, 2), "path": "bs_conv2d (TMA im2col)" if implicit else "bs_im2col + bs_spmm",
+                     "explicit_im2col_spmm_us": round(t_explicit, 2), "im2col_us": round(t_im2col, 2),
+                     "cudnn_dense_us": round(t_cudnn, 2),
                      "speedup_vs_cudnn": round(t_cudnn / t_ours, 2),
                      "TFLOPs_nnz": round(2.0 * Cout * (Kc // a.block) * ks * N / t_ours / 1e6, 2)})
         del A, v, i, Wm, Wd, X, Y
-    return {"conv": rows, "conv_note": "ours = bs_im2col + bs_spmm (NHWC, one weight matrix per layer, P:107/P:286); "
-                                       "cudnn = torch conv2d channels_last on the dense W_bs; batch 1"}
+    return {"conv": rows, "conv_note": "ours = bs_conv2d (implicit im2col: the tensor cores' X tiles loaded by TMA in "
+                                       "im2col mode from the NHWC input) where eligible, else bs_im2col + bs_spmm (NHWC, "
+                                       "one weight matrix per layer, P:107/P:286); cudnn = torch conv2d channels_last on "
+                                       "the dense W_bs; batch 1"}
 
 
 def lstm_rows(a, bs, l2):

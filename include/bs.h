@@ -188,6 +188,19 @@ int bs_block_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int6
 int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw, int pad,
               int stride, void* X, int64_t ldx, void* stream);
 
+/* bs_conv2d: a convolution layer as one balanced-sparse product with implicit im2col ("im2col that
+ * converts convolution operation to matrix-matrix multiplication"; all kernels of a layer form one
+ * weight matrix): Y [Nimg·OH·OW][M] = W_bs · im2col(in)ᵀ, i.e. the NHWC output [Nimg][OH][OW][Cout = M],
+ * with in NHWC [Nimg][H][W][C] (16-bit, 16-byte aligned) and W_bs's columns in (dy, dx, c) order (reading
+ * A23; A->K = kh·kw·C). The tensor cores' X tiles are loaded straight from `in` by TMA in im2col mode, so
+ * no [pixels][kh·kw·C] intermediate exists; the result is bit-identical to bs_im2col + bs_spmm.
+ * Requirements: layout SPMM, f16/bf16, block | 64, C % 64 == 0, stride 1. Y has room for
+ * Nimg·OH·OW·M elements of A's dtype (caller-owned).
+ * Errors: BS_ERR_SHAPE for inconsistent shapes; BS_ERR_ARG for NULL pointers; BS_ERR_UNSUPPORTED when an
+ * eligibility condition fails (use bs_im2col + bs_spmm then); BS_ERR_CUDA on a launch failure. */
+int bs_conv2d(const bs_matrix* A, const void* in, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw,
+              int pad, int stride, void* Y, void* stream);
+
 /* bs_pack: permute canonical (vals, idx) into the device layout `layout` and narrow the indices
  * (docs/layout.md: u8 for block <= 256, u16 above; in SPMV panels of 16-bit values with V = 8, 5-bit index
  * runs for block == 32 and 4-bit runs for block <= 16). This is a pure permutation, so the output is

@@ -31,7 +31,7 @@ EXPORTS = ("bs_k_from_sparsity", "bs_packed_bytes", "bs_status_str", "bs_version
            "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm", "bs_choose_layout", "bs_block_rank",
            "bs_schedule_sparsity", "bs_keep_count", "bs_decode", "bs_pattern_workspace_bytes", "bs_random_mask",
            "bs_block_mask", "bs_lstm_step", "bs_im2col", "bs_spmv_allgather", "bs_allgather_wait", "bs_peer_export",
-           "bs_peer_import", "bs_peer_close", "bs_x_slot_offset")
+           "bs_peer_import", "bs_peer_close", "bs_x_slot_offset", "bs_conv2d")
 ACTS = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}  # bs_act (include/bs.h)
 SPMV_PDL, SPMV_W_STATIC, SPMV_RING = 1, 2, 4  # bs_spmv_ex flags (include/bs.h)
 
@@ -92,6 +92,7 @@ def _load() -> ctypes.CDLL:
     L.bs_block_mask.argtypes = [vp, ci, i64, i64, i64, i64, i64, ctypes.c_double, ci, vp, vp, ctypes.c_size_t, vp]
     L.bs_lstm_step.argtypes = [ctypes.POINTER(_Matrix), vp, vp, vp, vp, vp, vp, ctypes.c_uint, vp]
     L.bs_im2col.argtypes = [vp, ci, i64, i64, i64, i64, ci, ci, ci, ci, vp, i64, vp]
+    L.bs_conv2d.argtypes = [ctypes.POINTER(_Matrix), vp, i64, i64, i64, i64, ci, ci, ci, ci, vp, vp]
     L.bs_x_slot_offset.argtypes = [i64, ci, ci, ci, i64, ci, ci]
     L.bs_x_slot_offset.restype = i64
     L.bs_spmv_allgather.argtypes = [ctypes.POINTER(_Matrix), vp, vp, ci, ctypes.POINTER(_AllGather), ctypes.c_uint, vp]
@@ -99,7 +100,7 @@ def _load() -> ctypes.CDLL:
     L.bs_peer_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_int64)]
     L.bs_peer_import.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]
     L.bs_peer_close.argtypes = [vp, ctypes.c_int64]
-    for f in ("bs_decode", "bs_random_mask", "bs_block_mask", "bs_lstm_step", "bs_im2col", "bs_spmv_allgather",
+    for f in ("bs_decode", "bs_random_mask", "bs_block_mask", "bs_lstm_step", "bs_im2col", "bs_conv2d", "bs_spmv_allgather",
               "bs_allgather_wait", "bs_peer_export", "bs_peer_import", "bs_peer_close"):
         getattr(L, f).restype = ci
     for f in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm"):
@@ -567,14 +568,32 @@ def im2col(inp: torch.Tensor, kh: int, kw: int, pad: int = 0, stride: int = 1, o
 
 
 def conv2d(A: BSMatrix, inp: torch.Tensor, kh: int, kw: int, pad: int = 0, stride: int = 1,
-           workspace: torch.Tensor | None = None) -> torch.Tensor:
-    """A conv layer with the balanced-sparse Cout × (kh·kw·C) weight matrix A: im2col then bs_spmm.
-    NHWC in [Nimg, H, W, C], NHWC out [Nimg, OH, OW, Cout]."""
+           workspace: torch.Tensor | None = None, implicit: bool | None = None) -> torch.Tensor:
+    """A conv layer with the balanced-sparse Cout × (kh·kw·C) weight matrix A. NHWC in [Nimg, H, W, C], NHWC out
+    [Nimg, OH, OW, Cout]. implicit=None: bs_conv2d (TMA im2col feeding the tensor cores, no intermediate) when
+    eligible (SPMM layout, 16-bit, C % 64 == 0, stride 1), else bs_im2col then bs_spmm; True/False forces one."""
+    _need_cuda(inp)
     Nimg, H, W, C = inp.shape
     if A.K != kh * kw * C:
         raise ValueError("A.K must equal kh·kw·C")
-    X = im2col(inp, kh, kw, pad, stride, out=workspace)
+    if inp.dtype != A.dtype:
+        raise ValueError("inp must have A.dtype")
+    _same_device(A, inp)
     OH, OW = (H + 2 * pad - kh) // stride + 1, (W + 2 * pad - kw) // stride + 1
+    if implicit is not False:
+        ok = A.layout == "spmm" and A.dtype != torch.float32 and C % 64 == 0 and stride == 1 and A.k > 0
+        if ok or implicit:
+            x = inp.contiguous()
+            Y = torch.empty((Nimg, OH, OW, A.M), dtype=A.dtype, device=inp.device)
+            m = A.cstruct()
+            with torch.cuda.device(inp.device):
+                st = lib().bs_conv2d(ctypes.byref(m), x.data_ptr(), Nimg, H, W, C, kh, kw, pad, stride, Y.data_ptr(),
+                                     _stream(inp.device))
+            if st == 0:
+                return Y
+            if implicit or st != BS_ERR_UNSUPPORTED:
+                _check(st, "bs_conv2d")
+    X = im2col(inp, kh, kw, pad, stride, out=workspace)
     return spmm(A, X).view(Nimg, OH, OW, A.M)
 
 

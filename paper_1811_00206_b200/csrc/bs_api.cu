@@ -252,6 +252,21 @@ int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_
   return from_cuda(bsk_launch_im2col(in, dt, Nimg, H, W, C, kh, kw, pad, stride, X, ldx, (cudaStream_t)stream));
 }
 
+int bs_conv2d(const bs_matrix* A, const void* in, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw,
+              int pad, int stride, void* Y, void* stream) {
+  bsk::Geom g;
+  int st = matrix_geom(A, &g);
+  if (st) return st;
+  if (Nimg < 1 || H < 1 || W < 1 || C < 1 || kh < 1 || kw < 1 || pad < 0 || stride < 1) return BS_ERR_SHAPE;
+  if (g.K != (int64_t)kh * kw * C) return BS_ERR_SHAPE;
+  if (H + 2 * pad < kh || W + 2 * pad < kw) return BS_ERR_SHAPE;
+  if (!in || !Y) return BS_ERR_ARG;
+  if (stride != 1) return BS_ERR_UNSUPPORTED;
+  const cudaError_t e = bsk_launch_conv(g, A->packed, in, Nimg, H, W, C, kh, kw, pad, Y, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported) return BS_ERR_UNSUPPORTED;
+  return from_cuda(e);
+}
+
 int64_t bs_x_slot_offset(int64_t K, int block, int dt, int nv, int64_t b, int o, int part) {
   bsk::Geom g;
   if (!bsk::make_geom(1, K, block, 1, dt, BS_LAYOUT_SPMV, &g)) return -1;

@@ -103,7 +103,24 @@ __device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// 4-D tensor copy in im2col mode (implicit im2col for convolution): a column of pixels × channels of an
+// NHWC tensor starting at base pixel (w, h, n), channel c, each pixel displaced by the filter offset
+// (dw, dh); pixels outside the tensor read as zeros
+__device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
+                                              uint16_t dw, uint16_t dh, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar), "h"(dw), "h"(dh)
+      : "memory");
+}
+
 }  // namespace bsk_tc
+
+// Im2col tensor map of an NHWC 16-bit tensor [Nimg][H][W][C] for a kh × kw, stride-1 convolution with
+// symmetric padding `pad`: columns of `pixels` output positions × 64 channels, 128-byte swizzle (the X tile
+// layout of K6). Returns false if the driver entry point is missing or the encoding is rejected.
+bool bsk_make_map_im2col(CUtensorMap* m, int dt, const void* in, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh,
+                         int kw, int pad, int pixels);
 
 // 2-D tensor map of a row-major [rows][cols] 16-bit matrix (dt f16 / bf16) with row stride `ld`
 // elements; box of bc columns × br rows, 128-byte swizzle, zero fill out of bounds. Returns false if

@@ -92,6 +92,8 @@ struct TcArgs {
   uint32_t idesc;
   int tmem_cols, acc_cols;  // allocated columns; columns per accumulator (one per MMA warp)
   int colfast;        // grid order (bsk::tc_cols_fast)
+  // implicit im2col (bs_conv2d): X is the im2col of an NHWC input, loaded by TMA in im2col mode
+  int conv, cC, cKW, cOW, cOHW, cPad;
 };
 
 template <int DT>
@@ -170,7 +172,16 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
         const uint32_t bytes = blob_bytes(cb);
         mbar_expect_tx(full + 8 * s, bytes + XSZ);
         bulk_g2s(sR + (uint32_t)s * (uint32_t)a.blob_max, tile_base + (int64_t)c * blobCB, bytes, full + 8 * s);
-        tma_2d(sX + (uint32_t)s * XSZ, &tX, c * KC, (int)n0, full + 8 * s);
+        if (a.conv) {  // chunk c = 64 channels of one filter tap (dy, dx); the column tile starts at pixel n0
+          const int col0 = c * KC, tap = col0 / a.cC, coff = col0 - tap * a.cC;
+          const int dy = tap / a.cKW, dx = tap - dy * a.cKW;
+          const int img = (int)(n0 / a.cOHW), pix = (int)(n0 - (int64_t)img * a.cOHW);
+          const int oy = pix / a.cOW, ox = pix - oy * a.cOW;
+          tma_im2col_4d(sX + (uint32_t)s * XSZ, &tX, coff, ox - a.cPad, oy - a.cPad, img, (uint16_t)dx, (uint16_t)dy,
+                        full + 8 * s);
+        } else {
+          tma_2d(sX + (uint32_t)s * XSZ, &tX, c * KC, (int)n0, full + 8 * s);
+        }
         s += kProducers;
         if (s >= NSB) { s -= NSB; ph ^= 1u; }
       }
@@ -429,11 +440,24 @@ int split_k(int64_t tiles, int64_t NC) {
   return S < 1 ? 1 : (int)S;
 }
 
+struct ConvGeom {  // implicit im2col input of bsk_launch_conv (NHWC, stride 1)
+  int64_t Nimg, H, W, C;
+  int kh, kw, pad;
+};
+
 template <int DT>
 cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
-                      int64_t ldy, cudaStream_t s) {
-  if (((uintptr_t)X & 15) != 0 || (ldx % 8) != 0) return cudaErrorNotSupported;  // TMA: 16-byte rows
+                      int64_t ldy, cudaStream_t s, const ConvGeom* cv = nullptr) {
+  if (!cv && (((uintptr_t)X & 15) != 0 || (ldx % 8) != 0)) return cudaErrorNotSupported;  // TMA: 16-byte rows
   TcArgs a;
+  a.conv = cv != nullptr;
+  if (cv) {
+    a.cC = (int)cv->C;
+    a.cKW = cv->kw;
+    a.cOW = (int)(cv->W + 2 * cv->pad - cv->kw + 1);
+    a.cOHW = (int)((cv->H + 2 * cv->pad - cv->kh + 1) * a.cOW);
+    a.cPad = cv->pad;
+  }
   a.W = (const uint8_t*)packed;
   a.Y = Y;
   a.M = g.M; a.NB = g.NB; a.N = N; a.ldy = ldy;
@@ -476,7 +500,12 @@ cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int
   const int64_t smem = 1024 + (int64_t)a.NA * BM * 128 + nsb * (BN * 128 + a.blob_max);
   if (a.S > 1 && BN * BM * 4 > smem - 1024) return cudaErrorNotSupported;  // partial tile must fit
   CUtensorMap tX;
-  if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, KC, (int)BN)) return cudaErrorNotSupported;
+  if (cv) {
+    if (!bsk_make_map_im2col(&tX, DT, X, cv->Nimg, cv->H, cv->W, cv->C, cv->kh, cv->kw, cv->pad, (int)BN))
+      return cudaErrorNotSupported;
+  } else if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, KC, (int)BN)) {
+    return cudaErrorNotSupported;
+  }
   cudaLaunchConfig_t cfg = {};
   // column tiles adjacent only when W exceeds half of L2 (fc6, 31 MB, ran 10 % slower at N = 128 with them)
   a.colfast = bsk::tc_cols_fast() && g.P <= 65535 && g.total > (int64_t)bsk::dev_props().l2_bytes / 2;
@@ -509,6 +538,24 @@ cudaError_t launch_cc(const bsk::Geom& g, const void* packed, const void* X, int
 }
 
 }  // namespace
+
+// Convolution with implicit im2col (bs_conv2d): Y [pixels][Cout] = W_bs · im2col(in)ᵀ with the X tiles loaded
+// straight from the NHWC input by TMA in im2col mode (no im2col kernel, no [pixels][kh·kw·C] intermediate).
+// Eligible: SPMM layout, 16-bit, B | 64, C % 64 == 0 (a 64-column chunk is one filter tap), stride 1,
+// symmetric padding, a 16-byte aligned input; cudaErrorNotSupported otherwise.
+cudaError_t bsk_launch_conv(const bsk::Geom& g, const void* packed, const void* in, int64_t Nimg, int64_t H, int64_t W,
+                            int64_t C, int kh, int kw, int pad, void* Y, cudaStream_t s) {
+  if (g.layout != BS_LAYOUT_SPMM || g.es != 2 || (64 % g.B) != 0 || g.k == 0) return cudaErrorNotSupported;
+  if (C % 64 != 0 || g.K != (int64_t)kh * kw * C || ((uintptr_t)in & 15) != 0) return cudaErrorNotSupported;
+  if (pad > 127 || kh > 128 || kw > 128) return cudaErrorNotSupported;
+  const int64_t OH = H + 2 * pad - kh + 1, OW = W + 2 * pad - kw + 1;
+  if (OH < 1 || OW < 1) return cudaErrorNotSupported;
+  const int64_t N = Nimg * OH * OW;
+  if (N >= (1LL << 31)) return cudaErrorNotSupported;
+  const ConvGeom cv{Nimg, H, W, C, kh, kw, pad};
+  return g.dt == BS_BF16 ? launch_tc<BS_BF16>(g, packed, in, N, g.K, Y, g.M, s, &cv)
+                         : launch_tc<BS_F16>(g, packed, in, N, g.K, Y, g.M, s, &cv);
+}
 
 // Returns cudaErrorNotSupported when the caller should fall back to column-at-a-time SpMV
 // (SPMV layout).

@@ -651,6 +651,35 @@ bool bsk_make_map_2d(CUtensorMap* m, int dt, const void* base, int64_t cols, int
          CUDA_SUCCESS;
 }
 
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+bool bsk_make_map_im2col(CUtensorMap* m, int dt, const void* in, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh,
+                         int kw, int pad, int pixels) {
+  static EncodeIm2colFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeIm2colFn)p;
+  }
+  if (!fn) return false;
+  // dims innermost first: C, W, H, N. The base pixels of the output positions run over
+  // [-pad, extent - 1 + pad - (k - 1)] in each spatial dimension (stride 1).
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)Nimg};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)(W * C * 2), (cuuint64_t)(H * W * C * 2)};
+  int lower[2] = {-pad, -pad};
+  int upper[2] = {pad - (kw - 1), pad - (kh - 1)};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUtensorMapDataType t = dt == BS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  return fn(m, t, 4, const_cast<void*>(in), dims, strides, lower, upper, 64, (cuuint32_t)pixels, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Y = W·X for W in SP24 layout.
 //   spmv (bs_spmv, N = 1): the HBM-bound CUDA-core SpMV with 16-byte loads.
 //   otherwise (bs_spmm): the sparse tensor cores whenever the operands allow it (f16/bf16, K % 128 == 0,

@@ -88,3 +88,44 @@ def test_conv_weight_matrix_matches_torch(bs):
     Wm = bs.conv_weight_matrix(w)
     X = torch.from_numpy(oracle.im2col(x.permute(0, 2, 3, 1).contiguous().float().numpy(), oracle.F32, 3, 3, 1, 1)).double()
     assert torch.allclose(X @ Wm.T, ref, atol=1e-5)
+
+
+@pytest.mark.parametrize("Nimg,H,W,C,Cout,kh,kw,pad,dname,B,s", [
+    (1, 8, 8, 256, 256, 3, 3, 1, "f16", 32, 0.88),    # conv3_3-like
+    (2, 7, 5, 64, 128, 3, 3, 1, "bf16", 32, 0.9),     # two images: pixel columns run across the image border
+    (1, 14, 14, 512, 512, 3, 3, 1, "f16", 16, 0.75),  # B = 16, conv4_x width
+    (1, 9, 6, 128, 64, 3, 1, 1, "f16", 32, 0.9),      # kh != kw: corner and filter-offset order
+    (1, 5, 5, 64, 32, 1, 1, 0, "bf16", 32, 0.5),      # 1x1
+    (3, 4, 4, 64, 200, 5, 5, 2, "f16", 32, 0.9),      # 5x5, pad 2, ragged Cout
+])
+def test_conv2d_implicit_im2col_matches_explicit(bs, Nimg, H, W, C, Cout, kh, kw, pad, dname, B, s):
+    """bs_conv2d (X tiles loaded by TMA in im2col mode straight from the NHWC input) against bs_im2col +
+    bs_spmm on the same matrix: the same X values reach the same MMAs in the same order, so the outputs
+    are bit-identical; and against the oracle's direct convolution on integer-exact data, bit for bit."""
+    Kc = kh * kw * C
+    k = bs.k_from_sparsity(B, s)
+    Wm = synth.matrix(Cout, Kc, dname, seed=synth.seed_for(53, Cout + C + kh))
+    vals, idx, _ = bs.prune(Wm.cuda(), B, k=k)
+    A = bs.pack(vals, idx, Kc, B, layout="spmm")
+    inp = _img(Nimg, H, W, C, dname, synth.seed_for(53, 9)).cuda()
+    Yi = bs.conv2d(A, inp, kh, kw, pad=pad, implicit=True)
+    Ye = bs.conv2d(A, inp, kh, kw, pad=pad, implicit=False)
+    assert torch.equal(Yi, Ye)
+    Wi = synth.matrix(Cout, Kc, dname, family="intexact", seed=synth.seed_for(53, 1))
+    vi, ii, _ = bs.prune(Wi.cuda(), B, k=k)
+    Ai = bs.pack(vi, ii, Kc, B, layout="spmm")
+    xi = _img(Nimg, H, W, C, dname, synth.seed_for(53, 2), family="intexact")
+    Y = bs.conv2d(Ai, xi.cuda(), kh, kw, pad=pad, implicit=True)
+    ov, oi = oracle.prune(synth.to_numpy(Wi), DT[dname], B, k)
+    ref, _ = oracle.conv2d(ov, oi, DT[dname], Cout, B, k, synth.to_numpy(xi), kh, kw, pad, 1)
+    np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(Y), DT[dname]).reshape(ref.shape), ref)
+
+
+def test_conv2d_implicit_errors(bs):
+    Wm = synth.matrix(64, 9 * 32, "f16", seed=5).cuda()
+    v, i, _ = bs.prune(Wm, 32, k=3)
+    inp = _img(1, 6, 6, 32, "f16", 6).cuda()
+    with pytest.raises(bs.BSError):   # C % 64 != 0: not eligible when forced
+        bs.conv2d(bs.pack(v, i, 9 * 32, 32, layout="spmm"), inp, 3, 3, pad=1, implicit=True)
+    Y = bs.conv2d(bs.pack(v, i, 9 * 32, 32, layout="spmm"), inp, 3, 3, pad=1)  # auto: falls back to im2col
+    assert Y.shape == (1, 6, 6, 64)
