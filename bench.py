@@ -711,11 +711,18 @@ def conv_rows(a, bs, l2):
         Wd = Wd.contiguous(memory_format=torch.channels_last)
         xin = inp.permute(0, 3, 1, 2)  # NHWC storage = channels_last NCHW view
         t_cudnn = graph_time_us(lambda j: torch.nn.functional.conv2d(xin, Wd, padding=1), 20)
+        bvec = synth.vector(Cout, a.dtype, seed=synth.seed_for(6, 2), device=dev)
+        extra = {}
+        if implicit:  # the VGG layer as it runs: conv + bias + ReLU, fused into bs_conv2d's epilogue
+            extra["ours_bias_relu_us"] = round(graph_time_us(lambda j: bs.conv2d(A, inp, 3, 3, pad=1, bias=bvec,
+                                                                                  act="relu"), 20), 2)
+            extra["cudnn_bias_relu_us"] = round(graph_time_us(
+                lambda j: torch.relu(torch.nn.functional.conv2d(xin, Wd, bvec, padding=1)), 20), 2)
         rows.append({"layer": name, "C": C, "Cout": Cout, "HW": HW, "sparsity": s, "k": ks, "N": N, "layout": lay,
                      "ours_us": round(t_ours, 2), "path": "bs_conv2d (TMA im2col)" if implicit else "bs_im2col + bs_spmm",
                      "explicit_im2col_spmm_us": round(t_explicit, 2), "im2col_us": round(t_im2col, 2),
                      "cudnn_dense_us": round(t_cudnn, 2),
-                     "speedup_vs_cudnn": round(t_cudnn / t_ours, 2),
+                     "speedup_vs_cudnn": round(t_cudnn / t_ours, 2), **extra,
                      "TFLOPs_nnz": round(2.0 * Cout * (Kc // a.block) * ks * N / t_ours / 1e6, 2)})
         del A, v, i, Wm, Wd, X, Y
     return {"conv": rows, "conv_note": "ours = bs_conv2d (implicit im2col: the tensor cores' X tiles loaded by TMA in "

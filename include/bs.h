@@ -196,10 +196,15 @@ int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_
  * no [pixels][kh·kw·C] intermediate exists; the result is bit-identical to bs_im2col + bs_spmm.
  * Requirements: layout SPMM, f16/bf16, block | 64, C % 64 == 0, stride 1. Y has room for
  * Nimg·OH·OW·M elements of A's dtype (caller-owned).
- * Errors: BS_ERR_SHAPE for inconsistent shapes; BS_ERR_ARG for NULL pointers; BS_ERR_UNSUPPORTED when an
- * eligibility condition fails (use bs_im2col + bs_spmm then); BS_ERR_CUDA on a launch failure. */
+ * Layer epilogue (Eq. 1's +B, and the activation that follows a VGG conv layer): `bias` (M elements
+ * of A's dtype, one per output channel, or NULL) is added and `act` (bs_act) applied in fp32 before the
+ * one rounding to A's dtype, with bs_spmv_fused's expressions. bias = NULL and act = BS_ACT_NONE give the
+ * plain product.
+ * Errors: BS_ERR_SHAPE for inconsistent shapes; BS_ERR_ARG for NULL pointers or an unknown act;
+ * BS_ERR_UNSUPPORTED when an eligibility condition fails (use bs_im2col + bs_spmm then); BS_ERR_CUDA on a
+ * launch failure. */
 int bs_conv2d(const bs_matrix* A, const void* in, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw,
-              int pad, int stride, void* Y, void* stream);
+              int pad, int stride, const void* bias, int act, void* Y, void* stream);
 
 /* bs_pack: permute canonical (vals, idx) into the device layout `layout` and narrow the indices
  * (docs/layout.md: u8 for block <= 256, u16 above; in SPMV panels of 16-bit values with V = 8, 5-bit index

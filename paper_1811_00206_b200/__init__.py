@@ -92,7 +92,7 @@ def _load() -> ctypes.CDLL:
     L.bs_block_mask.argtypes = [vp, ci, i64, i64, i64, i64, i64, ctypes.c_double, ci, vp, vp, ctypes.c_size_t, vp]
     L.bs_lstm_step.argtypes = [ctypes.POINTER(_Matrix), vp, vp, vp, vp, vp, vp, ctypes.c_uint, vp]
     L.bs_im2col.argtypes = [vp, ci, i64, i64, i64, i64, ci, ci, ci, ci, vp, i64, vp]
-    L.bs_conv2d.argtypes = [ctypes.POINTER(_Matrix), vp, i64, i64, i64, i64, ci, ci, ci, ci, vp, vp]
+    L.bs_conv2d.argtypes = [ctypes.POINTER(_Matrix), vp, i64, i64, i64, i64, ci, ci, ci, ci, vp, ci, vp, vp]
     L.bs_x_slot_offset.argtypes = [i64, ci, ci, ci, i64, ci, ci]
     L.bs_x_slot_offset.restype = i64
     L.bs_spmv_allgather.argtypes = [ctypes.POINTER(_Matrix), vp, vp, ci, ctypes.POINTER(_AllGather), ctypes.c_uint, vp]
@@ -568,17 +568,27 @@ def im2col(inp: torch.Tensor, kh: int, kw: int, pad: int = 0, stride: int = 1, o
 
 
 def conv2d(A: BSMatrix, inp: torch.Tensor, kh: int, kw: int, pad: int = 0, stride: int = 1,
-           workspace: torch.Tensor | None = None, implicit: bool | None = None) -> torch.Tensor:
+           workspace: torch.Tensor | None = None, implicit: bool | None = None,
+           bias: torch.Tensor | None = None, act: str | None = None) -> torch.Tensor:
     """A conv layer with the balanced-sparse Cout × (kh·kw·C) weight matrix A. NHWC in [Nimg, H, W, C], NHWC out
     [Nimg, OH, OW, Cout]. implicit=None: bs_conv2d (TMA im2col feeding the tensor cores, no intermediate) when
-    eligible (SPMM layout, 16-bit, C % 64 == 0, stride 1), else bs_im2col then bs_spmm; True/False forces one."""
+    eligible (SPMM layout, 16-bit, C % 64 == 0, stride 1), else bs_im2col then bs_spmm; True/False forces one.
+    bias ([Cout] of A.dtype) and act ("relu" | "sigmoid" | "tanh") fuse the layer epilogue into bs_conv2d
+    (they need the implicit path)."""
     _need_cuda(inp)
     Nimg, H, W, C = inp.shape
     if A.K != kh * kw * C:
         raise ValueError("A.K must equal kh·kw·C")
     if inp.dtype != A.dtype:
         raise ValueError("inp must have A.dtype")
-    _same_device(A, inp)
+    if act not in ACTS:
+        raise ValueError(f"act must be one of {sorted(k for k in ACTS if k)}")
+    if bias is not None and (bias.dtype != A.dtype or bias.numel() != A.M or not bias.is_contiguous()):
+        raise ValueError("bias must be a contiguous vector of A.M elements of A.dtype")
+    _same_device(A, inp, bias)
+    fused = bias is not None or ACTS[act] != 0
+    if fused and implicit is False:
+        raise ValueError("bias/act are fused into bs_conv2d only (implicit=True or None)")
     OH, OW = (H + 2 * pad - kh) // stride + 1, (W + 2 * pad - kw) // stride + 1
     if implicit is not False:
         ok = A.layout == "spmm" and A.dtype != torch.float32 and C % 64 == 0 and stride == 1 and A.k > 0
@@ -587,12 +597,15 @@ def conv2d(A: BSMatrix, inp: torch.Tensor, kh: int, kw: int, pad: int = 0, strid
             Y = torch.empty((Nimg, OH, OW, A.M), dtype=A.dtype, device=inp.device)
             m = A.cstruct()
             with torch.cuda.device(inp.device):
-                st = lib().bs_conv2d(ctypes.byref(m), x.data_ptr(), Nimg, H, W, C, kh, kw, pad, stride, Y.data_ptr(),
+                st = lib().bs_conv2d(ctypes.byref(m), x.data_ptr(), Nimg, H, W, C, kh, kw, pad, stride,
+                                     bias.data_ptr() if bias is not None else None, ACTS[act], Y.data_ptr(),
                                      _stream(inp.device))
             if st == 0:
                 return Y
-            if implicit or st != BS_ERR_UNSUPPORTED:
+            if implicit or fused or st != BS_ERR_UNSUPPORTED:
                 _check(st, "bs_conv2d")
+        elif fused:
+            raise BSError(BS_ERR_UNSUPPORTED, "bs_conv2d (bias/act need the implicit path)")
     X = im2col(inp, kh, kw, pad, stride, out=workspace)
     return spmm(A, X).view(Nimg, OH, OW, A.M)
 

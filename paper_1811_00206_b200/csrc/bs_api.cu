@@ -253,7 +253,7 @@ int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_
 }
 
 int bs_conv2d(const bs_matrix* A, const void* in, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw,
-              int pad, int stride, void* Y, void* stream) {
+              int pad, int stride, const void* bias, int act, void* Y, void* stream) {
   bsk::Geom g;
   int st = matrix_geom(A, &g);
   if (st) return st;
@@ -261,8 +261,9 @@ int bs_conv2d(const bs_matrix* A, const void* in, int64_t Nimg, int64_t H, int64
   if (g.K != (int64_t)kh * kw * C) return BS_ERR_SHAPE;
   if (H + 2 * pad < kh || W + 2 * pad < kw) return BS_ERR_SHAPE;
   if (!in || !Y) return BS_ERR_ARG;
+  if (act < BS_ACT_NONE || act > BS_ACT_TANH) return BS_ERR_ARG;
   if (stride != 1) return BS_ERR_UNSUPPORTED;
-  const cudaError_t e = bsk_launch_conv(g, A->packed, in, Nimg, H, W, C, kh, kw, pad, Y, (cudaStream_t)stream);
+  const cudaError_t e = bsk_launch_conv(g, A->packed, in, Nimg, H, W, C, kh, kw, pad, bias, act, Y, (cudaStream_t)stream);
   if (e == cudaErrorNotSupported) return BS_ERR_UNSUPPORTED;
   return from_cuda(e);
 }

@@ -94,7 +94,21 @@ struct TcArgs {
   int colfast;        // grid order (bsk::tc_cols_fast)
   // implicit im2col (bs_conv2d): X is the im2col of an NHWC input, loaded by TMA in im2col mode
   int conv, cC, cKW, cOW, cOHW, cPad;
+  const void* bias;   // bs_conv2d: optional per-row (output channel) bias of D, Eq. 1's +B
+  int act;            // bs_conv2d: bs_act after the bias, in fp32 before the one rounding (as bs_spmv_fused)
 };
+
+// Layer epilogue of bs_conv2d (the expressions of bs_spmv_fused's apply_act)
+template <int DT>
+__device__ __forceinline__ float tc_epilogue(float v, const TcArgs& a, int64_t row) {
+  if (a.bias) v += bsk::to_float<DT>(__ldg((const uint16_t*)a.bias + row));
+  switch (a.act) {
+    case BS_ACT_RELU: return fmaxf(v, 0.f);
+    case BS_ACT_SIGMOID: return 1.f / (1.f + expf(-v));
+    case BS_ACT_TANH: return tanhf(v);
+    default: return v;
+  }
+}
 
 template <int DT>
 __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_constant__ CUtensorMap tX, TcArgs a) {
@@ -340,7 +354,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int64_t ng = n0 + nb + e;
-            if (ng < a.N) ((raw_t*)a.Y)[ng * a.ldy + m0 + m] = (raw_t)bsk::from_float<DT>(__uint_as_float(rr[e]));
+            if (ng < a.N)
+              ((raw_t*)a.Y)[ng * a.ldy + m0 + m] = (raw_t)bsk::from_float<DT>(tc_epilogue<DT>(__uint_as_float(rr[e]), a, m0 + m));
           }
         }
       }
@@ -380,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc_kernel(const __grid_const
             const float f[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (row + e < mt) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
+              if (row + e < mt) yp[e] = (raw_t)bsk::from_float<DT>(tc_epilogue<DT>(f[e], a, m0 + row + e));
           }
         }
       }
@@ -440,9 +455,11 @@ int split_k(int64_t tiles, int64_t NC) {
   return S < 1 ? 1 : (int)S;
 }
 
-struct ConvGeom {  // implicit im2col input of bsk_launch_conv (NHWC, stride 1)
+struct ConvGeom {  // implicit im2col input of bsk_launch_conv (NHWC, stride 1) and its layer epilogue
   int64_t Nimg, H, W, C;
   int kh, kw, pad;
+  const void* bias;
+  int act;
 };
 
 template <int DT>
@@ -451,6 +468,8 @@ cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int
   if (!cv && (((uintptr_t)X & 15) != 0 || (ldx % 8) != 0)) return cudaErrorNotSupported;  // TMA: 16-byte rows
   TcArgs a;
   a.conv = cv != nullptr;
+  a.bias = cv ? cv->bias : nullptr;
+  a.act = cv ? cv->act : 0;
   if (cv) {
     a.cC = (int)cv->C;
     a.cKW = cv->kw;
@@ -544,7 +563,7 @@ cudaError_t launch_cc(const bsk::Geom& g, const void* packed, const void* X, int
 // Eligible: SPMM layout, 16-bit, B | 64, C % 64 == 0 (a 64-column chunk is one filter tap), stride 1,
 // symmetric padding, a 16-byte aligned input; cudaErrorNotSupported otherwise.
 cudaError_t bsk_launch_conv(const bsk::Geom& g, const void* packed, const void* in, int64_t Nimg, int64_t H, int64_t W,
-                            int64_t C, int kh, int kw, int pad, void* Y, cudaStream_t s) {
+                            int64_t C, int kh, int kw, int pad, const void* bias, int act, void* Y, cudaStream_t s) {
   if (g.layout != BS_LAYOUT_SPMM || g.es != 2 || (64 % g.B) != 0 || g.k == 0) return cudaErrorNotSupported;
   if (C % 64 != 0 || g.K != (int64_t)kh * kw * C || ((uintptr_t)in & 15) != 0) return cudaErrorNotSupported;
   if (pad > 127 || kh > 128 || kw > 128) return cudaErrorNotSupported;
@@ -552,7 +571,7 @@ cudaError_t bsk_launch_conv(const bsk::Geom& g, const void* packed, const void* 
   if (OH < 1 || OW < 1) return cudaErrorNotSupported;
   const int64_t N = Nimg * OH * OW;
   if (N >= (1LL << 31)) return cudaErrorNotSupported;
-  const ConvGeom cv{Nimg, H, W, C, kh, kw, pad};
+  const ConvGeom cv{Nimg, H, W, C, kh, kw, pad, bias, act};
   return g.dt == BS_BF16 ? launch_tc<BS_BF16>(g, packed, in, N, g.K, Y, g.M, s, &cv)
                          : launch_tc<BS_F16>(g, packed, in, N, g.K, Y, g.M, s, &cv);
 }

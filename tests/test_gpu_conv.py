@@ -129,3 +129,32 @@ def test_conv2d_implicit_errors(bs):
         bs.conv2d(bs.pack(v, i, 9 * 32, 32, layout="spmm"), inp, 3, 3, pad=1, implicit=True)
     Y = bs.conv2d(bs.pack(v, i, 9 * 32, 32, layout="spmm"), inp, 3, 3, pad=1)  # auto: falls back to im2col
     assert Y.shape == (1, 6, 6, 64)
+
+
+@pytest.mark.parametrize("act,dname", [("relu", "f16"), ("tanh", "bf16"), ("sigmoid", "f16")])
+def test_conv2d_fused_bias_act(bs, act, dname):
+    """bs_conv2d's layer epilogue: act(conv + bias) in fp32 before the one rounding (Eq. 1's +B, P:150),
+    against the oracle's direct convolution + bias + act in fp64: bit-exact for ReLU on integer-exact data,
+    within the conv bound (the activations are 1-Lipschitz) plus one rounding otherwise."""
+    Nimg, H, W, C, Cout, B = 1, 6, 7, 64, 96, 32
+    Kc = 9 * C
+    k = 3
+    fam = "intexact" if act == "relu" else "gaussian"
+    Wm = synth.matrix(Cout, Kc, dname, family=fam, seed=synth.seed_for(54, 1))
+    vals, idx, _ = bs.prune(Wm.cuda(), B, k=k)
+    A = bs.pack(vals, idx, Kc, B, layout="spmm")
+    xi = _img(Nimg, H, W, C, dname, synth.seed_for(54, 2), family=fam)
+    bias = synth.vector(Cout, dname, family=fam, seed=synth.seed_for(54, 3))
+    Y = bs.conv2d(A, xi.cuda(), 3, 3, pad=1, bias=bias.cuda(), act=act)
+    ov, oi = oracle.prune(synth.to_numpy(Wm), DT[dname], B, k)
+    ref, bound = oracle.conv2d(ov, oi, DT[dname], Cout, B, k, synth.to_numpy(xi), 3, 3, 1, 1)
+    b = oracle.to_double(synth.to_numpy(bias), DT[dname])
+    want = np.vectorize(lambda v: oracle.act(v, act))(ref + b[None, :])
+    got = oracle.to_double(synth.to_numpy(Y), DT[dname]).reshape(want.shape)
+    if act == "relu":
+        np.testing.assert_array_equal(got, want)
+    else:
+        ulp = 2.0 ** (-10 if dname == "f16" else -7)
+        assert np.all(np.abs(got - want) <= 1e-2 * (bound + np.abs(b)[None, :]) + ulp * np.abs(want) + 1e-6)
+    with pytest.raises(ValueError):
+        bs.conv2d(A, xi.cuda(), 3, 3, pad=1, bias=bias.cuda(), act=act, implicit=False)
