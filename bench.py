@@ -808,6 +808,30 @@ def f32_rows(a, bs, hbm_peak, l2):
     return {"f32": rows}
 
 
+def fc_batch_rows(a, bs, l2):
+    """BASELINE configs[2] at batch 32 as the VGG classifier runs it: Y = ReLU(W_bs·X + b) for fc6 / fc7 at 90 %,
+    fused into K6's epilogue (bs_spmm_fused, SPMM layout) against cuBLAS addmm + ReLU on the dense W_bs.
+    CUDA-graph timed with rotating copies."""
+    rows = []
+    dev = torch.device("cuda")
+    for name, M, K in (("fc6", 4096, 25088), ("fc7", 4096, 4096)):
+        W = synth.matrix(M, K, a.dtype, seed=synth.seed_for(12, K), device=dev)
+        ks = bs.k_from_sparsity(a.block, 0.9)
+        v, i, _ = bs.prune(W, a.block, k=ks)
+        mats = rotating(bs, bs.pack(v, i, K, a.block, layout="spmm"), l2)
+        C = len(mats)
+        Wd = dense_from_canonical(v, i, M, K, a.block)
+        b = synth.vector(M, a.dtype, seed=synth.seed_for(12, 1), device=dev)
+        X = synth.vector(K, a.dtype, seed=synth.seed_for(12, 2), n=32, device=dev)
+        Y = torch.empty((32, M), dtype=W.dtype, device=dev)
+        t = graph_time_us(lambda j: bs.spmm(mats[j % C], X, out=Y, bias=b, act="relu"), 20 * C if C < 10 else 2 * C)
+        td = graph_time_us(lambda j: torch.relu(torch.addmm(b, X, Wd.t())), 20)
+        rows.append({"layer": f"{name} {M}x{K} s=0.9 N=32 +bias+ReLU", "ours_us": round(t, 2),
+                     "cublas_addmm_relu_us": round(td, 2), "speedup": round(td / t, 2)})
+        del W, v, i, mats, Wd
+    return {"fc_batch": rows}
+
+
 def vgg_head_rows(a, bs, l2):
     """NEXT-2 (o_time): VGG-16's classifier head fc6 -> fc7 -> fc8 with bias + ReLU at Table
     cnn-perf's balanced sparsities (93 %, 93 %, 75 % -> k = 2, 2, 8 of 32), batch 1: eager launches vs one
@@ -950,7 +974,7 @@ def extras(a, bs, W, A, vals, idx, x, k, es, hbm_peak, stream):
         res.update(f32_rows(a, bs, hbm_peak, l2))
     except Exception as e:
         res["f32_rows_error"] = f"{type(e).__name__}: {str(e)[:200]}"
-    for fn in (conv_rows, lstm_rows, vgg_head_rows):
+    for fn in (conv_rows, lstm_rows, vgg_head_rows, fc_batch_rows):
         try:
             res.update(fn(a, bs, l2))
         except Exception as e:  # a failing extra is reported, never hidden

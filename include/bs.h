@@ -188,6 +188,15 @@ int bs_block_mask(const void* W, int dt, int64_t M, int64_t K, int64_t ldw, int6
 int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw, int pad,
               int stride, void* X, int64_t ldx, void* stream);
 
+/* bs_spmm_fused: a fully connected layer at batch N, Y = act(W_bs·X + bias) (Eq. 1 with its +B; the VGG
+ * classifier layers at batch), on the tensor cores: layout SPMM, f16/bf16, block | 64, X rows
+ * 16-byte aligned with ldx % 8 == 0. bias: M elements of A's dtype or NULL; act: bs_act, applied in fp32
+ * before the one rounding (bs_spmv_fused's expressions). With bias = NULL and act = BS_ACT_NONE the result
+ * is bit-identical to bs_spmm on the same operands. X, Y as bs_spmm.
+ * Errors: as bs_spmm; BS_ERR_ARG for an unknown act; BS_ERR_UNSUPPORTED when the operands are not eligible. */
+int bs_spmm_fused(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, const void* bias, int act, void* Y,
+                  int64_t ldy, void* stream);
+
 /* bs_conv2d: a convolution layer as one balanced-sparse product with implicit im2col ("im2col that
  * converts convolution operation to matrix-matrix multiplication"; all kernels of a layer form one
  * weight matrix): Y [Nimg·OH·OW][M] = W_bs · im2col(in)ᵀ, i.e. the NHWC output [Nimg][OH][OW][Cout = M],

@@ -31,7 +31,7 @@ EXPORTS = ("bs_k_from_sparsity", "bs_packed_bytes", "bs_status_str", "bs_version
            "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm", "bs_choose_layout", "bs_block_rank",
            "bs_schedule_sparsity", "bs_keep_count", "bs_decode", "bs_pattern_workspace_bytes", "bs_random_mask",
            "bs_block_mask", "bs_lstm_step", "bs_im2col", "bs_spmv_allgather", "bs_allgather_wait", "bs_peer_export",
-           "bs_peer_import", "bs_peer_close", "bs_x_slot_offset", "bs_conv2d")
+           "bs_peer_import", "bs_peer_close", "bs_x_slot_offset", "bs_conv2d", "bs_spmm_fused")
 ACTS = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}  # bs_act (include/bs.h)
 SPMV_PDL, SPMV_W_STATIC, SPMV_RING = 1, 2, 4  # bs_spmv_ex flags (include/bs.h)
 
@@ -93,6 +93,7 @@ def _load() -> ctypes.CDLL:
     L.bs_lstm_step.argtypes = [ctypes.POINTER(_Matrix), vp, vp, vp, vp, vp, vp, ctypes.c_uint, vp]
     L.bs_im2col.argtypes = [vp, ci, i64, i64, i64, i64, ci, ci, ci, ci, vp, i64, vp]
     L.bs_conv2d.argtypes = [ctypes.POINTER(_Matrix), vp, i64, i64, i64, i64, ci, ci, ci, ci, vp, ci, vp, vp]
+    L.bs_spmm_fused.argtypes = [ctypes.POINTER(_Matrix), vp, i64, i64, vp, ci, vp, i64, vp]
     L.bs_x_slot_offset.argtypes = [i64, ci, ci, ci, i64, ci, ci]
     L.bs_x_slot_offset.restype = i64
     L.bs_spmv_allgather.argtypes = [ctypes.POINTER(_Matrix), vp, vp, ci, ctypes.POINTER(_AllGather), ctypes.c_uint, vp]
@@ -100,7 +101,7 @@ def _load() -> ctypes.CDLL:
     L.bs_peer_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_int64)]
     L.bs_peer_import.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]
     L.bs_peer_close.argtypes = [vp, ctypes.c_int64]
-    for f in ("bs_decode", "bs_random_mask", "bs_block_mask", "bs_lstm_step", "bs_im2col", "bs_conv2d", "bs_spmv_allgather",
+    for f in ("bs_decode", "bs_random_mask", "bs_block_mask", "bs_lstm_step", "bs_im2col", "bs_conv2d", "bs_spmm_fused", "bs_spmv_allgather",
               "bs_allgather_wait", "bs_peer_export", "bs_peer_import", "bs_peer_close"):
         getattr(L, f).restype = ci
     for f in ("bs_prune", "bs_prune_k", "bs_pack", "bs_unpack", "bs_spmv", "bs_spmv_ex", "bs_spmv_fused", "bs_spmv_host", "bs_spmm"):
@@ -352,12 +353,31 @@ def spmv_host(A: BSMatrix, x_host: torch.Tensor, y_host: torch.Tensor, x_dev: to
     _check(st, "bs_spmv_host")
 
 
-def spmm(A: BSMatrix, X: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """Y = W_bs·X for a batch. X: [N, K] (row n = column n of the K×N operand); returns Y: [N, M]."""
+def spmm(A: BSMatrix, X: torch.Tensor, out: torch.Tensor | None = None, bias: torch.Tensor | None = None,
+         act: str | None = None) -> torch.Tensor:
+    """Y = W_bs·X for a batch. X: [N, K] (row n = column n of the K×N operand); returns Y: [N, M].
+    bias ([M] of A.dtype) / act ("relu" | "sigmoid" | "tanh"): the fused layer epilogue Y = act(W_bs·X + bias)
+    (bs_spmm_fused; SPMM layout on the tensor cores)."""
     _need_cuda(X)
     if X.dim() != 2 or X.shape[1] != A.K or X.dtype != A.dtype or X.stride(1) != 1:
         raise ValueError("X must be [N, K] of A.dtype with unit column stride")
-    _same_device(A, X)
+    if act not in ACTS:
+        raise ValueError(f"act must be one of {sorted(k for k in ACTS if k)}")
+    if bias is not None and (bias.dtype != A.dtype or bias.numel() != A.M or not bias.is_contiguous()):
+        raise ValueError("bias must be a contiguous vector of A.M elements of A.dtype")
+    _same_device(A, X, bias)
+    if bias is not None or ACTS[act] != 0:
+        N = X.shape[0]
+        if out is not None:
+            _check_out(out, A, (N, A.M))
+        Y = out if out is not None else torch.empty((N, A.M), dtype=A.dtype, device=X.device)
+        m = A.cstruct()
+        with torch.cuda.device(X.device):
+            st = lib().bs_spmm_fused(ctypes.byref(m), X.data_ptr(), N, X.stride(0),
+                                     bias.data_ptr() if bias is not None else None, ACTS[act], Y.data_ptr(),
+                                     Y.stride(0), _stream(X.device))
+        _check(st, "bs_spmm_fused")
+        return Y
     N = X.shape[0]
     if out is not None:
         _check_out(out, A, (N, A.M))

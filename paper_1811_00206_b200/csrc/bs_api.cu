@@ -252,6 +252,18 @@ int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_
   return from_cuda(bsk_launch_im2col(in, dt, Nimg, H, W, C, kh, kw, pad, stride, X, ldx, (cudaStream_t)stream));
 }
 
+int bs_spmm_fused(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, const void* bias, int act, void* Y,
+                  int64_t ldy, void* stream) {
+  bsk::Geom g;
+  int st = matrix_geom(A, &g);
+  if (st) return st;
+  if (!X || !Y || N < 1 || ldx < g.K || ldy < g.M) return BS_ERR_ARG;
+  if (act < BS_ACT_NONE || act > BS_ACT_TANH) return BS_ERR_ARG;
+  const cudaError_t e = bsk_launch_spmm_fused(g, A->packed, X, N, ldx, Y, ldy, bias, act, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported) return BS_ERR_UNSUPPORTED;
+  return from_cuda(e);
+}
+
 int bs_conv2d(const bs_matrix* A, const void* in, int64_t Nimg, int64_t H, int64_t W, int64_t C, int kh, int kw,
               int pad, int stride, const void* bias, int act, void* Y, void* stream) {
   bsk::Geom g;

@@ -455,21 +455,20 @@ int split_k(int64_t tiles, int64_t NC) {
   return S < 1 ? 1 : (int)S;
 }
 
-struct ConvGeom {  // implicit im2col input of bsk_launch_conv (NHWC, stride 1) and its layer epilogue
+struct ConvGeom {  // implicit im2col input of bsk_launch_conv (NHWC, stride 1)
   int64_t Nimg, H, W, C;
   int kh, kw, pad;
-  const void* bias;
-  int act;
 };
 
 template <int DT>
 cudaError_t launch_tc(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
-                      int64_t ldy, cudaStream_t s, const ConvGeom* cv = nullptr) {
+                      int64_t ldy, cudaStream_t s, const ConvGeom* cv = nullptr, const void* bias = nullptr,
+                      int act = 0) {
   if (!cv && (((uintptr_t)X & 15) != 0 || (ldx % 8) != 0)) return cudaErrorNotSupported;  // TMA: 16-byte rows
   TcArgs a;
   a.conv = cv != nullptr;
-  a.bias = cv ? cv->bias : nullptr;
-  a.act = cv ? cv->act : 0;
+  a.bias = bias;
+  a.act = act;
   if (cv) {
     a.cC = (int)cv->C;
     a.cKW = cv->kw;
@@ -571,9 +570,18 @@ cudaError_t bsk_launch_conv(const bsk::Geom& g, const void* packed, const void* 
   if (OH < 1 || OW < 1) return cudaErrorNotSupported;
   const int64_t N = Nimg * OH * OW;
   if (N >= (1LL << 31)) return cudaErrorNotSupported;
-  const ConvGeom cv{Nimg, H, W, C, kh, kw, pad, bias, act};
-  return g.dt == BS_BF16 ? launch_tc<BS_BF16>(g, packed, in, N, g.K, Y, g.M, s, &cv)
-                         : launch_tc<BS_F16>(g, packed, in, N, g.K, Y, g.M, s, &cv);
+  const ConvGeom cv{Nimg, H, W, C, kh, kw, pad};
+  return g.dt == BS_BF16 ? launch_tc<BS_BF16>(g, packed, in, N, g.K, Y, g.M, s, &cv, bias, act)
+                         : launch_tc<BS_F16>(g, packed, in, N, g.K, Y, g.M, s, &cv, bias, act);
+}
+
+// Y = act(W_bs·X + bias) on the tensor cores (SPMM layout, 16-bit, B | 64, aligned X): K6 with the layer
+// epilogue of bs_conv2d. cudaErrorNotSupported otherwise.
+cudaError_t bsk_launch_spmm_fused(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,
+                                  void* Y, int64_t ldy, const void* bias, int act, cudaStream_t s) {
+  if (g.layout != BS_LAYOUT_SPMM || g.es != 2 || (64 % g.B) != 0 || g.k == 0) return cudaErrorNotSupported;
+  return g.dt == BS_BF16 ? launch_tc<BS_BF16>(g, packed, X, N, ldx, Y, ldy, s, nullptr, bias, act)
+                         : launch_tc<BS_F16>(g, packed, X, N, ldx, Y, ldy, s, nullptr, bias, act);
 }
 
 // Returns cudaErrorNotSupported when the caller should fall back to column-at-a-time SpMV

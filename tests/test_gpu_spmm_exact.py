@@ -361,3 +361,31 @@ def test_direct_kernel_integer_exact(bs):
     y = bs.spmv(A, x.cuda())
     yr, _ = oracle.spmv(ov, oi, oracle.BF16, M, K, B, k, synth.to_numpy(x))
     np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(y), oracle.BF16), yr)
+
+
+# ---------------------------------------------------------------- bs_spmm_fused: the FC layer epilogue at batch
+
+@pytest.mark.parametrize("act,dname", [("relu", "f16"), ("none", "bf16"), ("tanh", "f16")])
+def test_spmm_fused_bias_act(bs, act, dname):
+    """Y = act(W_bs·X + bias) on K6 (SPMM layout): with act = none and no bias it is bs_spmm bit for bit; with
+    bias + ReLU on integer-exact data it equals the oracle exactly; tanh within the product's bound plus one
+    rounding."""
+    M, K, B, k, N = 300, 4096 + 64, 32, 3, 40
+    fam = "gaussian" if act == "tanh" else "intexact"
+    A, ov, oi = _setup(bs, M, K, B, k, dname, synth.seed_for(60, 0), "spmm", family=fam)
+    X = synth.vector(K, dname, family=fam, seed=synth.seed_for(60, 1), n=N).cuda()
+    if act == "none":
+        assert torch.equal(bs.spmm(A, X, act="none"), bs.spmm(A, X))
+        return
+    bias = synth.vector(M, dname, family=fam, seed=synth.seed_for(60, 2))
+    Y = bs.spmm(A, X, bias=bias.cuda(), act=act)
+    Yr, bound = oracle.spmm(ov, oi, DT[dname], M, K, B, k, synth.to_numpy(X.cpu()))
+    b = oracle.to_double(synth.to_numpy(bias), DT[dname])
+    want = np.vectorize(lambda v: oracle.act(v, act))(Yr + b[None, :])
+    got = oracle.to_double(synth.to_numpy(Y), DT[dname])
+    if act == "relu":
+        np.testing.assert_array_equal(got, want)
+    else:
+        assert np.all(np.abs(got - want) <= 1e-2 * (bound + np.abs(b)[None, :]) + 2.0 ** -10 * np.abs(want) + 1e-6)
+    with pytest.raises(bs.BSError):  # the SPMV layout has no batched epilogue
+        bs.spmm(bs.pack(*bs.unpack(A), K, B, layout="spmv"), X, bias=bias.cuda(), act=act)
