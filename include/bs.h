@@ -189,8 +189,8 @@ int bs_im2col(const void* in, int dt, int64_t Nimg, int64_t H, int64_t W, int64_
               int stride, void* X, int64_t ldx, void* stream);
 
 /* bs_spmm_fused: a fully connected layer at batch N, Y = act(W_bs·X + bias) (Eq. 1 with its +B; the VGG
- * classifier layers at batch), on the tensor cores: layout SPMM, f16/bf16, block | 64, X rows
- * 16-byte aligned with ldx % 8 == 0. bias: M elements of A's dtype or NULL; act: bs_act, applied in fp32
+ * classifier layers at batch), on the tensor cores: layout SPMM (block | 64) or SP24 (K % 128 ==
+ * 0), f16/bf16, X rows 16-byte aligned with ldx % 8 == 0. bias: M elements of A's dtype or NULL; act: bs_act, applied in fp32
  * before the one rounding (bs_spmv_fused's expressions). With bias = NULL and act = BS_ACT_NONE the result
  * is bit-identical to bs_spmm on the same operands. X, Y as bs_spmm.
  * Errors: as bs_spmm; BS_ERR_ARG for an unknown act; BS_ERR_UNSUPPORTED when the operands are not eligible. */

@@ -259,7 +259,9 @@ int bs_spmm_fused(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, con
   if (st) return st;
   if (!X || !Y || N < 1 || ldx < g.K || ldy < g.M) return BS_ERR_ARG;
   if (act < BS_ACT_NONE || act > BS_ACT_TANH) return BS_ERR_ARG;
-  const cudaError_t e = bsk_launch_spmm_fused(g, A->packed, X, N, ldx, Y, ldy, bias, act, (cudaStream_t)stream);
+  const cudaError_t e = g.layout == BS_LAYOUT_SP24
+                            ? bsk_launch_sp24_fused(g, A->packed, X, N, ldx, Y, ldy, bias, act, (cudaStream_t)stream)
+                            : bsk_launch_spmm_fused(g, A->packed, X, N, ldx, Y, ldy, bias, act, (cudaStream_t)stream);
   if (e == cudaErrorNotSupported) return BS_ERR_UNSUPPORTED;
   return from_cuda(e);
 }

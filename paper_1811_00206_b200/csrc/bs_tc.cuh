@@ -114,6 +114,19 @@ __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const CUtensorMap* m
       : "memory");
 }
 
+// Layer epilogue of the tensor-core products (bs_conv2d, bs_spmm_fused): v + bias[row] (16-bit D), then
+// ReLU / sigmoid / tanh (bs_act), in fp32 before the one rounding; the expressions of bs_spmv_fused.
+template <int DT>
+__device__ __forceinline__ float act_epilogue(float v, const void* bias, int act, int64_t row) {
+  if (bias) v += bsk::to_float<DT>(__ldg((const uint16_t*)bias + row));
+  switch (act) {
+    case BS_ACT_RELU: return fmaxf(v, 0.f);
+    case BS_ACT_SIGMOID: return 1.f / (1.f + expf(-v));
+    case BS_ACT_TANH: return tanhf(v);
+    default: return v;
+  }
+}
+
 }  // namespace bsk_tc
 
 // Im2col tensor map of an NHWC 16-bit tensor [Nimg][H][W][C] for a kh × kw, stride-1 convolution with

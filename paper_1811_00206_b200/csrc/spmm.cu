@@ -98,16 +98,10 @@ struct TcArgs {
   int act;            // bs_conv2d: bs_act after the bias, in fp32 before the one rounding (as bs_spmv_fused)
 };
 
-// Layer epilogue of bs_conv2d (the expressions of bs_spmv_fused's apply_act)
+// Layer epilogue of bs_conv2d / bs_spmm_fused (bsk_tc::act_epilogue)
 template <int DT>
 __device__ __forceinline__ float tc_epilogue(float v, const TcArgs& a, int64_t row) {
-  if (a.bias) v += bsk::to_float<DT>(__ldg((const uint16_t*)a.bias + row));
-  switch (a.act) {
-    case BS_ACT_RELU: return fmaxf(v, 0.f);
-    case BS_ACT_SIGMOID: return 1.f / (1.f + expf(-v));
-    case BS_ACT_TANH: return tanhf(v);
-    default: return v;
-  }
+  return act_epilogue<DT>(v, a.bias, a.act, row);
 }
 
 template <int DT>

@@ -55,6 +55,8 @@ struct Sp24Args {
   int meta_cols;        // TMEM metadata columns per row tile: NST stages × 4 K-steps × mstride
   int mstride;          // TMEM columns between the metadata of consecutive K = 32 steps
   int colfast;          // grid order (bsk::tc_cols_fast)
+  const void* bias;     // bs_spmm_fused: per-row bias of D or NULL
+  int act;              // bs_spmm_fused: bs_act
 };
 
 using namespace bsk_tc;
@@ -218,7 +220,9 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int64_t ng = n0 + nb + e;
-          if (ng < a.N) ((raw_t*)a.Y)[ng * a.ldy + m0 + trow] = (raw_t)bsk::from_float<DT>(__uint_as_float(r[e]));
+          if (ng < a.N)
+            ((raw_t*)a.Y)[ng * a.ldy + m0 + trow] =
+                (raw_t)bsk::from_float<DT>(act_epilogue<DT>(__uint_as_float(r[e]), a.bias, a.act, m0 + trow));
         }
       }
     }
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
             const float f[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (r4 + e < mrows) yp[e] = (raw_t)bsk::from_float<DT>(f[e]);
+              if (r4 + e < mrows) yp[e] = (raw_t)bsk::from_float<DT>(act_epilogue<DT>(f[e], a.bias, a.act, m0 + r4 + e));
           }
         }
       }
@@ -416,7 +420,9 @@ __global__ void __launch_bounds__(192, 1) spmm24_pair_kernel(const __grid_consta
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int64_t ng = n0 + nb + e;
-          if (ng < a.N) ((raw_t*)a.Y)[ng * a.ldy + m0 + row] = (raw_t)bsk::from_float<DT>(__uint_as_float(r[e]));
+          if (ng < a.N)
+            ((raw_t*)a.Y)[ng * a.ldy + m0 + row] =
+                (raw_t)bsk::from_float<DT>(act_epilogue<DT>(__uint_as_float(r[e]), a.bias, a.act, m0 + row));
         }
       }
     }
@@ -502,7 +508,7 @@ __global__ void __launch_bounds__(256) sp24_spmv16_kernel(const uint16_t* __rest
 
 template <int DT>
 cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
-                        int64_t ldy, cudaStream_t s) {
+                        int64_t ldy, cudaStream_t s, const void* bias = nullptr, int act = 0) {
   int BN = (int)((N + 15) / 16 * 16);
   static const int bn_max = [] {  // BS_K5_BN_MAX: tuning knob (128 or 256); BN only partitions columns
     const char* e = getenv("BS_K5_BN_MAX");
@@ -545,6 +551,8 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   if (!bsk_make_map_2d(&tA, DT, base + g.offA, g.K / 2, g.M, g.K / 2, 64, BM)) return cudaErrorNotSupported;
   if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, 64, pair ? BN / 2 : BN)) return cudaErrorNotSupported;
   Sp24Args a;
+  a.bias = bias;
+  a.act = act;
   a.meta = base + g.offB;
   a.Y = Y;
   a.M = g.M; a.K = g.K; a.N = N; a.ldy = ldy;
@@ -678,6 +686,16 @@ bool bsk_make_map_im2col(CUtensorMap* m, int dt, const void* in, int64_t Nimg, i
   return fn(m, t, 4, const_cast<void*>(in), dims, strides, lower, upper, 64, (cuuint32_t)pixels, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Y = act(W·X + bias) on the sparse tensor cores (bs_spmm_fused, SP24 layout); NotSupported when the operands
+// do not allow the tensor-core path.
+cudaError_t bsk_launch_sp24_fused(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
+                                  int64_t ldy, const void* bias, int act, cudaStream_t s) {
+  const bool tc = g.es == 2 && g.K % KCH == 0 && ((uintptr_t)X & 15) == 0 && (ldx % 8) == 0;
+  if (!tc) return cudaErrorNotSupported;
+  return g.dt == BS_BF16 ? launch_tc24<BS_BF16>(g, packed, X, N, ldx, Y, ldy, s, bias, act)
+                         : launch_tc24<BS_F16>(g, packed, X, N, ldx, Y, ldy, s, bias, act);
 }
 
 // Y = W·X for W in SP24 layout.

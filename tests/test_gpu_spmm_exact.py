@@ -389,3 +389,18 @@ def test_spmm_fused_bias_act(bs, act, dname):
         assert np.all(np.abs(got - want) <= 1e-2 * (bound + np.abs(b)[None, :]) + 2.0 ** -10 * np.abs(want) + 1e-6)
     with pytest.raises(bs.BSError):  # the SPMV layout has no batched epilogue
         bs.spmm(bs.pack(*bs.unpack(A), K, B, layout="spmv"), X, bias=bias.cuda(), act=act)
+
+
+def test_spmm_fused_sp24(bs):
+    """bs_spmm_fused on the 2:4 layout (K5: single CTA with split-K, and CTA pairs): bias + ReLU exact on integer
+    data, and the plain product bit-identical to bs_spmm."""
+    for M in (1000, 9728):  # split-K single-CTA kernel; CTA pairs (>= 75 row tiles)
+        K, N = 1024, 48
+        A, ov, oi = _setup(bs, M, K, 4, 2, "f16", synth.seed_for(61, M), "sp24")
+        X = synth.vector(K, "f16", family="intexact", seed=synth.seed_for(61, 1), n=N).cuda()
+        bias = synth.vector(M, "f16", family="intexact", seed=synth.seed_for(61, 2))
+        Y = bs.spmm(A, X, bias=bias.cuda(), act="relu")
+        Yr, _ = oracle.spmm(ov, oi, oracle.F16, M, K, 4, 2, synth.to_numpy(X.cpu()))
+        b = oracle.to_double(synth.to_numpy(bias), oracle.F16)
+        np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(Y), oracle.F16), np.maximum(Yr + b[None, :], 0.0))
+        assert torch.equal(bs.spmm(A, X, act="none"), bs.spmm(A, X))
