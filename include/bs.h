@@ -203,7 +203,8 @@ int bs_spmm_fused(const bs_matrix* A, const void* X, int64_t N, int64_t ldx, con
  * with in NHWC [Nimg][H][W][C] (16-bit, 16-byte aligned) and W_bs's columns in (dy, dx, c) order (reading
  * A23; A->K = kh·kw·C). The tensor cores' X tiles are loaded straight from `in` by TMA in im2col mode, so
  * no [pixels][kh·kw·C] intermediate exists; the result is bit-identical to bs_im2col + bs_spmm.
- * Requirements: layout SPMM, f16/bf16, block | 64, C % 64 == 0, stride 1. Y has room for
+ * Requirements: layout SPMM (block | 64; K6) or SP24 (kh·kw·C % 128 == 0; K5, the 2:4 sparse tensor cores),
+ * f16/bf16, C % 64 == 0, stride 1. Y has room for
  * Nimg·OH·OW·M elements of A's dtype (caller-owned).
  * Layer epilogue (Eq. 1's +B, and the activation that follows a VGG conv layer): `bias` (M elements
  * of A's dtype, one per output channel, or NULL) is added and `act` (bs_act) applied in fp32 before the

@@ -611,7 +611,8 @@ def conv2d(A: BSMatrix, inp: torch.Tensor, kh: int, kw: int, pad: int = 0, strid
         raise ValueError("bias/act are fused into bs_conv2d only (implicit=True or None)")
     OH, OW = (H + 2 * pad - kh) // stride + 1, (W + 2 * pad - kw) // stride + 1
     if implicit is not False:
-        ok = A.layout == "spmm" and A.dtype != torch.float32 and C % 64 == 0 and stride == 1 and A.k > 0
+        ok = (A.layout == "spmm" or (A.layout == "sp24" and A.K % 128 == 0)) and A.dtype != torch.float32 and \
+            C % 64 == 0 and stride == 1 and A.k > 0
         if ok or implicit:
             x = inp.contiguous()
             Y = torch.empty((Nimg, OH, OW, A.M), dtype=A.dtype, device=inp.device)

@@ -277,7 +277,10 @@ int bs_conv2d(const bs_matrix* A, const void* in, int64_t Nimg, int64_t H, int64
   if (!in || !Y) return BS_ERR_ARG;
   if (act < BS_ACT_NONE || act > BS_ACT_TANH) return BS_ERR_ARG;
   if (stride != 1) return BS_ERR_UNSUPPORTED;
-  const cudaError_t e = bsk_launch_conv(g, A->packed, in, Nimg, H, W, C, kh, kw, pad, bias, act, Y, (cudaStream_t)stream);
+  const cudaError_t e =
+      g.layout == BS_LAYOUT_SP24
+          ? bsk_launch_conv24(g, A->packed, in, Nimg, H, W, C, kh, kw, pad, bias, act, Y, (cudaStream_t)stream)
+          : bsk_launch_conv(g, A->packed, in, Nimg, H, W, C, kh, kw, pad, bias, act, Y, (cudaStream_t)stream);
   if (e == cudaErrorNotSupported) return BS_ERR_UNSUPPORTED;
   return from_cuda(e);
 }

@@ -193,6 +193,8 @@ cudaError_t bsk_launch_sp24(const bsk::Geom& g, const void* packed, const void* 
                             int64_t ldy, cudaStream_t s, bool spmv);
 cudaError_t bsk_launch_spmm(const bsk::Geom& g, const void* packed, const void* X, int64_t N,
                             int64_t ldx, void* Y, int64_t ldy, cudaStream_t s);
+cudaError_t bsk_launch_conv24(const bsk::Geom& g, const void* packed, const void* in, int64_t Nimg, int64_t H, int64_t W,
+                              int64_t C, int kh, int kw, int pad, const void* bias, int act, void* Y, cudaStream_t s);
 cudaError_t bsk_launch_sp24_fused(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
                                   int64_t ldy, const void* bias, int act, cudaStream_t s);
 cudaError_t bsk_launch_spmm_fused(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx,

@@ -127,6 +127,34 @@ __device__ __forceinline__ float act_epilogue(float v, const void* bias, int act
   }
 }
 
+// im2col copy completing on an mbarrier of either CTA of a pair (the K5 CTA-pair kernel)
+__device__ __forceinline__ void tma_im2col_4d_pair(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
+                                                   uint16_t dw, uint16_t dh, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar_cluster), "h"(dw), "h"(dh)
+      : "memory");
+}
+
+// Implicit im2col geometry of a tensor-core SpMM over a convolution (bs_conv2d): the X column starting at
+// pixel p of K-columns [col0, col0 + 64) is 64 channels of one filter tap
+struct ConvX {
+  int conv, C, KW, OW, OHW, pad;
+  __device__ __forceinline__ void coords(int64_t p, int col0, int& c, int& w, int& h, int& n, uint16_t& dw,
+                                         uint16_t& dh) const {
+    const int tap = col0 / C;
+    c = col0 - tap * C;
+    const int dy = tap / KW, dx = tap - dy * KW;
+    n = (int)(p / OHW);
+    const int pix = (int)(p - (int64_t)n * OHW);
+    const int oy = pix / OW, ox = pix - oy * OW;
+    w = ox - pad;
+    h = oy - pad;
+    dw = (uint16_t)dx;
+    dh = (uint16_t)dy;
+  }
+};
+
 }  // namespace bsk_tc
 
 // Im2col tensor map of an NHWC 16-bit tensor [Nimg][H][W][C] for a kh × kw, stride-1 convolution with

@@ -57,6 +57,7 @@ struct Sp24Args {
   int colfast;          // grid order (bsk::tc_cols_fast)
   const void* bias;     // bs_spmm_fused: per-row bias of D or NULL
   int act;              // bs_spmm_fused: bs_act
+  bsk_tc::ConvX cx;     // bs_conv2d: implicit im2col (cx.conv != 0; C % 64 == 0)
 };
 
 using namespace bsk_tc;
@@ -123,8 +124,18 @@ __global__ void __launch_bounds__(64 + 128 * RT, 1) spmm24_kernel(const __grid_c
         if (i >= NST) mbar_wait(empty + 8 * s, ph ^ 1u);
         mbar_expect_tx(full + 8 * s, (uint32_t)rtl * ASZ + BSZ);
         for (int t = 0; t < rtl; ++t) tma_2d(sA + (s * RT + t) * ASZ, &tA, c * (KCH / 2), (int)(m0 + t * BM), full + 8 * s);
-        tma_2d(sB + s * BSZ, &tX, c * KCH, (int)n0, full + 8 * s);
-        tma_2d(sB + s * BSZ + (uint32_t)a.BN * 128, &tX, c * KCH + 64, (int)n0, full + 8 * s);
+        if (a.cx.conv) {  // implicit im2col: each 64-column atom is 64 channels of one filter tap
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            int cc, w, hh, nn;
+            uint16_t dw, dh;
+            a.cx.coords(n0, c * KCH + 64 * h2, cc, w, hh, nn, dw, dh);
+            tma_im2col_4d(sB + s * BSZ + (uint32_t)h2 * (uint32_t)a.BN * 128, &tX, cc, w, hh, nn, dw, dh, full + 8 * s);
+          }
+        } else {
+          tma_2d(sB + s * BSZ, &tX, c * KCH, (int)n0, full + 8 * s);
+          tma_2d(sB + s * BSZ + (uint32_t)a.BN * 128, &tX, c * KCH + 64, (int)n0, full + 8 * s);
+        }
         if (++s == NST) { s = 0; ph ^= 1u; }
       }
     }
@@ -342,8 +353,18 @@ __global__ void __launch_bounds__(192, 1) spmm24_pair_kernel(const __grid_consta
         if (rank == 0) mbar_expect_tx(full + 8 * s, 2u * (ASZ + BSZ));
         else mbar_arrive_cluster(lf);
         tma_2d_pair(sA + s * ASZ, &tA, i * (KCH / 2), (int)m0, lf);
-        tma_2d_pair(sB + s * BSZ, &tX, i * KCH, (int)(n0 + rank * BNh), lf);
-        tma_2d_pair(sB + s * BSZ + (uint32_t)BNh * 128, &tX, i * KCH + 64, (int)(n0 + rank * BNh), lf);
+        if (a.cx.conv) {
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            int cc, w, hh, nn;
+            uint16_t dw, dh;
+            a.cx.coords(n0 + rank * BNh, i * KCH + 64 * h2, cc, w, hh, nn, dw, dh);
+            tma_im2col_4d_pair(sB + s * BSZ + (uint32_t)h2 * (uint32_t)BNh * 128, &tX, cc, w, hh, nn, dw, dh, lf);
+          }
+        } else {
+          tma_2d_pair(sB + s * BSZ, &tX, i * KCH, (int)(n0 + rank * BNh), lf);
+          tma_2d_pair(sB + s * BSZ + (uint32_t)BNh * 128, &tX, i * KCH + 64, (int)(n0 + rank * BNh), lf);
+        }
         if (++s == NST) { s = 0; ph ^= 1u; }
       }
     }
@@ -506,9 +527,15 @@ __global__ void __launch_bounds__(256) sp24_spmv16_kernel(const uint16_t* __rest
   }
 }
 
+struct Conv24 {  // implicit im2col input (bs_conv2d on SP24)
+  int64_t Nimg, H, W, C;
+  int kh, kw, pad;
+};
+
 template <int DT>
 cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, int64_t N, int64_t ldx, void* Y,
-                        int64_t ldy, cudaStream_t s, const void* bias = nullptr, int act = 0) {
+                        int64_t ldy, cudaStream_t s, const void* bias = nullptr, int act = 0,
+                        const Conv24* cv = nullptr) {
   int BN = (int)((N + 15) / 16 * 16);
   static const int bn_max = [] {  // BS_K5_BN_MAX: tuning knob (128 or 256); BN only partitions columns
     const char* e = getenv("BS_K5_BN_MAX");
@@ -549,10 +576,23 @@ cudaError_t launch_tc24(const bsk::Geom& g, const void* packed, const void* X, i
   CUtensorMap tA, tX;
   const uint8_t* base = (const uint8_t*)packed;
   if (!bsk_make_map_2d(&tA, DT, base + g.offA, g.K / 2, g.M, g.K / 2, 64, BM)) return cudaErrorNotSupported;
-  if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, 64, pair ? BN / 2 : BN)) return cudaErrorNotSupported;
+  if (cv) {
+    if (!bsk_make_map_im2col(&tX, DT, X, cv->Nimg, cv->H, cv->W, cv->C, cv->kh, cv->kw, cv->pad, pair ? BN / 2 : BN))
+      return cudaErrorNotSupported;
+  } else if (!bsk_make_map_2d(&tX, DT, X, g.K, N, ldx, 64, pair ? BN / 2 : BN)) {
+    return cudaErrorNotSupported;
+  }
   Sp24Args a;
   a.bias = bias;
   a.act = act;
+  a.cx.conv = cv != nullptr;
+  if (cv) {
+    a.cx.C = (int)cv->C;
+    a.cx.KW = cv->kw;
+    a.cx.OW = (int)(cv->W + 2 * cv->pad - cv->kw + 1);
+    a.cx.OHW = (int)((cv->H + 2 * cv->pad - cv->kh + 1) * a.cx.OW);
+    a.cx.pad = cv->pad;
+  }
   a.meta = base + g.offB;
   a.Y = Y;
   a.M = g.M; a.K = g.K; a.N = N; a.ldy = ldy;
@@ -686,6 +726,21 @@ bool bsk_make_map_im2col(CUtensorMap* m, int dt, const void* in, int64_t Nimg, i
   return fn(m, t, 4, const_cast<void*>(in), dims, strides, lower, upper, 64, (cuuint32_t)pixels, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// bs_conv2d on the SP24 layout: K5 with its X atoms loaded by TMA in im2col mode (as bsk_launch_conv for K6).
+cudaError_t bsk_launch_conv24(const bsk::Geom& g, const void* packed, const void* in, int64_t Nimg, int64_t H, int64_t W,
+                              int64_t C, int kh, int kw, int pad, const void* bias, int act, void* Y, cudaStream_t s) {
+  if (g.layout != BS_LAYOUT_SP24 || g.es != 2 || g.K % KCH != 0) return cudaErrorNotSupported;
+  if (C % 64 != 0 || g.K != (int64_t)kh * kw * C || ((uintptr_t)in & 15) != 0) return cudaErrorNotSupported;
+  if (pad > 127 || kh > 128 || kw > 128) return cudaErrorNotSupported;
+  const int64_t OH = H + 2 * pad - kh + 1, OW = W + 2 * pad - kw + 1;
+  if (OH < 1 || OW < 1) return cudaErrorNotSupported;
+  const int64_t N = Nimg * OH * OW;
+  if (N >= (1LL << 31)) return cudaErrorNotSupported;
+  const Conv24 cv{Nimg, H, W, C, kh, kw, pad};
+  return g.dt == BS_BF16 ? launch_tc24<BS_BF16>(g, packed, in, N, g.K, Y, g.M, s, bias, act, &cv)
+                         : launch_tc24<BS_F16>(g, packed, in, N, g.K, Y, g.M, s, bias, act, &cv);
 }
 
 // Y = act(W·X + bias) on the sparse tensor cores (bs_spmm_fused, SP24 layout); NotSupported when the operands

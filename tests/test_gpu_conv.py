@@ -158,3 +158,27 @@ def test_conv2d_fused_bias_act(bs, act, dname):
         assert np.all(np.abs(got - want) <= 1e-2 * (bound + np.abs(b)[None, :]) + ulp * np.abs(want) + 1e-6)
     with pytest.raises(ValueError):
         bs.conv2d(A, xi.cuda(), 3, 3, pad=1, bias=bias.cuda(), act=act, implicit=False)
+
+
+@pytest.mark.parametrize("Nimg,H,W,C,Cout,kh,kw,pad", [
+    (1, 8, 8, 128, 256, 3, 3, 1),    # K5 single-CTA kernel with split-K
+    (2, 5, 5, 64, 9728, 2, 2, 0),    # >= 75 row tiles: K5 CTA pairs (each CTA loads its half of the pixel column)
+])
+def test_conv2d_implicit_im2col_sp24(bs, Nimg, H, W, C, Cout, kh, kw, pad):
+    """bs_conv2d on the 2:4 layout (K5 with TMA im2col loads of each 64-channel atom): bit-identical to
+    bs_im2col + bs_spmm, and with bias + ReLU exact against the oracle on integer-exact data."""
+    Kc = kh * kw * C
+    Wm = synth.matrix(Cout, Kc, "f16", family="intexact", seed=synth.seed_for(55, Cout))
+    vals, idx, _ = bs.prune(Wm.cuda(), 4, k=2)
+    A = bs.pack(vals, idx, Kc, 4, layout="sp24")
+    xi = _img(Nimg, H, W, C, "f16", synth.seed_for(55, 2), family="intexact")
+    Yi = bs.conv2d(A, xi.cuda(), kh, kw, pad=pad, implicit=True)
+    Ye = bs.conv2d(A, xi.cuda(), kh, kw, pad=pad, implicit=False)
+    assert torch.equal(Yi, Ye)
+    bias = synth.vector(Cout, "f16", family="intexact", seed=synth.seed_for(55, 3))
+    Y = bs.conv2d(A, xi.cuda(), kh, kw, pad=pad, bias=bias.cuda(), act="relu")
+    ov, oi = oracle.prune(synth.to_numpy(Wm), oracle.F16, 4, 2)
+    ref, _ = oracle.conv2d(ov, oi, oracle.F16, Cout, 4, 2, synth.to_numpy(xi), kh, kw, pad, 1)
+    b = oracle.to_double(synth.to_numpy(bias), oracle.F16)
+    np.testing.assert_array_equal(oracle.to_double(synth.to_numpy(Y), oracle.F16).reshape(ref.shape),
+                                  np.maximum(ref + b[None, :], 0.0))
