@@ -129,6 +129,17 @@ def test_conv2d_implicit_errors(bs):
         bs.conv2d(bs.pack(v, i, 9 * 32, 32, layout="spmm"), inp, 3, 3, pad=1, implicit=True)
     Y = bs.conv2d(bs.pack(v, i, 9 * 32, 32, layout="spmm"), inp, 3, 3, pad=1)  # auto: falls back to im2col
     assert Y.shape == (1, 6, 6, 64)
+    W2 = synth.matrix(64, 9 * 64, "f16", seed=7).cuda()
+    v2, i2, _ = bs.prune(W2, 32, k=3)
+    A2 = bs.pack(v2, i2, 9 * 64, 32, layout="spmm")
+    x2 = _img(1, 8, 8, 64, "f16", 8).cuda()
+    with pytest.raises(bs.BSError):   # stride 2: only the explicit path
+        bs.conv2d(A2, x2, 3, 3, pad=1, stride=2, implicit=True)
+    assert bs.conv2d(A2, x2, 3, 3, pad=1, stride=2).shape == (1, 4, 4, 64)
+    with pytest.raises(ValueError):   # bias of the wrong length
+        bs.conv2d(A2, x2, 3, 3, pad=1, bias=torch.zeros(63, dtype=torch.float16, device="cuda"))
+    with pytest.raises(ValueError):   # unknown activation
+        bs.conv2d(A2, x2, 3, 3, pad=1, act="gelu")
 
 
 @pytest.mark.parametrize("act,dname", [("relu", "f16"), ("tanh", "bf16"), ("sigmoid", "f16")])
